@@ -1,0 +1,510 @@
+/*
+ * epg_oracle.c -- plain, slow, obviously-correct CPU oracle for the edge-partition
+ * (EP) hot path of arXiv 1605.02043, "A Graph-based Model for GPU Caching Problems".
+ *
+ * TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library. It shares no code,
+ * header, table or helper with the CUDA path (paper_1605_02043_b200/), and neither
+ * includes the other.
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n; "O<k>" = SURVEY.md §8(c) item,
+ * "Z<k>" = SURVEY.md §8(c) reading (restated in DESIGN.md "Readings").
+ * Every routine follows the definition or algorithm step by step, in the paper's
+ * notation; no blocking, fusion or reordering. Floating point is fp64 (the paper does
+ * not fix the precision); fp32 inputs are promoted on read.
+ *
+ * Status codes: 0 ok, 2 input error, 3 infeasible configuration.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <math.h>
+
+#define ORC_OK 0
+#define ORC_ERR_INPUT 2
+#define ORC_ERR_INFEASIBLE 3
+#define ORC_MAX_PART 4096
+#define INF64 INT64_MAX
+
+/* ------------------------------------------------------------------------- */
+/* O1. Conventions: k = ceil(m/P); s_i = floor(m/k) + [i < m mod k]            */
+/* Eq. (1), "L_i(x) = m/k", read as exact +-1 balance (Z2).              */
+/* ------------------------------------------------------------------------- */
+int64_t orc_num_parts(int64_t m, int32_t P) {
+    if (m <= 0 || P <= 0) return 0;
+    return (m + P - 1) / P;
+}
+
+void orc_part_sizes(int64_t m, int64_t k, int64_t *s) {
+    for (int64_t i = 0; i < k; i++) s[i] = m / k + (i < m % k ? 1 : 0);
+}
+
+/* first edge with an endpoint outside [0, n), or -1 (Def. 1) */
+int64_t orc_first_bad_edge(const int32_t *edges, int64_t m, int32_t n) {
+    for (int64_t e = 0; e < m; e++)
+        if (edges[2 * e] < 0 || edges[2 * e] >= n || edges[2 * e + 1] < 0 || edges[2 * e + 1] >= n) return e;
+    return -1;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O2. Cost function, Def. 2 / Eq. (1) and fig:mot.    */
+/*   V_p = {u_e, v_e : part[e] = p};  L = sum_p |V_p|  ("one load is for      */
+/*   every distinct particle");  p_v = #clusters touching v;         */
+/*   touched = #{v : deg v >= 1};  C = sum_v (p_v - 1) over touched v.        */
+/* rep[0..5] = k, L, touched, C, max_size, min_size.                         */
+/* ------------------------------------------------------------------------- */
+typedef struct { int64_t a, b; } pair64;
+
+static int cmp_pair64(const void *x, const void *y) {
+    const pair64 *p = (const pair64 *)x, *q = (const pair64 *)y;
+    if (p->a != q->a) return p->a < q->a ? -1 : 1;
+    if (p->b != q->b) return p->b < q->b ? -1 : 1;
+    return 0;
+}
+
+int orc_cost(const int32_t *edges, int64_t m, int32_t n, const int32_t *part, int64_t k,
+             int64_t *per_part, int64_t *rep) {
+    if (m <= 0 || n <= 0 || k <= 0) return ORC_ERR_INPUT;
+    if (orc_first_bad_edge(edges, m, n) >= 0) return ORC_ERR_INPUT;
+    for (int64_t e = 0; e < m; e++) if (part[e] < 0 || part[e] >= k) return ORC_ERR_INPUT;
+
+    /* all (partition, vertex) incidences; distinct pairs are the loads */
+    pair64 *pv = (pair64 *)malloc(sizeof(pair64) * 2 * m);
+    for (int64_t e = 0; e < m; e++)
+        for (int s = 0; s < 2; s++) { pv[2 * e + s].a = part[e]; pv[2 * e + s].b = edges[2 * e + s]; }
+    qsort(pv, 2 * m, sizeof(pair64), cmp_pair64);
+    if (per_part) for (int64_t p = 0; p < k; p++) per_part[p] = 0;
+    int64_t L = 0;
+    int64_t *p_v = (int64_t *)calloc(n, sizeof(int64_t));
+    for (int64_t i = 0; i < 2 * m; i++) {
+        if (i > 0 && pv[i].a == pv[i - 1].a && pv[i].b == pv[i - 1].b) continue;
+        L++;
+        if (per_part) per_part[pv[i].a]++;
+        p_v[pv[i].b]++;
+    }
+    /* C = sum over touched v of (p_v - 1), evaluated vertex by vertex (Eq. 1) */
+    int64_t touched = 0, C = 0;
+    for (int32_t v = 0; v < n; v++) if (p_v[v] >= 1) { touched++; C += p_v[v] - 1; }
+    /* partition sizes L_i (edges per cluster) */
+    int64_t *size = (int64_t *)calloc(k, sizeof(int64_t));
+    for (int64_t e = 0; e < m; e++) size[part[e]]++;
+    int64_t mx = 0, mn = INF64;
+    for (int64_t p = 0; p < k; p++) { if (size[p] > mx) mx = size[p]; if (size[p] < mn) mn = size[p]; }
+    rep[0] = k; rep[1] = L; rep[2] = touched; rep[3] = C; rep[4] = mx; rep[5] = mn;
+    free(pv); free(p_v); free(size);
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O3. Default task schedule ("default task scheduling"): task e */
+/* goes to the i-th contiguous chunk of sizes s_i.                           */
+/* ------------------------------------------------------------------------- */
+int orc_default_partition(int64_t m, int32_t P, int32_t *part) {
+    if (m <= 0) return ORC_ERR_INPUT;
+    if (P < 1 || P > ORC_MAX_PART) return ORC_ERR_INFEASIBLE;
+    int64_t k = orc_num_parts(m, P);
+    int64_t *s = (int64_t *)malloc(sizeof(int64_t) * k);
+    orc_part_sizes(m, k, s);
+    int64_t e = 0;
+    for (int64_t i = 0; i < k; i++)
+        for (int64_t j = 0; j < s[i]; j++) part[e++] = (int32_t)i;
+    free(s);
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O4. Clone-and-connect, contracted (Def. 3; "very large weight"  */
+/* on original edges; chain "in index order").                 */
+/* Every clone lies on exactly one original edge and original    */
+/* edges are never cut, so each original edge with its two clones contracts  */
+/* to one task node. Vertex v's clones are chained in ascending (e, s) order;*/
+/* the chain edge between consecutive clones (e_j,s_j),(e_j+1,s_j+1) becomes  */
+/* a T-edge {e_j, e_j+1} of weight 1 unless e_j = e_j+1 (a self-loop's two   */
+/* clones, contracted into one node). Parallel T-edges sum their weights.    */
+/* Output: CSR over tasks, neighbours ascending. Capacity needed <= 4m.      */
+/* ------------------------------------------------------------------------- */
+typedef struct { int32_t v; int64_t e; int s; } slot_t;
+
+static int cmp_slot(const void *x, const void *y) {
+    const slot_t *p = (const slot_t *)x, *q = (const slot_t *)y;
+    if (p->v != q->v) return p->v < q->v ? -1 : 1;
+    if (p->e != q->e) return p->e < q->e ? -1 : 1;
+    return p->s - q->s;
+}
+
+int orc_build_T(const int32_t *edges, int64_t m, int32_t n, int64_t *t_ptr, int32_t *t_adj,
+                int32_t *t_w, int64_t cap, int64_t *nnz_out) {
+    if (m <= 0 || n <= 0) return ORC_ERR_INPUT;
+    if (orc_first_bad_edge(edges, m, n) >= 0) return ORC_ERR_INPUT;
+    slot_t *sl = (slot_t *)malloc(sizeof(slot_t) * 2 * m);
+    for (int64_t e = 0; e < m; e++)
+        for (int s = 0; s < 2; s++) { sl[2 * e + s].v = edges[2 * e + s]; sl[2 * e + s].e = e; sl[2 * e + s].s = s; }
+    qsort(sl, 2 * m, sizeof(slot_t), cmp_slot);
+    /* directed T-edge list (both directions), weight 1 each */
+    pair64 *te = (pair64 *)malloc(sizeof(pair64) * 4 * m);
+    int64_t nte = 0;
+    for (int64_t i = 0; i + 1 < 2 * m; i++) {
+        if (sl[i].v != sl[i + 1].v) continue;              /* chain is per vertex   */
+        if (sl[i].e == sl[i + 1].e) continue;              /* self-loop: contracted */
+        te[nte].a = sl[i].e; te[nte].b = sl[i + 1].e; nte++;
+        te[nte].a = sl[i + 1].e; te[nte].b = sl[i].e; nte++;
+    }
+    qsort(te, nte, sizeof(pair64), cmp_pair64);
+    for (int64_t t = 0; t <= m; t++) t_ptr[t] = 0;
+    int64_t nnz = 0;
+    for (int64_t i = 0; i < nte; i++) {
+        if (i > 0 && te[i].a == te[i - 1].a && te[i].b == te[i - 1].b) { t_w[nnz - 1] += 1; continue; }
+        if (nnz >= cap) { free(sl); free(te); return ORC_ERR_INPUT; }
+        t_adj[nnz] = (int32_t)te[i].b; t_w[nnz] = 1; nnz++;
+        t_ptr[te[i].a + 1]++;
+    }
+    for (int64_t t = 0; t < m; t++) t_ptr[t + 1] += t_ptr[t];
+    *nnz_out = nnz;
+    free(sl); free(te);
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O5. EPG-1: balanced growing on T (the role METIS plays in P:384;   */
+/* Z3). For partition i = 0..nparts-1:                                       */
+/*  1. seed = unassigned task with the smallest global stamp gst if any has  */
+/*     one, else the smallest-id unassigned task;                            */
+/*  2. reset local state: g = 0, lst = INF for all tasks, c = 0;             */
+/*     lst[seed] = c++;                                                      */
+/*  3. repeat s_i times:                                                     */
+/*     - if no unassigned task has finite lst, the smallest-id unassigned    */
+/*       task gets lst = c++ (restart on a disconnected remainder);          */
+/*     - pick the unassigned task with finite lst maximising g, ties by the  */
+/*       smallest lst; part[t] = i;                                          */
+/*     - for each T-neighbour (nb, w) of t, ascending nb, with part[nb] = -1:*/
+/*       if lst[nb] = INF then lst[nb] = c++; g[nb] += w;                    */
+/*       if gst[nb] = INF then gst[nb] = G++ (G never reset).                */
+/* The pick is a plain linear scan over the tasks stamped in this partition */
+/* ("finite lst" = stamped since the reset).                                */
+/* ------------------------------------------------------------------------- */
+int orc_epg1(int64_t ntask, const int64_t *t_ptr, const int32_t *t_adj, const int32_t *t_w,
+             const int64_t *sizes, int64_t nparts, int32_t *part) {
+    int64_t total = 0;
+    for (int64_t i = 0; i < nparts; i++) total += sizes[i];
+    if (total != ntask) return ORC_ERR_INPUT;
+    int64_t *gst = (int64_t *)malloc(sizeof(int64_t) * ntask);
+    int64_t *lst = (int64_t *)malloc(sizeof(int64_t) * ntask);
+    int64_t *g = (int64_t *)malloc(sizeof(int64_t) * ntask);
+    int64_t *gst_order = (int64_t *)malloc(sizeof(int64_t) * (ntask + 1));  /* tasks by gst */
+    int64_t *stamped = (int64_t *)malloc(sizeof(int64_t) * (ntask + 1));
+    for (int64_t t = 0; t < ntask; t++) { part[t] = -1; gst[t] = INF64; lst[t] = INF64; g[t] = 0; }
+    int64_t G = 0, n_gst = 0, gptr = 0, idptr = 0, nst = 0;
+
+    for (int64_t i = 0; i < nparts; i++) {
+        /* 1. seed */
+        while (gptr < n_gst && part[gst_order[gptr]] != -1) gptr++;
+        int64_t seed;
+        if (gptr < n_gst) seed = gst_order[gptr];
+        else {
+            while (idptr < ntask && part[idptr] != -1) idptr++;
+            seed = idptr;
+        }
+        /* 2. reset local state (only stamped tasks differ from the reset value) */
+        for (int64_t j = 0; j < nst; j++) { lst[stamped[j]] = INF64; g[stamped[j]] = 0; }
+        nst = 0;
+        int64_t c = 0;
+        if (sizes[i] == 0) continue;
+        lst[seed] = c++; stamped[nst++] = seed;
+        /* 3. grow */
+        for (int64_t r = 0; r < sizes[i]; r++) {
+            int64_t best = -1;
+            for (int64_t j = 0; j < nst; j++) {
+                int64_t t = stamped[j];
+                if (part[t] != -1) continue;
+                if (best < 0 || g[t] > g[best] || (g[t] == g[best] && lst[t] < lst[best])) best = t;
+            }
+            if (best < 0) {
+                while (idptr < ntask && part[idptr] != -1) idptr++;
+                best = idptr;
+                lst[best] = c++; stamped[nst++] = best;
+            }
+            part[best] = (int32_t)i;
+            for (int64_t q = t_ptr[best]; q < t_ptr[best + 1]; q++) {
+                int64_t nb = t_adj[q];
+                if (part[nb] != -1) continue;
+                if (lst[nb] == INF64) { lst[nb] = c++; stamped[nst++] = nb; }
+                g[nb] += t_w[q];
+                if (gst[nb] == INF64) { gst[nb] = G++; gst_order[n_gst++] = nb; }
+            }
+        }
+    }
+    free(gst); free(lst); free(g); free(gst_order); free(stamped);
+    return ORC_OK;
+}
+
+/* Flat (shards = 1) or hierarchical (shards = G > 1) EPG-1 (O5):
+ *  shard g receives partitions [floor(gk/G), floor((g+1)k/G)) and target size the
+ *  sum of their s_i; EPG-1 on T with those G sizes gives shard[t]; then, for g
+ *  ascending, EPG-1 on T restricted to shard g (tasks renumbered by ascending id)
+ *  with its slice of s_i, partition ids offset by floor(gk/G).                   */
+int orc_partition(const int32_t *edges, int64_t m, int32_t n, int32_t P, int32_t shards, int32_t *part) {
+    if (m <= 0 || n <= 0) return ORC_ERR_INPUT;
+    if (orc_first_bad_edge(edges, m, n) >= 0) return ORC_ERR_INPUT;
+    if (P < 1 || P > ORC_MAX_PART) return ORC_ERR_INFEASIBLE;
+    int64_t k = orc_num_parts(m, P);
+    if (!(shards == 1 || shards == 2 || shards == 4 || shards == 8) || shards > k) return ORC_ERR_INFEASIBLE;
+
+    int64_t *t_ptr = (int64_t *)malloc(sizeof(int64_t) * (m + 1));
+    int32_t *t_adj = (int32_t *)malloc(sizeof(int32_t) * 4 * m);
+    int32_t *t_w = (int32_t *)malloc(sizeof(int32_t) * 4 * m);
+    int64_t nnz = 0;
+    int st = orc_build_T(edges, m, n, t_ptr, t_adj, t_w, 4 * m, &nnz);
+    if (st) { free(t_ptr); free(t_adj); free(t_w); return st; }
+    int64_t *s = (int64_t *)malloc(sizeof(int64_t) * k);
+    orc_part_sizes(m, k, s);
+
+    if (shards == 1) {
+        st = orc_epg1(m, t_ptr, t_adj, t_w, s, k, part);
+    } else {
+        int64_t Gs = shards;
+        int64_t *ssize = (int64_t *)calloc(Gs, sizeof(int64_t));
+        for (int64_t gi = 0; gi < Gs; gi++)
+            for (int64_t i = gi * k / Gs; i < (gi + 1) * k / Gs; i++) ssize[gi] += s[i];
+        int32_t *shard = (int32_t *)malloc(sizeof(int32_t) * m);
+        st = orc_epg1(m, t_ptr, t_adj, t_w, ssize, Gs, shard);
+        int64_t *loc = (int64_t *)malloc(sizeof(int64_t) * m);   /* task -> id inside its shard */
+        int64_t *glob = (int64_t *)malloc(sizeof(int64_t) * m);  /* local id -> task           */
+        int64_t *sp = (int64_t *)malloc(sizeof(int64_t) * (m + 1));
+        int32_t *sa = (int32_t *)malloc(sizeof(int32_t) * (nnz > 0 ? nnz : 1));
+        int32_t *sw = (int32_t *)malloc(sizeof(int32_t) * (nnz > 0 ? nnz : 1));
+        int32_t *sub = (int32_t *)malloc(sizeof(int32_t) * m);
+        for (int64_t gi = 0; gi < Gs && st == ORC_OK; gi++) {
+            int64_t mg = 0;
+            for (int64_t t = 0; t < m; t++) if (shard[t] == gi) { loc[t] = mg; glob[mg] = t; mg++; }
+            /* induced subgraph of T on shard gi; ascending ids keep neighbours ascending */
+            int64_t q2 = 0;
+            sp[0] = 0;
+            for (int64_t j = 0; j < mg; j++) {
+                int64_t t = glob[j];
+                for (int64_t q = t_ptr[t]; q < t_ptr[t + 1]; q++)
+                    if (shard[t_adj[q]] == gi) { sa[q2] = (int32_t)loc[t_adj[q]]; sw[q2] = t_w[q]; q2++; }
+                sp[j + 1] = q2;
+            }
+            int64_t p0 = gi * k / Gs, p1 = (gi + 1) * k / Gs;
+            st = orc_epg1(mg, sp, sa, sw, s + p0, p1 - p0, sub);
+            for (int64_t j = 0; j < mg; j++) part[glob[j]] = (int32_t)(sub[j] + p0);
+        }
+        free(ssize); free(shard); free(loc); free(glob); free(sp); free(sa); free(sw); free(sub);
+    }
+    free(t_ptr); free(t_adj); free(t_w); free(s);
+    return st;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O6. Remap: task reorganisation + cpack data layout*/
+/*  1. new edge order = sort by (part, original id) -> edge_perm (new->old), */
+/*     part_edge_begin;                                                      */
+/*  2. key(v) = min over endpoint slots of (2 e' + s), e' new edge index;    */
+/*  3. new vertex id: ascending (key, v) over touched vertices, untouched    */
+/*     appended in ascending id -> vertex_perm (old->new);                   */
+/*  4. part_vertex_begin[p] = #{v : key(v) < 2 part_edge_begin[p]} ("beginA")*/
+/*  5. O_p = [pvb[p], pvb[p+1]); H_p = V_p \ O_p ascending (all < pvb[p]);   */
+/*  6. slot of v in p: v - pvb[p] if v in O_p, else |O_p| + rank of v in H_p;*/
+/*  7. halo_ids = concatenation of H_p, halo_begin its offsets.              */
+/* Untouched vertices get pvb-free ids >= touched.                           */
+/* ------------------------------------------------------------------------- */
+static int cmp_i64(const void *x, const void *y) {
+    int64_t a = *(const int64_t *)x, b = *(const int64_t *)y;
+    return a < b ? -1 : (a > b ? 1 : 0);
+}
+
+int orc_remap(const int32_t *edges, int64_t m, int32_t n, const int32_t *part, int64_t k,
+              int32_t *edge_perm, int32_t *part_edge_begin, int32_t *vertex_perm, int32_t *part_vertex_begin,
+              int32_t *halo_begin, int32_t *halo_ids, int64_t halo_cap, uint16_t *slots) {
+    if (m <= 0 || n <= 0 || k <= 0) return ORC_ERR_INPUT;
+    if (orc_first_bad_edge(edges, m, n) >= 0) return ORC_ERR_INPUT;
+    for (int64_t e = 0; e < m; e++) if (part[e] < 0 || part[e] >= k) return ORC_ERR_INPUT;
+    /* 1. sort by (part, id) */
+    pair64 *pe = (pair64 *)malloc(sizeof(pair64) * m);
+    for (int64_t e = 0; e < m; e++) { pe[e].a = part[e]; pe[e].b = e; }
+    qsort(pe, m, sizeof(pair64), cmp_pair64);
+    for (int64_t i = 0; i < m; i++) edge_perm[i] = (int32_t)pe[i].b;
+    for (int64_t p = 0; p <= k; p++) part_edge_begin[p] = 0;
+    for (int64_t e = 0; e < m; e++) part_edge_begin[part[e] + 1]++;
+    for (int64_t p = 0; p < k; p++) part_edge_begin[p + 1] += part_edge_begin[p];
+    /* 2. first-touch keys */
+    int64_t *key = (int64_t *)malloc(sizeof(int64_t) * n);
+    for (int32_t v = 0; v < n; v++) key[v] = INF64;
+    for (int64_t i = 0; i < m; i++)
+        for (int s = 0; s < 2; s++) {
+            int32_t v = edges[2 * (int64_t)edge_perm[i] + s];
+            if (2 * i + s < key[v]) key[v] = 2 * i + s;
+        }
+    /* 3. ascending (key, v) over touched, then untouched by id */
+    pair64 *kv = (pair64 *)malloc(sizeof(pair64) * n);
+    int64_t nt = 0;
+    for (int32_t v = 0; v < n; v++) if (key[v] != INF64) { kv[nt].a = key[v]; kv[nt].b = v; nt++; }
+    qsort(kv, nt, sizeof(pair64), cmp_pair64);
+    for (int64_t j = 0; j < nt; j++) vertex_perm[kv[j].b] = (int32_t)j;
+    int64_t nxt = nt;
+    for (int32_t v = 0; v < n; v++) if (key[v] == INF64) vertex_perm[v] = (int32_t)nxt++;
+    /* 4. beginA */
+    for (int64_t p = 0; p <= k; p++) {
+        int64_t cnt = 0;
+        int64_t lim = 2 * (int64_t)part_edge_begin[p];
+        for (int32_t v = 0; v < n; v++) if (key[v] != INF64 && key[v] < lim) cnt++;
+        part_vertex_begin[p] = (int32_t)cnt;
+    }
+    /* 5-7. halo lists and local slots, partition by partition */
+    int64_t hpos = 0;
+    int64_t *vp = (int64_t *)malloc(sizeof(int64_t) * 2 * (m > 0 ? m : 1));
+    int st = ORC_OK;
+    for (int64_t p = 0; p < k; p++) {
+        halo_begin[p] = (int32_t)hpos;
+        int64_t e0 = part_edge_begin[p], e1 = part_edge_begin[p + 1], nv = 0;
+        for (int64_t i = e0; i < e1; i++)
+            for (int s = 0; s < 2; s++) vp[nv++] = vertex_perm[edges[2 * (int64_t)edge_perm[i] + s]];
+        qsort(vp, nv, sizeof(int64_t), cmp_i64);
+        int64_t h0 = hpos;
+        for (int64_t j = 0; j < nv; j++) {
+            if (j > 0 && vp[j] == vp[j - 1]) continue;
+            if (vp[j] < part_vertex_begin[p]) {
+                if (hpos >= halo_cap) { st = ORC_ERR_INPUT; goto done; }
+                halo_ids[hpos++] = (int32_t)vp[j];
+            }
+        }
+        int64_t own0 = part_vertex_begin[p], nown = part_vertex_begin[p + 1] - part_vertex_begin[p];
+        for (int64_t i = e0; i < e1; i++)
+            for (int s = 0; s < 2; s++) {
+                int64_t v = vertex_perm[edges[2 * (int64_t)edge_perm[i] + s]];
+                int64_t slot;
+                if (v >= own0 && v < own0 + nown) slot = v - own0;
+                else {
+                    int64_t r = 0;
+                    while (halo_ids[h0 + r] != v) r++;          /* rank of v in H_p */
+                    slot = nown + r;
+                }
+                slots[2 * i + s] = (uint16_t)slot;
+            }
+    }
+    halo_begin[k] = (int32_t)hpos;
+done:
+    free(pe); free(key); free(kv); free(vp);
+    return st;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O7. Multi-GPU ownership and halos (build design; the paper is single-GPU).*/
+/*  Shard g holds partitions [floor(gk/G), floor((g+1)k/G)); its owned range */
+/*  is [pvb[p_begin(g)], pvb[p_end(g)]). Halo^g = (U_{p in g} V_p) \ owned_g */
+/*  ascending; Halo^{g<-g'} = Halo^g intersect owned_{g'}.                    */
+/*  Output: begin[(g*G + g')] .. begin[(g*G+g')+1] slices of ids (new ids),  */
+/*  ordered by toucher g, then owner g', then id.                            */
+/* ------------------------------------------------------------------------- */
+int orc_shard_halos(const int32_t *edges, int64_t m, int32_t n, const int32_t *part, int64_t k, int32_t G,
+                    const int32_t *vertex_perm, const int32_t *part_vertex_begin,
+                    int32_t *shard_halo_begin, int32_t *ids, int64_t cap) {
+    if (G < 1 || G > k) return ORC_ERR_INFEASIBLE;
+    unsigned char *mark = (unsigned char *)malloc(n);
+    int64_t pos = 0;
+    for (int32_t g = 0; g < G; g++) {
+        int64_t pb = (int64_t)g * k / G, pe = (int64_t)(g + 1) * k / G;
+        memset(mark, 0, n);
+        for (int64_t e = 0; e < m; e++)
+            if (part[e] >= pb && part[e] < pe)
+                for (int s = 0; s < 2; s++) mark[vertex_perm[edges[2 * e + s]]] = 1;
+        for (int32_t g2 = 0; g2 < G; g2++) {
+            shard_halo_begin[g * G + g2] = (int32_t)pos;
+            if (g2 == g) continue;
+            int64_t lo = part_vertex_begin[(int64_t)g2 * k / G], hi = part_vertex_begin[(int64_t)(g2 + 1) * k / G];
+            for (int64_t v = lo; v < hi; v++)
+                if (mark[v]) { if (pos >= cap) { free(mark); return ORC_ERR_INPUT; } ids[pos++] = (int32_t)v; }
+        }
+    }
+    shard_halo_begin[G * G] = (int32_t)pos;
+    free(mark);
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O8/O9. Edge functors and the time step, fp64.                              */
+/* The paper gives no cfd formula (its pseudo-code is in \iffalse,  */
+/* P:207-231). Reading Z9: Rodinia Euler3D-style face flux,      */
+/* gamma = 1.4, sigma = 0.2, forward Euler U' = U + dt_v F_v.                */
+/*  per vertex: u = m/rho; p = (gamma-1)(E - rho|u|^2/2); c = sqrt(gamma p/rho)*/
+/*    G_rho = m; G_m = m u^T + p I (rows x,y,z); G_E = u (E + p)             */
+/*  per edge (a,b), area-normal n out of a:                                  */
+/*    f = -|n| sigma (|u_a| + |u_b| + c_a + c_b) / 2                         */
+/*    Phi = f (U_a - U_b) - n . (G_a + G_b) / 2       (5 components)         */
+/*    F_a += Phi;  F_b -= Phi                                                */
+/*  U'_v = U_v + dt_v F_v for touched v; untouched v unchanged.              */
+/* ------------------------------------------------------------------------- */
+#define ORC_GAMMA 1.4
+#define ORC_SIGMA 0.2
+
+static void cfd_vertex(const float *U5, double *Uv, double *u, double *p, double *c, double *speed) {
+    for (int j = 0; j < 5; j++) Uv[j] = (double)U5[j];
+    double rho = Uv[0];
+    u[0] = Uv[1] / rho; u[1] = Uv[2] / rho; u[2] = Uv[3] / rho;
+    double uu = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+    *p = (ORC_GAMMA - 1.0) * (Uv[4] - 0.5 * rho * uu);
+    *c = sqrt(ORC_GAMMA * (*p) / rho);
+    *speed = sqrt(uu);
+}
+
+/* physical flux through a face with normal n: Gn[j] = n . G_j(U) */
+static void cfd_flux_dot(const double *Uv, const double *u, double p, const double *n, double *Gn) {
+    double un = u[0] * n[0] + u[1] * n[1] + u[2] * n[2];
+    Gn[0] = Uv[1] * n[0] + Uv[2] * n[1] + Uv[3] * n[2];     /* m . n           */
+    Gn[1] = Uv[1] * un + p * n[0];                          /* (m_x u + p e_x).n */
+    Gn[2] = Uv[2] * un + p * n[1];
+    Gn[3] = Uv[3] * un + p * n[2];
+    Gn[4] = (Uv[4] + p) * un;                               /* (E + p) u . n   */
+}
+
+void orc_cfd_flux(const int32_t *edges, int64_t m, int32_t n, const float *normals, const float *U, double *F) {
+    for (int64_t v = 0; v < (int64_t)n * 5; v++) F[v] = 0.0;
+    for (int64_t e = 0; e < m; e++) {
+        int32_t a = edges[2 * e], b = edges[2 * e + 1];
+        double nv[3] = {normals[3 * e], normals[3 * e + 1], normals[3 * e + 2]};
+        double Ua[5], Ub[5], ua[3], ub[3], pa, pb, ca, cb, sa, sb, Ga[5], Gb[5];
+        cfd_vertex(U + 5 * (int64_t)a, Ua, ua, &pa, &ca, &sa);
+        cfd_vertex(U + 5 * (int64_t)b, Ub, ub, &pb, &cb, &sb);
+        cfd_flux_dot(Ua, ua, pa, nv, Ga);
+        cfd_flux_dot(Ub, ub, pb, nv, Gb);
+        double nlen = sqrt(nv[0] * nv[0] + nv[1] * nv[1] + nv[2] * nv[2]);
+        double f = -nlen * ORC_SIGMA * 0.5 * (sa + sb + ca + cb);
+        for (int j = 0; j < 5; j++) {
+            double phi = f * (Ua[j] - Ub[j]) - 0.5 * (Ga[j] + Gb[j]);
+            F[5 * (int64_t)a + j] += phi;
+            F[5 * (int64_t)b + j] -= phi;
+        }
+    }
+}
+
+void orc_cfd_step(const int32_t *edges, int64_t m, int32_t n, const float *normals, const float *U,
+                  const float *dt, double *Uout, double *F) {
+    orc_cfd_flux(edges, m, n, normals, U, F);
+    unsigned char *touched = (unsigned char *)calloc(n, 1);
+    for (int64_t e = 0; e < m; e++) { touched[edges[2 * e]] = 1; touched[edges[2 * e + 1]] = 1; }
+    for (int64_t v = 0; v < n; v++)
+        for (int j = 0; j < 5; j++)
+            Uout[5 * v + j] = (double)U[5 * v + j] + (touched[v] ? (double)dt[v] * F[5 * v + j] : 0.0);
+    free(touched);
+}
+
+/* GATHER_SCATTER (config C4): y_a += w_e x_b, y_b += w_e x_a (w = 1 if NULL).  */
+void orc_gather_scatter(const int32_t *edges, int64_t m, int32_t n, const float *w, const float *x, double *y) {
+    for (int64_t v = 0; v < n; v++) y[v] = 0.0;
+    for (int64_t e = 0; e < m; e++) {
+        int32_t a = edges[2 * e], b = edges[2 * e + 1];
+        double we = w ? (double)w[e] : 1.0;
+        y[a] += we * (double)x[b];
+        y[b] += we * (double)x[a];
+    }
+}
+
+/* SPMV (config C5) on the bipartite data-affinity graph: edge e =  */
+/* (column vertex j, row vertex i) for nonzero A[i,j] = w_e; y_i += A[i,j] x_j. */
+void orc_spmv(const int32_t *edges, int64_t m, int32_t n, const float *w, const float *x, double *y) {
+    for (int64_t v = 0; v < n; v++) y[v] = 0.0;
+    for (int64_t e = 0; e < m; e++) {
+        int32_t j = edges[2 * e], i = edges[2 * e + 1];
+        y[i] += (double)w[e] * (double)x[j];
+    }
+}

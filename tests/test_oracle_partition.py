@@ -1,0 +1,197 @@
+"""Pins for clone-and-connect T (O4, Def. 3) and EPG-1 (O5, P:384/P:418 role)."""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth as S
+from bruteforce import loads_and_cut, optimum, t_cut, balanced_maps
+from conftest import golden
+
+
+def _T_undirected_weight(T):
+    t_ptr, t_adj, t_w = T
+    return int(t_w.sum()) // 2
+
+
+def test_T_star_and_two_triangle():
+    # K_{1,3}: 3 original edges, the centre's 3 clones chained by 2 aux edges
+    e = np.array([[0, 1], [0, 2], [0, 3]], np.int32)
+    t_ptr, t_adj, t_w = O.build_T(e, 4)
+    assert t_ptr.tolist() == [0, 1, 3, 4]
+    assert t_adj.tolist() == [1, 0, 2, 1] and t_w.tolist() == [1, 1, 1, 1]
+    # two-triangle: 6 aux edges
+    g = golden("two_triangle.json")
+    assert _T_undirected_weight(O.build_T(np.array(g["edges"], np.int32), 6)) == 6
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_T_structure(seed):
+    rng = np.random.default_rng(100 + seed)
+    m, n = int(rng.integers(1, 40)), int(rng.integers(1, 20))
+    n, e = S.random_multigraph(seed, m, n)
+    T = O.build_T(e, n)
+    t_ptr, t_adj, t_w = T
+    # neighbours strictly ascending, no self edges, symmetric weights
+    W = {}
+    for t in range(m):
+        nb = t_adj[t_ptr[t]:t_ptr[t + 1]]
+        assert np.all(np.diff(nb) > 0) and np.all(nb != t)
+        for q in range(t_ptr[t], t_ptr[t + 1]):
+            W[(t, int(t_adj[q]))] = int(t_w[q])
+    assert all(W[(b, a)] == w for (a, b), w in W.items())
+    # total aux weight = sum_v (d_v - 1) minus contracted self-loop links
+    touched = len(set(e.ravel().tolist()))
+    loops = int(np.sum(e[:, 0] == e[:, 1]))
+    assert _T_undirected_weight(T) == 2 * m - touched - loops
+
+
+@pytest.mark.parametrize("seed", range(25))
+def test_theorem1_every_map(seed):
+    """Theorem 1: cut_w(T)(x) >= C(x) for EVERY edge map x; equality when
+    max degree <= 2 (each vertex has at most one chain edge)."""
+    rng = np.random.default_rng(200 + seed)
+    m, n = int(rng.integers(2, 9)), int(rng.integers(2, 8))
+    n, e = S.random_multigraph(1000 + seed, m, n)
+    T = O.build_T(e, n)
+    deg = np.bincount(e.ravel(), minlength=n)
+    for k in (2, 3):
+        for x in balanced_maps(list(O.part_sizes(m, k))) if m >= k else []:
+            _, c = loads_and_cut(e, x)
+            tc = t_cut(*T, x)
+            assert tc >= c
+            if deg.max() <= 2:
+                assert tc == c
+
+
+def test_theorem1_equality_cycles_paths():
+    for m in (5, 9, 12):
+        for n, e in (S.path_graph(m), S.cycle_graph(m)):
+            T = O.build_T(e, n)
+            rng = np.random.default_rng(m)
+            for _ in range(20):
+                x = rng.integers(0, 3, m)
+                assert t_cut(*T, x) == loads_and_cut(e, x)[1]
+
+
+def test_epg1_fig_mot_and_two_triangle():
+    g = golden("fig_mot.json")
+    e = np.array(g["topologies"]["star_plus_triangle"], np.int32)
+    part = O.partition(e, 6, 3)
+    assert part.tolist() == g["schedule_b"]                      # hand-traced: e1 -> e2 -> e4
+    assert O.cost(e, 6, part, 2).load_count == g["loads_b"]      # P:74, 7 loads
+    g2 = golden("two_triangle.json")
+    e2 = np.array(g2["edges"], np.int32)
+    part = O.partition(e2, 6, 3)
+    assert part.tolist() == g2["optimal_partition"]
+    assert O.cost(e2, 6, part, 2).cut_cost == 0
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_epg1_invariants(seed):
+    rng = np.random.default_rng(300 + seed)
+    m = int(rng.integers(1, 500))
+    n = int(rng.integers(1, 200))
+    n, e = S.random_multigraph(seed, m, n)
+    P = int(rng.integers(1, 70))
+    k = O.num_parts(m, P)
+    part = O.partition(e, n, P)
+    sizes = np.bincount(part, minlength=k)
+    assert sizes.tolist() == O.part_sizes(m, k).tolist()          # exact +-1 balance (Z2)
+    assert np.array_equal(part, O.partition(e, n, P))             # deterministic
+
+
+def test_epg1_vs_bruteforce_and_theorem2():
+    """C(EPG-1) >= C* always; Theorem 2 bracket C* <= T-cut* <= (d_max - 1) C*
+    (P:520-570). The equality rate is a regression guard only: 122/289 = 42% on this
+    corpus when first recorded (SURVEY's scratch corpus, with a different graph mix,
+    reported 62%)."""
+    hits = total = 0
+    for seed in range(120):
+        rng = np.random.default_rng(400 + seed)
+        m = int(rng.integers(4, 9))
+        n = int(rng.integers(3, 8))
+        n, e = S.random_multigraph(5000 + seed, m, n)
+        for k in (2, 3, 4):
+            if k > m:
+                continue
+            P = -(-m // k)
+            if O.num_parts(m, P) != k:
+                continue
+            sizes = list(O.part_sizes(m, k))
+            T = O.build_T(e, n)
+            c_star, t_star = optimum(e, sizes, T)
+            dmax = int(np.bincount(e.ravel()).max())
+            assert c_star <= t_star <= max(dmax - 1, 1) * c_star or (c_star == 0 and t_star == 0)
+            part = O.partition(e, n, P)
+            _, c = loads_and_cut(e, part)
+            assert c >= c_star
+            hits += c == c_star
+            total += 1
+    assert total > 150
+    assert hits / total >= 0.40
+
+
+def test_theorem2_star_with_pendants():
+    """SPEC S:437's instance: K_{1,3} with each leaf extended by a pendant edge (m = 6,
+    d_max = 3), k = 2. SPEC quotes the bracket [1, 2] assuming C* = 1, but C* = 2 by hand:
+    the hub is cut unless all three hub edges share a cluster (then leaves 1,2,3 are
+    cut, C = 3); otherwise the cluster holding two hub edges has room for only one of
+    their two pendants, so one more leaf is cut. Theorem 2 then brackets
+    the VP optimum in [C*, (d_max-1) C*] = [2, 4]."""
+    e = np.array([[0, 1], [0, 2], [0, 3], [1, 4], [2, 5], [3, 6]], np.int32)
+    c_star, t_star = optimum(e, [3, 3], O.build_T(e, 7))
+    assert c_star == 2 and 2 <= t_star <= 4
+
+
+def test_equal_cycles_zero_cost():
+    """Appendix: k equal cycles split with zero communication; task order
+    interleaved so that the default schedule is bad."""
+    g = golden("appendix_cycles.json")
+    L = g["cycle_length"]
+    for k in g["k_values"]:
+        cyc = [S.cycle_graph(L, offset=L * j)[1] for j in range(k)]
+        e = np.stack([cyc[j][i] for i in range(L) for j in range(k)]).astype(np.int32)
+        c_star, _ = optimum(e, [L] * k)
+        assert c_star == g["expected_C_star"]
+        part = O.partition(e, L * k, L)
+        assert loads_and_cut(e, part)[1] == 0
+        assert loads_and_cut(e, O.default_partition(L * k, L))[1] > 0
+
+
+def test_path_cycle_presets():
+    for m, k in [(12, 3), (12, 2), (40, 4)]:
+        n, e = S.path_graph(m)
+        assert O.cost(e, n, O.partition(e, n, m // k), k).cut_cost == k - 1
+        n, e = S.cycle_graph(m)
+        assert O.cost(e, n, O.partition(e, n, m // k), k).cut_cost == k
+
+
+def test_hierarchical(small_mesh):
+    M = small_mesh
+    P = 256
+    k = O.num_parts(M.m, P)
+    flat = O.partition(M.edges, M.n, P, 1)
+    T = O.build_T(M.edges, M.n)
+    assert np.array_equal(flat, O.epg1(*T, O.part_sizes(M.m, k)))
+    s = O.part_sizes(M.m, k)
+    for G in (2, 4, 8):
+        part = O.partition(M.edges, M.n, P, G)
+        assert np.bincount(part, minlength=k).tolist() == s.tolist()
+        # shard-level map = EPG-1 on T with the G shard sizes
+        ssz = [int(s[g * k // G:(g + 1) * k // G].sum()) for g in range(G)]
+        shard = O.epg1(*T, ssz)
+        for g in range(G):
+            sel = shard == g
+            assert np.all((part[sel] >= g * k // G) & (part[sel] < (g + 1) * k // G))
+        r = O.cost(M.edges, M.n, part, k)
+        assert r.replication < 1.8
+
+
+def test_epg1_quality_on_cfd_mesh(mesh_c1):
+    """EP beats the default schedule by >= 2x in vertex loads at P = 1024."""
+    M = mesh_c1
+    k = O.num_parts(M.m, 1024)
+    r_ep = O.cost(M.edges, M.n, O.partition(M.edges, M.n, 1024), k)
+    r_def = O.cost(M.edges, M.n, O.default_partition(M.m, 1024), k)
+    assert r_ep.max_size - r_ep.min_size <= 1 and r_ep.balance_factor < 1.03
+    assert r_def.replication / r_ep.replication > 2.0
