@@ -1,0 +1,216 @@
+/*
+ * epg.h -- C ABI of libepg.so: the edge-partition (EP) scheduled irregular kernel of
+ * arXiv 1605.02043, "A Graph-based Model for GPU Caching Problems", on B200 (sm_100a).
+ *
+ * Citations: "P:n" = PAPER.md line n (section / equation named beside it);
+ * "S:n" = SPEC.md line n; "O<k>"/"Z<k>" = SURVEY.md §8(c) items, restated in DESIGN.md.
+ *
+ * The calls follow the paper's problem statement: "partition all m edges
+ * evenly into k clusters ... every edge (task) is assigned to exactly one cluster
+ * (thread block)", then "reorganize tasks among thread blocks ... and data layout"
+ * (P:751-757), then run the transformed kernel:
+ *
+ *   epg_partition  -> edge -> partition map + load count      (§3, Eq. (1), Def. 3-4)
+ *   epg_load_count -> the cost function on any map            (Eq. (1); fig:mot P:68-74)
+ *   epg_remap      -> reordered edges + cpack vertex layout   (opt_indexA,
+ *                     + the run plan                            opt_arrayA, beginA)
+ *   epg_run        -> one or more time steps of the staged edge kernel
+ *
+ * Conventions (all calls):
+ *  - ids are int32, counts int64, little-endian. Vertex ids in [0, n). The input edge
+ *    order is the task id. Self-loops and parallel edges are distinct tasks
+ *    (S:78-79); isolated vertices cost nothing.
+ *  - Ownership: the caller owns every array passed in or out and allocates outputs
+ *    (sizes are m, n, k+1, or come from an earlier report). The library never frees
+ *    caller memory. The ctx owns its stream handle reference, scratch workspace and
+ *    error string; an epg_plan owns the device descriptors its kernels read.
+ *  - Memory spaces are stated per argument: "device" = CUDA device memory of the
+ *    ctx's device; "host" = host memory; "host or device" = either (detected with
+ *    cudaPointerGetAttributes).
+ *  - Streams: work is enqueued on the ctx stream. Calls that fill an epg_report
+ *    (epg_partition, epg_load_count) synchronise that stream before returning; all
+ *    others are asynchronous.
+ *  - Threads: one ctx per host thread; a ctx is not thread-safe.
+ *  - Errors: every call returns an epg_status; the message of the last failure is
+ *    epg_last_error(ctx). On error no output is guaranteed to be written.
+ *      EPG_ERR_INPUT      m <= 0, n <= 0, an endpoint outside [0, n) (the message
+ *                         names the first offending edge id), a partition id outside
+ *                         [0, k), a too-small output capacity, NULL required pointer.
+ *      EPG_ERR_INFEASIBLE part_size outside [1, 4096]; shards not in {1,2,4,8} or
+ *                         shards > k; a partition whose staged rows exceed shared memory.
+ *      EPG_ERR_CUDA       a CUDA runtime error (message carries cudaGetErrorString).
+ *      EPG_ERR_NOMEM      device allocation failed.
+ *      EPG_ERR_STATE      ctx/plan mismatch (wrong device, plan from another ctx).
+ */
+#ifndef EPG_H
+#define EPG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    EPG_OK = 0,
+    EPG_ERR_INPUT = 2,
+    EPG_ERR_INFEASIBLE = 3,
+    EPG_ERR_CUDA = 4,
+    EPG_ERR_NCCL = 5,
+    EPG_ERR_NOMEM = 6,
+    EPG_ERR_STATE = 7
+} epg_status;
+
+#define EPG_MAX_PART_SIZE 4096
+
+typedef struct epg_ctx epg_ctx;
+typedef struct epg_plan epg_plan;
+
+/* Cost report, Eq. (1) with the load accounting of fig:mot:
+ *   k          number of partitions (thread blocks);
+ *   load_count L = sum_p |V_p|, V_p = distinct endpoints of partition p
+ *              ("one load is for every distinct particle");
+ *   touched    #vertices with degree >= 1;
+ *   cut_cost   C = sum_v (p_v - 1) = L - touched (the redundant loads);
+ *   max_size / min_size  largest / smallest partition, in edges (balance). */
+typedef struct {
+    int64_t k, load_count, touched, cut_cost, max_size, min_size;
+} epg_report;
+
+/* Remapped layout (O6). Every array is DEVICE memory,
+ * caller-allocated with the stated sizes. The staged kernel does not read these
+ * arrays (the plan keeps its own copies), so they may be freed after epg_remap.
+ *   edge_perm         [m]   new edge index -> original task id (edges sorted by
+ *                           (partition, task id); the paper's reorganised tasks)
+ *   part_edge_begin   [k+1] first new edge index of each partition
+ *   vertex_perm       [n]   original vertex id -> new id (cpack first-touch order;
+ *                           untouched vertices appended by id)  -- opt_arrayA's map
+ *   part_vertex_begin [k+1] first owned new vertex id of each partition ("beginA");
+ *                           partition p owns O_p = [pvb[p], pvb[p+1])
+ *   halo_begin        [k+1] offsets into halo_ids
+ *   halo_ids          [halo_cap] concatenated H_p = V_p \ O_p, ascending; the total
+ *                           is C, so halo_cap >= cut_cost from epg_load_count
+ *   slots             [m][2] uint16 local slot of each endpoint within its partition:
+ *                           v - pvb[p] if owned, else |O_p| + rank of v in H_p
+ *                           ("opt_indexA") */
+typedef struct {
+    int32_t *edge_perm;
+    int32_t *part_edge_begin;
+    int32_t *vertex_perm;
+    int32_t *part_vertex_begin;
+    int32_t *halo_begin;
+    int32_t *halo_ids;
+    int64_t halo_cap;
+    uint16_t *slots;
+} epg_layout;
+
+/* Edge functors (O9; reading Z9). Row layouts are AoS float32.
+ *  EPG_KERNEL_CFD_FLUX       state rows (rho, m_x, m_y, m_z, E) [n][5]; edge payload
+ *                            area-normal [m][3] oriented edges[e][0] -> edges[e][1];
+ *                            vertex_const dt [n]. Output U' = U + dt F (untouched
+ *                            vertices copied). Face flux of P:62-64's "interaction
+ *                            between two adjacent particles" (Rodinia-style, Z9).
+ *  EPG_KERNEL_GATHER_SCATTER state x [n]; payload weight w [m] or NULL (w = 1);
+ *                            output y [n], y_a += w x_b, y_b += w x_a.
+ *  EPG_KERNEL_SPMV           bipartite graph of P:859-861: edge e = (column vertex j,
+ *                            row vertex i), payload A[i,j] [m]; output y [n],
+ *                            y_i += A[i,j] x_j (y = 0 at column vertices).          */
+typedef enum {
+    EPG_KERNEL_CFD_FLUX = 1,
+    EPG_KERNEL_GATHER_SCATTER = 2,
+    EPG_KERNEL_SPMV = 3
+} epg_kernel;
+
+/* Arguments of a time step. All DEVICE pointers in the layout the call expects:
+ * epg_run: rows in the plan's NEW vertex order and payload in NEW edge order
+ * (use epg_permute_rows); epg_run_naive: original orders.
+ * state_in and state_out must not alias. With steps > 1 the two buffers ping-pong:
+ * step s (1-based) reads the buffer written by step s-1, so the final result is in
+ * state_out when steps is odd and in state_in when steps is even (state_in is then
+ * overwritten, so it must be writable). */
+typedef struct {
+    void *state_in;
+    void *state_out;
+    const void *edge_payload;
+    const void *vertex_const;
+} epg_state;
+
+/* -- context ------------------------------------------------------------------ */
+/* Create a context on CUDA device `device`, enqueuing on `cuda_stream` (a
+ * cudaStream_t; NULL = the legacy default stream). */
+epg_status epg_create(int device, void *cuda_stream, epg_ctx **out);
+void epg_destroy(epg_ctx *ctx);
+/* Message of the last failed call on ctx (ctx-owned, valid until the next call). */
+const char *epg_last_error(const epg_ctx *ctx);
+/* k = ceil(m / part_size) (O1); 0 if m <= 0 or part_size <= 0. */
+int64_t epg_num_parts(int64_t m, int32_t part_size);
+
+/* -- partition (step a2 + a3) ------------------------------------------------- */
+/* Host-only EPG-1 partition (no device needed): the balanced growing partitioner on
+ * the contracted clone-and-connect graph T (Def. 3, weight P:377, chain
+ * order P:380; EPG-1 replaces METIS P:384/P:418, reading Z3). Partition sizes are
+ * s_i = floor(m/k) + [i < m mod k] (Eq. (1) "L_i = m/k", exact +-1, Z2).
+ * shards = G > 1 runs the hierarchical variant (shard-level EPG-1, then per shard).
+ *   edges [m][2] HOST; part_of_edge [m] HOST out.
+ * Returns EPG_ERR_INPUT / EPG_ERR_INFEASIBLE as above; writes the message into
+ * errbuf (errbuf_len bytes, may be NULL). */
+epg_status epg_partition_host(const int32_t *edges, int64_t m, int32_t n_vertices, int32_t part_size,
+                              int32_t shards, int32_t *part_of_edge, char *errbuf, int64_t errbuf_len);
+
+/* epg_partition_host, then the GPU cost function on the result (epg_load_count).
+ *   edges [m][2] host or device; part_of_edge [m] host or device out; out report. */
+epg_status epg_partition(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n_vertices, int32_t part_size,
+                         int32_t shards, int32_t *part_of_edge, epg_report *out);
+
+/* Default task schedule (O3; "default task scheduling" P:75): task e goes to
+ * the i-th contiguous chunk of sizes s_i.  part_of_edge [m] DEVICE out. */
+epg_status epg_default_partition(epg_ctx *ctx, int64_t m, int32_t part_size, int32_t *part_of_edge);
+
+/* GPU cost function (step a3; Eq. (1), fig:mot P:68-74). Any map with
+ * part ids in [0, k).  edges [m][2] DEVICE; part_of_edge [m] DEVICE;
+ * per_part_distinct [k] DEVICE out (|V_p|) or NULL; out report (host). Synchronises. */
+epg_status epg_load_count(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n_vertices,
+                          const int32_t *part_of_edge, int64_t k, int32_t *per_part_distinct, epg_report *out);
+
+/* -- remap (step a4) ---------------------------------------------------------- */
+/* Task reorganisation + cpack layout on the GPU (O6). Fills `layout` (device arrays,
+ * see epg_layout) and creates *plan: the device descriptors of the staged kernel
+ * (per-partition incidence lists, shared-vertex lists, accumulators). Requires every
+ * partition to have at most EPG_MAX_PART_SIZE edges.
+ *   edges [m][2] DEVICE (original task order); part_of_edge [m] DEVICE. */
+epg_status epg_remap(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n_vertices,
+                     const int32_t *part_of_edge, int64_t k, epg_layout *layout, epg_plan **plan);
+void epg_plan_destroy(epg_plan *plan);
+/* Sizes of a plan: out[0..5] = m, n, k, touched, cut_cost (= |halo_ids|),
+ * shared vertex count (vertices with p_v > 1). */
+epg_status epg_plan_info(const epg_plan *plan, int64_t *out6);
+
+/* Row permutation (step a7 and the layout change of a4), DEVICE arrays:
+ *   mode 0 (gather):  dst[i]       = src[perm[i]]   for i < rows
+ *   mode 1 (scatter): dst[perm[i]] = src[i]         for i < rows
+ * vertex rows into the new layout: scatter with vertex_perm; back to the original
+ * layout: gather with vertex_perm; edge payload into the new order: gather with
+ * edge_perm. row_bytes must be a multiple of 4. */
+epg_status epg_permute_rows(epg_ctx *ctx, const void *src, void *dst, int64_t rows, int32_t row_bytes,
+                            const int32_t *perm, int32_t mode);
+
+/* -- run (steps a5 + a6) ------------------------------------------------------ */
+/* `steps` time steps of the partition-scheduled kernel: one CTA per
+ * partition stages V_p (owned rows O_p contiguous, halo rows H_p gathered) into
+ * shared memory, evaluates the functor per edge from shared memory, reduces each
+ * vertex's incident contributions in shared memory and writes interior vertices'
+ * results directly; vertices shared by several partitions (p_v > 1) are completed
+ * by a boundary-finalise pass. Deterministic: the summation order is fixed. */
+epg_status epg_run(epg_ctx *ctx, const epg_plan *plan, epg_kernel kernel, epg_state *state, int32_t steps);
+
+/* The default (unscheduled) comparator: the same functor with one thread per task
+ * in original order, operands read straight from global memory and results
+ * accumulated with global atomics, then a per-vertex update (the original kernel of
+ * P:75 / P:1009 that the paper's schedule replaces).  edges [m][2] DEVICE. */
+epg_status epg_run_naive(epg_ctx *ctx, epg_kernel kernel, const int32_t *edges, int64_t m, int32_t n_vertices,
+                         epg_state *state, int32_t steps);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EPG_H */

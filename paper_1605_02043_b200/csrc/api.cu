@@ -1,0 +1,653 @@
+// api.cu -- the C ABI of libepg.so (include/epg.h): context, plans, and the host-side
+// orchestration of the cost, remap and run kernels.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "epg_internal.h"
+#include "layout_kernels.cuh"
+#include "run_kernels.cuh"
+
+struct epg_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    float *naive_F = nullptr;
+    size_t naive_F_bytes = 0;
+    epg_status fail(epg_status s, const std::string &msg) {
+        err = msg;
+        return s;
+    }
+};
+
+struct epg_plan {
+    epg_ctx *ctx = nullptr;
+    int device = 0;
+    int64_t m = 0, n = 0, k = 0, touched = 0, C = 0, S = 0;
+    int Lcap = 0, Scap = 0;
+    int32_t *peb = nullptr, *pvb = nullptr, *hb = nullptr, *halo_ids = nullptr, *sidx = nullptr;
+    int32_t *shared_ids = nullptr, *hv_off = nullptr, *hv_list = nullptr;
+    uint32_t *slots = nullptr;
+    uint16_t *inc = nullptr, *inc_off = nullptr;
+    float *owner_buf = nullptr, *halo_buf = nullptr;
+    std::vector<void *> allocs;
+    ~epg_plan() {
+        for (void *p : allocs) cudaFree(p);
+    }
+};
+
+namespace {
+
+using namespace epg;
+
+constexpr int kThreads = 256;
+
+inline unsigned grid_for(int64_t work, int threads = kThreads) {
+    return (unsigned)std::max<int64_t>(1, (work + threads - 1) / threads);
+}
+
+inline int bits_for(int64_t maxval) {  // bits needed for values in [0, maxval]
+    int b = 1;
+    while (b < 31 && (int64_t(1) << b) <= maxval) b++;
+    return b;
+}
+
+#define CU(call)                                                                                        \
+    do {                                                                                                \
+        cudaError_t _e = (call);                                                                        \
+        if (_e != cudaSuccess) return ctx->fail(EPG_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+#define CHECK_LAUNCH() CU(cudaGetLastError())
+
+// stream-ordered temporary device buffer
+struct Tmp {
+    epg_ctx *ctx;
+    void *p = nullptr;
+    explicit Tmp(epg_ctx *c) : ctx(c) {}
+    ~Tmp() {
+        if (p) cudaFreeAsync(p, ctx->stream);
+    }
+    cudaError_t alloc(size_t bytes) { return cudaMallocAsync(&p, std::max<size_t>(bytes, 16), ctx->stream); }
+    template <class T> T *as() { return static_cast<T *>(p); }
+};
+
+bool is_device_ptr(const void *p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+template <class T>
+__global__ void k_fill(T *a, int64_t len, T v) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < len) a[i] = v;
+}
+
+epg_status plan_alloc(epg_plan *pl, epg_ctx *ctx, void **out, size_t bytes) {
+    *out = nullptr;
+    cudaError_t e = cudaMalloc(out, std::max<size_t>(bytes, 16));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return ctx->fail(EPG_ERR_NOMEM, std::string("cudaMalloc(plan): ") + cudaGetErrorString(e));
+    }
+    pl->allocs.push_back(*out);
+    return EPG_OK;
+}
+
+template <class T>
+epg_status plan_alloc_t(epg_plan *pl, epg_ctx *ctx, T **out, int64_t count) {
+    void *p;
+    epg_status s = plan_alloc(pl, ctx, &p, sizeof(T) * (size_t)std::max<int64_t>(count, 1));
+    *out = static_cast<T *>(p);
+    return s;
+}
+
+// validate endpoints and (optionally) partition ids on the device
+epg_status validate(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, const int32_t *part, int64_t k) {
+    Tmp bad(ctx);
+    CU(bad.alloc(2 * sizeof(unsigned long long)));
+    k_fill<unsigned long long><<<1, 2, 0, ctx->stream>>>(bad.as<unsigned long long>(), 2, ULLONG_MAX);
+    k_validate<<<grid_for(m), kThreads, 0, ctx->stream>>>(edges, part, m, n, k, bad.as<unsigned long long>(),
+                                                          bad.as<unsigned long long>() + 1);
+    CHECK_LAUNCH();
+    unsigned long long h[2];
+    CU(cudaMemcpyAsync(h, bad.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (h[0] != ULLONG_MAX)
+        return ctx->fail(EPG_ERR_INPUT, "edge " + std::to_string(h[0]) + " has an endpoint outside [0, n)");
+    if (h[1] != ULLONG_MAX)
+        return ctx->fail(EPG_ERR_INPUT, "edge " + std::to_string(h[1]) + " has a partition id outside [0, k)");
+    return EPG_OK;
+}
+
+// stable sort of task ids by partition -> edge_perm (new -> old), part_edge_begin
+epg_status group_by_part(epg_ctx *ctx, const int32_t *part, int64_t m, int64_t k, int32_t *edge_perm, int32_t *peb,
+                         std::vector<int32_t> *peb_host) {
+    Tmp iota(ctx), keys_out(ctx), temp(ctx);
+    CU(iota.alloc(sizeof(int32_t) * m));
+    CU(keys_out.alloc(sizeof(int32_t) * m));
+    k_iota<<<grid_for(m), kThreads, 0, ctx->stream>>>(iota.as<int32_t>(), m);
+    size_t tb = 0;
+    const int kb = bits_for(k);
+    CU(cub::DeviceRadixSort::SortPairs(nullptr, tb, part, keys_out.as<int32_t>(), iota.as<int32_t>(), edge_perm,
+                                       (int)m, 0, kb, ctx->stream));
+    CU(temp.alloc(tb));
+    CU(cub::DeviceRadixSort::SortPairs(temp.p, tb, part, keys_out.as<int32_t>(), iota.as<int32_t>(), edge_perm,
+                                       (int)m, 0, kb, ctx->stream));
+    k_part_begin<<<grid_for(k + 1), kThreads, 0, ctx->stream>>>(keys_out.as<int32_t>(), m, k, peb);
+    CHECK_LAUNCH();
+    peb_host->resize(k + 1);
+    CU(cudaMemcpyAsync(peb_host->data(), peb, sizeof(int32_t) * (k + 1), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return EPG_OK;
+}
+
+template <int BLOCK, int ITEMS>
+size_t distinct_smem() {
+    using Sort = cub::BlockRadixSort<int, BLOCK, ITEMS>;
+    using Disc = cub::BlockDiscontinuity<int, BLOCK>;
+    using Red = cub::BlockReduce<int, BLOCK>;
+    union TS {
+        typename Sort::TempStorage sort;
+        typename Disc::TempStorage disc;
+        typename Red::TempStorage red;
+    };
+    return sizeof(TS);
+}
+
+template <int BLOCK, int ITEMS>
+size_t remap_smem() {
+    using Sort = cub::BlockRadixSort<int, BLOCK, ITEMS, int>;
+    using Disc = cub::BlockDiscontinuity<int, BLOCK>;
+    using Scan = cub::BlockScan<int, BLOCK>;
+    union TS {
+        typename Sort::TempStorage sort;
+        typename Disc::TempStorage disc;
+        typename Scan::TempStorage scan;
+    };
+    return sizeof(TS);
+}
+
+template <int BLOCK, int ITEMS>
+epg_status launch_distinct(epg_ctx *ctx, const int32_t *edges, const int32_t *edge_perm, const int32_t *peb,
+                           int64_t k, int32_t *per_part, int end_bit) {
+    const size_t sm = distinct_smem<BLOCK, ITEMS>();
+    CU(cudaFuncSetAttribute(k_distinct<BLOCK, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_distinct<BLOCK, ITEMS><<<(unsigned)k, BLOCK, sm, ctx->stream>>>(edges, edge_perm, peb, per_part, end_bit);
+    CHECK_LAUNCH();
+    return EPG_OK;
+}
+
+// |V_p| for every partition; edges grouped by edge_perm / peb
+epg_status distinct_counts(epg_ctx *ctx, const int32_t *edges, const int32_t *part, int64_t m, int32_t n,
+                           const int32_t *edge_perm, const int32_t *peb, int64_t k, int64_t smax, int32_t *per_part) {
+    const int eb = bits_for(n);
+    if (2 * smax <= 512) return launch_distinct<256, 2>(ctx, edges, edge_perm, peb, k, per_part, eb);
+    if (2 * smax <= 2048) return launch_distinct<256, 8>(ctx, edges, edge_perm, peb, k, per_part, eb);
+    if (2 * smax <= 8192) return launch_distinct<512, 16>(ctx, edges, edge_perm, peb, k, per_part, eb);
+    // large partitions: global sort of (partition, vertex) keys
+    Tmp keys(ctx), sorted(ctx), temp(ctx);
+    CU(keys.alloc(sizeof(unsigned long long) * 2 * m));
+    CU(sorted.alloc(sizeof(unsigned long long) * 2 * m));
+    k_pv_keys<<<grid_for(2 * m), kThreads, 0, ctx->stream>>>(edges, part, m, keys.as<unsigned long long>());
+    size_t tb = 0;
+    CU(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys.as<unsigned long long>(), sorted.as<unsigned long long>(),
+                                      (int)(2 * m), 0, 32 + bits_for(k), ctx->stream));
+    CU(temp.alloc(tb));
+    CU(cub::DeviceRadixSort::SortKeys(temp.p, tb, keys.as<unsigned long long>(), sorted.as<unsigned long long>(),
+                                      (int)(2 * m), 0, 32 + bits_for(k), ctx->stream));
+    CU(cudaMemsetAsync(per_part, 0, sizeof(int32_t) * k, ctx->stream));
+    k_distinct_global<<<grid_for(2 * m), kThreads, 0, ctx->stream>>>(sorted.as<unsigned long long>(), 2 * m, per_part);
+    CHECK_LAUNCH();
+    return EPG_OK;
+}
+
+epg_status sum_i32(epg_ctx *ctx, const int32_t *a, int64_t len, int64_t *out) {
+    Tmp acc(ctx);
+    CU(acc.alloc(sizeof(unsigned long long)));
+    CU(cudaMemsetAsync(acc.p, 0, sizeof(unsigned long long), ctx->stream));
+    k_sum<<<(unsigned)std::min<int64_t>(1184, std::max<int64_t>(1, (len + 255) / 256)), 256, 0, ctx->stream>>>(
+        a, len, acc.as<unsigned long long>());
+    CHECK_LAUNCH();
+    unsigned long long h = 0;
+    CU(cudaMemcpyAsync(&h, acc.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    *out = (int64_t)h;
+    return EPG_OK;
+}
+
+epg_status exclusive_scan(epg_ctx *ctx, const int32_t *in, int32_t *out, int64_t len) {
+    Tmp temp(ctx);
+    size_t tb = 0;
+    CU(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, (int)len, ctx->stream));
+    CU(temp.alloc(tb));
+    CU(cub::DeviceScan::ExclusiveSum(temp.p, tb, in, out, (int)len, ctx->stream));
+    return EPG_OK;
+}
+
+epg_status read_i32(epg_ctx *ctx, const int32_t *dev, int32_t *host) {
+    CU(cudaMemcpyAsync(host, dev, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return EPG_OK;
+}
+
+// cost function on device edges / part: report + optional per-partition counts
+epg_status load_count_dev(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, const int32_t *part, int64_t k,
+                          int32_t *per_part_out, epg_report *rep) {
+    epg_status st = validate(ctx, edges, m, n, part, k);
+    if (st) return st;
+    Tmp perm(ctx), peb(ctx), distinct(ctx), flag(ctx);
+    CU(perm.alloc(sizeof(int32_t) * m));
+    CU(peb.alloc(sizeof(int32_t) * (k + 1)));
+    std::vector<int32_t> peb_h;
+    st = group_by_part(ctx, part, m, k, perm.as<int32_t>(), peb.as<int32_t>(), &peb_h);
+    if (st) return st;
+    int64_t smax = 0, smin = INT64_MAX;
+    for (int64_t p = 0; p < k; p++) {
+        smax = std::max<int64_t>(smax, peb_h[p + 1] - peb_h[p]);
+        smin = std::min<int64_t>(smin, peb_h[p + 1] - peb_h[p]);
+    }
+    int32_t *pp = per_part_out;
+    if (!pp) {
+        CU(distinct.alloc(sizeof(int32_t) * k));
+        pp = distinct.as<int32_t>();
+    }
+    st = distinct_counts(ctx, edges, part, m, n, perm.as<int32_t>(), peb.as<int32_t>(), k, smax, pp);
+    if (st) return st;
+    CU(flag.alloc(sizeof(int32_t) * n));
+    CU(cudaMemsetAsync(flag.p, 0, sizeof(int32_t) * n, ctx->stream));
+    k_mark_touched<<<grid_for(2 * m), kThreads, 0, ctx->stream>>>(edges, m, flag.as<int32_t>());
+    CHECK_LAUNCH();
+    int64_t touched = 0, L = 0;
+    if ((st = sum_i32(ctx, flag.as<int32_t>(), n, &touched))) return st;
+    if ((st = sum_i32(ctx, pp, k, &L))) return st;
+    rep->k = k;
+    rep->load_count = L;
+    rep->touched = touched;
+    rep->cut_cost = L - touched;
+    rep->max_size = smax;
+    rep->min_size = smin;
+    return EPG_OK;
+}
+
+template <int BLOCK, int ITEMS>
+epg_status launch_remap_part(epg_ctx *ctx, const int32_t *edges, const int32_t *edge_perm,
+                             const int32_t *vertex_perm, const int32_t *peb, const int32_t *pvb, const int32_t *hb,
+                             int32_t *halo_ids, uint16_t *slots, uint16_t *inc, uint16_t *inc_off, int64_t k,
+                             int end_bit) {
+    const size_t sm = remap_smem<BLOCK, ITEMS>();
+    CU(cudaFuncSetAttribute(k_remap_part<BLOCK, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_remap_part<BLOCK, ITEMS><<<(unsigned)k, BLOCK, sm, ctx->stream>>>(edges, edge_perm, vertex_perm, peb, pvb, hb,
+                                                                        halo_ids, slots, inc, inc_off, end_bit);
+    CHECK_LAUNCH();
+    return EPG_OK;
+}
+
+template <class Fn>
+epg_status run_staged(epg_ctx *ctx, const epg_plan *pl, epg_state *state, int32_t steps) {
+    const size_t smem = sizeof(float) * ((size_t)Fn::NV * pl->Lcap + (size_t)Fn::NPHI * pl->Scap);
+    int dev_max = 0;
+    CU(cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+    if (smem > (size_t)dev_max)
+        return ctx->fail(EPG_ERR_INFEASIBLE, "run: a partition stages " + std::to_string(pl->Lcap) +
+                                                 " rows; shared memory needed " + std::to_string(smem) +
+                                                 " B exceeds " + std::to_string(dev_max) + " B");
+    CU(cudaFuncSetAttribute(k_edge_staged<Fn, kThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RunArgs a;
+    a.peb = pl->peb; a.pvb = pl->pvb; a.hb = pl->hb; a.halo_ids = pl->halo_ids; a.slots = pl->slots;
+    a.inc = pl->inc; a.inc_off = pl->inc_off; a.sidx = pl->sidx;
+    a.payload = static_cast<const float *>(state->edge_payload);
+    a.vconst = static_cast<const float *>(state->vertex_const);
+    a.owner_buf = pl->owner_buf; a.halo_buf = pl->halo_buf;
+    a.Lcap = pl->Lcap; a.Scap = pl->Scap;
+    float *bufs[2] = {static_cast<float *>(state->state_in), static_cast<float *>(state->state_out)};
+    const int64_t fin_work = pl->S + (pl->n - pl->touched);
+    for (int32_t s = 0; s < steps; s++) {
+        a.state_in = bufs[s & 1];
+        a.state_out = bufs[(s + 1) & 1];
+        k_edge_staged<Fn, kThreads><<<(unsigned)pl->k, kThreads, smem, ctx->stream>>>(a);
+        if (fin_work > 0)
+            k_finalise<Fn><<<grid_for(fin_work), kThreads, 0, ctx->stream>>>(
+                pl->shared_ids, pl->hv_off, pl->hv_list, pl->owner_buf, pl->halo_buf, a.state_in, a.state_out,
+                a.vconst, (int32_t)pl->S, pl->touched, pl->n);
+    }
+    CHECK_LAUNCH();
+    return EPG_OK;
+}
+
+template <class Fn>
+epg_status run_naive(epg_ctx *ctx, const int32_t *edges, int64_t m, int64_t n, epg_state *state, int32_t steps) {
+    const size_t need = sizeof(float) * Fn::ROW * (size_t)n;
+    if (ctx->naive_F_bytes < need) {
+        if (ctx->naive_F) cudaFree(ctx->naive_F);
+        ctx->naive_F = nullptr;
+        ctx->naive_F_bytes = 0;
+        cudaError_t e = cudaMalloc(&ctx->naive_F, need);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return ctx->fail(EPG_ERR_NOMEM, std::string("cudaMalloc(naive workspace): ") + cudaGetErrorString(e));
+        }
+        ctx->naive_F_bytes = need;
+        CU(cudaMemsetAsync(ctx->naive_F, 0, need, ctx->stream));
+    }
+    float *bufs[2] = {static_cast<float *>(state->state_in), static_cast<float *>(state->state_out)};
+    const float *payload = static_cast<const float *>(state->edge_payload);
+    const float *vc = static_cast<const float *>(state->vertex_const);
+    for (int32_t s = 0; s < steps; s++) {
+        k_naive_edges<Fn><<<grid_for(m), kThreads, 0, ctx->stream>>>(edges, m, bufs[s & 1], payload, ctx->naive_F);
+        k_naive_update<Fn><<<grid_for(n), kThreads, 0, ctx->stream>>>(n, bufs[s & 1], bufs[(s + 1) & 1], vc,
+                                                                        ctx->naive_F);
+    }
+    CHECK_LAUNCH();
+    return EPG_OK;
+}
+
+epg_status check_state(epg_ctx *ctx, epg_kernel kernel, const epg_state *state) {
+    if (!state || !state->state_in || !state->state_out)
+        return ctx->fail(EPG_ERR_INPUT, "run: state_in and state_out are required");
+    if (state->state_in == state->state_out) return ctx->fail(EPG_ERR_INPUT, "run: state_in and state_out alias");
+    if (kernel == EPG_KERNEL_CFD_FLUX && (!state->edge_payload || !state->vertex_const))
+        return ctx->fail(EPG_ERR_INPUT, "run: CFD_FLUX needs edge_payload (normals) and vertex_const (dt)");
+    if (kernel == EPG_KERNEL_SPMV && !state->edge_payload)
+        return ctx->fail(EPG_ERR_INPUT, "run: SPMV needs edge_payload (matrix values)");
+    if (kernel < EPG_KERNEL_CFD_FLUX || kernel > EPG_KERNEL_SPMV)
+        return ctx->fail(EPG_ERR_INPUT, "run: unknown kernel id");
+    return EPG_OK;
+}
+
+}  // namespace
+
+// =====================================================================================
+extern "C" {
+
+epg_status epg_create(int device, void *cuda_stream, epg_ctx **out) {
+    if (!out) return EPG_ERR_INPUT;
+    *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || device < 0 || device >= count) {
+        cudaGetLastError();
+        return EPG_ERR_CUDA;
+    }
+    if (cudaSetDevice(device) != cudaSuccess) return EPG_ERR_CUDA;
+    epg_ctx *c = new epg_ctx();
+    c->device = device;
+    c->stream = static_cast<cudaStream_t>(cuda_stream);
+    *out = c;
+    return EPG_OK;
+}
+
+void epg_destroy(epg_ctx *ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->naive_F) cudaFree(ctx->naive_F);
+    delete ctx;
+}
+
+const char *epg_last_error(const epg_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+epg_status epg_partition(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, int32_t part_size,
+                         int32_t shards, int32_t *part_of_edge, epg_report *out) {
+    if (!ctx) return EPG_ERR_STATE;
+    if (!edges || !part_of_edge || !out || m <= 0 || n <= 0)
+        return ctx->fail(EPG_ERR_INPUT, "partition: need m > 0, n > 0 and non-NULL arrays");
+    CU(cudaSetDevice(ctx->device));
+    const bool edges_dev = is_device_ptr(edges), part_dev = is_device_ptr(part_of_edge);
+    std::vector<int32_t> eh, ph(m);
+    const int32_t *edges_h = edges;
+    if (edges_dev) {
+        eh.resize(2 * m);
+        CU(cudaMemcpyAsync(eh.data(), edges, sizeof(int32_t) * 2 * m, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        edges_h = eh.data();
+    }
+    std::string err;
+    epg_status st = epg::host_partition(edges_h, m, n, part_size, shards, ph.data(), &err);
+    if (st) return ctx->fail(st, err);
+    Tmp ed(ctx), pd(ctx);
+    const int32_t *edges_d = edges;
+    if (!edges_dev) {
+        CU(ed.alloc(sizeof(int32_t) * 2 * m));
+        CU(cudaMemcpyAsync(ed.p, edges, sizeof(int32_t) * 2 * m, cudaMemcpyHostToDevice, ctx->stream));
+        edges_d = ed.as<int32_t>();
+    }
+    int32_t *part_d = part_of_edge;
+    if (!part_dev) {
+        std::memcpy(part_of_edge, ph.data(), sizeof(int32_t) * m);
+        CU(pd.alloc(sizeof(int32_t) * m));
+        part_d = pd.as<int32_t>();
+    }
+    CU(cudaMemcpyAsync(part_d, ph.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx->stream));
+    return load_count_dev(ctx, edges_d, m, n, part_d, epg_num_parts(m, part_size), nullptr, out);
+}
+
+epg_status epg_default_partition(epg_ctx *ctx, int64_t m, int32_t part_size, int32_t *part_of_edge) {
+    if (!ctx) return EPG_ERR_STATE;
+    if (m <= 0 || !part_of_edge) return ctx->fail(EPG_ERR_INPUT, "default_partition: need m > 0 and an output");
+    if (part_size < 1 || part_size > EPG_MAX_PART_SIZE)
+        return ctx->fail(EPG_ERR_INFEASIBLE, "default_partition: part_size must be in [1, 4096]");
+    CU(cudaSetDevice(ctx->device));
+    k_default_partition<<<grid_for(m), kThreads, 0, ctx->stream>>>(m, epg_num_parts(m, part_size), part_of_edge);
+    CHECK_LAUNCH();
+    return EPG_OK;
+}
+
+epg_status epg_load_count(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, const int32_t *part_of_edge,
+                          int64_t k, int32_t *per_part_distinct, epg_report *out) {
+    if (!ctx) return EPG_ERR_STATE;
+    if (!edges || !part_of_edge || !out || m <= 0 || n <= 0 || k <= 0)
+        return ctx->fail(EPG_ERR_INPUT, "load_count: need m > 0, n > 0, k > 0 and non-NULL arrays");
+    CU(cudaSetDevice(ctx->device));
+    return load_count_dev(ctx, edges, m, n, part_of_edge, k, per_part_distinct, out);
+}
+
+epg_status epg_remap(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, const int32_t *part, int64_t k,
+                     epg_layout *L, epg_plan **plan_out) {
+    if (!ctx) return EPG_ERR_STATE;
+    if (!edges || !part || !L || !plan_out || m <= 0 || n <= 0 || k <= 0)
+        return ctx->fail(EPG_ERR_INPUT, "remap: need m > 0, n > 0, k > 0 and non-NULL arrays");
+    if (!L->edge_perm || !L->part_edge_begin || !L->vertex_perm || !L->part_vertex_begin || !L->halo_begin ||
+        !L->slots || (!L->halo_ids && L->halo_cap > 0))
+        return ctx->fail(EPG_ERR_INPUT, "remap: every layout array is required");
+    *plan_out = nullptr;
+    CU(cudaSetDevice(ctx->device));
+    epg_status st = validate(ctx, edges, m, n, part, k);
+    if (st) return st;
+    // 1. task reorganisation: stable sort by partition
+    std::vector<int32_t> peb_h;
+    if ((st = group_by_part(ctx, part, m, k, L->edge_perm, L->part_edge_begin, &peb_h))) return st;
+    int64_t smax = 0;
+    for (int64_t p = 0; p < k; p++) smax = std::max<int64_t>(smax, peb_h[p + 1] - peb_h[p]);
+    if (smax > EPG_MAX_PART_SIZE)
+        return ctx->fail(EPG_ERR_INFEASIBLE, "remap: a partition has " + std::to_string(smax) +
+                                                 " edges; at most 4096 fit the uint16 slots");
+    Tmp distinct(ctx), key(ctx), flag(ctx), rank(ctx), uflag(ctx), urank(ctx), nh(ctx);
+    CU(distinct.alloc(sizeof(int32_t) * k));
+    if ((st = distinct_counts(ctx, edges, part, m, n, L->edge_perm, L->part_edge_begin, k, smax,
+                              distinct.as<int32_t>())))
+        return st;
+    // 2. first-touch keys; 3. ranks -> vertex_perm
+    CU(key.alloc(sizeof(int32_t) * n));
+    k_fill<int32_t><<<grid_for(n), kThreads, 0, ctx->stream>>>(key.as<int32_t>(), n, kSentinel);
+    k_first_touch<<<grid_for(m), kThreads, 0, ctx->stream>>>(edges, L->edge_perm, m, key.as<int32_t>());
+    CU(flag.alloc(sizeof(int32_t) * (2 * m + 1)));
+    CU(rank.alloc(sizeof(int32_t) * (2 * m + 1)));
+    k_first_touch_flags<<<grid_for(2 * m + 1), kThreads, 0, ctx->stream>>>(edges, L->edge_perm, m,
+                                                                          key.as<int32_t>(), flag.as<int32_t>());
+    CHECK_LAUNCH();
+    if ((st = exclusive_scan(ctx, flag.as<int32_t>(), rank.as<int32_t>(), 2 * m + 1))) return st;
+    int32_t touched = 0;
+    if ((st = read_i32(ctx, rank.as<int32_t>() + 2 * m, &touched))) return st;
+    CU(uflag.alloc(sizeof(int32_t) * (n + 1)));
+    CU(urank.alloc(sizeof(int32_t) * (n + 1)));
+    k_vperm_touched<<<grid_for(n + 1), kThreads, 0, ctx->stream>>>(key.as<int32_t>(), rank.as<int32_t>(), n,
+                                                                  L->vertex_perm, uflag.as<int32_t>());
+    if ((st = exclusive_scan(ctx, uflag.as<int32_t>(), urank.as<int32_t>(), n + 1))) return st;
+    k_vperm_untouched<<<grid_for(n), kThreads, 0, ctx->stream>>>(key.as<int32_t>(), urank.as<int32_t>(), n, touched,
+                                                                L->vertex_perm);
+    // 4. beginA
+    k_pvb<<<grid_for(k + 1), kThreads, 0, ctx->stream>>>(rank.as<int32_t>(), L->part_edge_begin, k,
+                                                        L->part_vertex_begin);
+    // 5. halo sizes -> halo_begin
+    CU(nh.alloc(sizeof(int32_t) * (k + 1)));
+    k_halo_counts<<<grid_for(k + 1), kThreads, 0, ctx->stream>>>(distinct.as<int32_t>(), L->part_vertex_begin, k,
+                                                                nh.as<int32_t>());
+    CHECK_LAUNCH();
+    if ((st = exclusive_scan(ctx, nh.as<int32_t>(), L->halo_begin, k + 1))) return st;
+    int32_t C = 0;
+    if ((st = read_i32(ctx, L->halo_begin + k, &C))) return st;
+    if (C > L->halo_cap)
+        return ctx->fail(EPG_ERR_INPUT, "remap: halo_cap " + std::to_string(L->halo_cap) + " < cut cost " +
+                                            std::to_string(C));
+    // plan
+    epg_plan *pl = new epg_plan();
+    pl->ctx = ctx; pl->device = ctx->device;
+    pl->m = m; pl->n = n; pl->k = k; pl->touched = touched; pl->C = C;
+    auto fail_plan = [&](epg_status s) { delete pl; return s; };
+    if ((st = plan_alloc_t(pl, ctx, &pl->peb, k + 1)) || (st = plan_alloc_t(pl, ctx, &pl->pvb, k + 1)) ||
+        (st = plan_alloc_t(pl, ctx, &pl->hb, k + 1)) || (st = plan_alloc_t(pl, ctx, &pl->halo_ids, C)) ||
+        (st = plan_alloc_t(pl, ctx, &pl->slots, m)) || (st = plan_alloc_t(pl, ctx, &pl->inc, 2 * m)) ||
+        (st = plan_alloc_t(pl, ctx, &pl->inc_off, (int64_t)touched + C)) ||
+        (st = plan_alloc_t(pl, ctx, &pl->sidx, n + 1)))
+        return fail_plan(st);
+    // 6-7. per-partition sort: halo ids, slots, incidence lists
+    {
+        const int eb = bits_for(n);
+        uint16_t *slots16 = L->slots;
+        if (2 * smax <= 512)
+            st = launch_remap_part<256, 2>(ctx, edges, L->edge_perm, L->vertex_perm, L->part_edge_begin,
+                                           L->part_vertex_begin, L->halo_begin, L->halo_ids, slots16, pl->inc,
+                                           pl->inc_off, k, eb);
+        else if (2 * smax <= 2048)
+            st = launch_remap_part<256, 8>(ctx, edges, L->edge_perm, L->vertex_perm, L->part_edge_begin,
+                                           L->part_vertex_begin, L->halo_begin, L->halo_ids, slots16, pl->inc,
+                                           pl->inc_off, k, eb);
+        else
+            st = launch_remap_part<512, 16>(ctx, edges, L->edge_perm, L->vertex_perm, L->part_edge_begin,
+                                            L->part_vertex_begin, L->halo_begin, L->halo_ids, slots16, pl->inc,
+                                            pl->inc_off, k, eb);
+        if (st) return fail_plan(st);
+    }
+#define CPY(dst, src, bytes)                                                                          \
+    do {                                                                                              \
+        cudaError_t _e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream);     \
+        if (_e != cudaSuccess) return fail_plan(ctx->fail(EPG_ERR_CUDA, cudaGetErrorString(_e)));      \
+    } while (0)
+    CPY(pl->peb, L->part_edge_begin, sizeof(int32_t) * (k + 1));
+    CPY(pl->pvb, L->part_vertex_begin, sizeof(int32_t) * (k + 1));
+    CPY(pl->hb, L->halo_begin, sizeof(int32_t) * (k + 1));
+    if (C > 0) CPY(pl->halo_ids, L->halo_ids, sizeof(int32_t) * C);
+    CPY(pl->slots, L->slots, sizeof(uint32_t) * m);
+    // shared vertices (p_v > 1) and their halo positions
+    {
+        Tmp sflag(ctx), sscan(ctx), iota(ctx), skeys(ctx), temp(ctx);
+        if (sflag.alloc(sizeof(int32_t) * (n + 1)) || sscan.alloc(sizeof(int32_t) * (n + 1)))
+            return fail_plan(ctx->fail(EPG_ERR_NOMEM, "remap: temporaries"));
+        cudaMemsetAsync(sflag.p, 0, sizeof(int32_t) * (n + 1), ctx->stream);
+        if (C > 0) k_mark_shared<<<grid_for(C), kThreads, 0, ctx->stream>>>(pl->halo_ids, C, sflag.as<int32_t>());
+        if ((st = exclusive_scan(ctx, sflag.as<int32_t>(), sscan.as<int32_t>(), n + 1))) return fail_plan(st);
+        int32_t S = 0;
+        if ((st = read_i32(ctx, sscan.as<int32_t>() + n, &S))) return fail_plan(st);
+        pl->S = S;
+        if ((st = plan_alloc_t(pl, ctx, &pl->shared_ids, S)) || (st = plan_alloc_t(pl, ctx, &pl->hv_off, S + 1)) ||
+            (st = plan_alloc_t(pl, ctx, &pl->hv_list, C)) || (st = plan_alloc_t(pl, ctx, &pl->owner_buf, 5 * S)) ||
+            (st = plan_alloc_t(pl, ctx, &pl->halo_buf, 5 * (int64_t)C)))
+            return fail_plan(st);
+        k_shared_index<<<grid_for(n), kThreads, 0, ctx->stream>>>(sflag.as<int32_t>(), sscan.as<int32_t>(), n,
+                                                                 pl->sidx, pl->shared_ids);
+        if (C > 0) {
+            if (iota.alloc(sizeof(int32_t) * C) || skeys.alloc(sizeof(int32_t) * C))
+                return fail_plan(ctx->fail(EPG_ERR_NOMEM, "remap: temporaries"));
+            k_iota<<<grid_for(C), kThreads, 0, ctx->stream>>>(iota.as<int32_t>(), C);
+            size_t tb = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, tb, pl->halo_ids, skeys.as<int32_t>(), iota.as<int32_t>(),
+                                            pl->hv_list, (int)C, 0, bits_for(n), ctx->stream);
+            if (temp.alloc(tb)) return fail_plan(ctx->fail(EPG_ERR_NOMEM, "remap: temporaries"));
+            cub::DeviceRadixSort::SortPairs(temp.p, tb, pl->halo_ids, skeys.as<int32_t>(), iota.as<int32_t>(),
+                                            pl->hv_list, (int)C, 0, bits_for(n), ctx->stream);
+        }
+        k_hv_off<<<grid_for(C + 1), kThreads, 0, ctx->stream>>>(skeys.as<int32_t>(), C, pl->sidx, S, pl->hv_off);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return fail_plan(ctx->fail(EPG_ERR_CUDA, cudaGetErrorString(e)));
+    }
+#undef CPY
+    // staging capacities
+    {
+        std::vector<int32_t> dh(k);
+        cudaError_t e = cudaMemcpyAsync(dh.data(), distinct.p, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) return fail_plan(ctx->fail(EPG_ERR_CUDA, cudaGetErrorString(e)));
+        pl->Lcap = *std::max_element(dh.begin(), dh.end());
+        pl->Scap = (int)smax;
+    }
+    *plan_out = pl;
+    return EPG_OK;
+}
+
+void epg_plan_destroy(epg_plan *plan) {
+    if (!plan) return;
+    cudaSetDevice(plan->device);
+    delete plan;
+}
+
+epg_status epg_plan_info(const epg_plan *plan, int64_t *out6) {
+    if (!plan || !out6) return EPG_ERR_INPUT;
+    out6[0] = plan->m; out6[1] = plan->n; out6[2] = plan->k;
+    out6[3] = plan->touched; out6[4] = plan->C; out6[5] = plan->S;
+    return EPG_OK;
+}
+
+epg_status epg_permute_rows(epg_ctx *ctx, const void *src, void *dst, int64_t rows, int32_t row_bytes,
+                            const int32_t *perm, int32_t mode) {
+    if (!ctx) return EPG_ERR_STATE;
+    if (!src || !dst || !perm || rows < 0 || row_bytes <= 0 || row_bytes % 4 || (mode != 0 && mode != 1))
+        return ctx->fail(EPG_ERR_INPUT, "permute_rows: bad arguments");
+    if (src == dst) return ctx->fail(EPG_ERR_INPUT, "permute_rows: src and dst alias");
+    CU(cudaSetDevice(ctx->device));
+    const int32_t words = row_bytes / 4;
+    if (rows > 0)
+        k_permute_rows<<<grid_for(rows * words), kThreads, 0, ctx->stream>>>(
+            static_cast<const uint32_t *>(src), static_cast<uint32_t *>(dst), rows, words, perm, mode);
+    CHECK_LAUNCH();
+    return EPG_OK;
+}
+
+epg_status epg_run(epg_ctx *ctx, const epg_plan *plan, epg_kernel kernel, epg_state *state, int32_t steps) {
+    if (!ctx) return EPG_ERR_STATE;
+    if (!plan) return ctx->fail(EPG_ERR_INPUT, "run: plan is NULL");
+    if (plan->ctx != ctx || plan->device != ctx->device)
+        return ctx->fail(EPG_ERR_STATE, "run: plan belongs to another context");
+    epg_status st = check_state(ctx, kernel, state);
+    if (st) return st;
+    if (steps < 0) return ctx->fail(EPG_ERR_INPUT, "run: steps < 0");
+    CU(cudaSetDevice(ctx->device));
+    switch (kernel) {
+        case EPG_KERNEL_CFD_FLUX: return run_staged<CfdFlux>(ctx, plan, state, steps);
+        case EPG_KERNEL_GATHER_SCATTER: return run_staged<GatherScatter>(ctx, plan, state, steps);
+        default: return run_staged<Spmv>(ctx, plan, state, steps);
+    }
+}
+
+epg_status epg_run_naive(epg_ctx *ctx, epg_kernel kernel, const int32_t *edges, int64_t m, int32_t n,
+                         epg_state *state, int32_t steps) {
+    if (!ctx) return EPG_ERR_STATE;
+    if (!edges || m <= 0 || n <= 0) return ctx->fail(EPG_ERR_INPUT, "run_naive: need m > 0, n > 0, edges");
+    epg_status st = check_state(ctx, kernel, state);
+    if (st) return st;
+    if (steps < 0) return ctx->fail(EPG_ERR_INPUT, "run_naive: steps < 0");
+    CU(cudaSetDevice(ctx->device));
+    switch (kernel) {
+        case EPG_KERNEL_CFD_FLUX: return run_naive<CfdFlux>(ctx, edges, m, n, state, steps);
+        case EPG_KERNEL_GATHER_SCATTER: return run_naive<GatherScatter>(ctx, edges, m, n, state, steps);
+        default: return run_naive<Spmv>(ctx, edges, m, n, state, steps);
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,249 @@
+"""Thin Python binding of libepg.so (include/epg.h): argument marshalling only.
+
+Every step of the path runs in the library (host C++ partitioner, CUDA kernels); torch
+tensors only supply device memory and the CUDA stream. There is no fallback: if
+libepg.so is missing or fails to load, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libepg.so")
+
+OK, ERR_INPUT, ERR_INFEASIBLE, ERR_CUDA, ERR_NCCL, ERR_NOMEM, ERR_STATE = 0, 2, 3, 4, 5, 6, 7
+KERNEL_CFD_FLUX, KERNEL_GATHER_SCATTER, KERNEL_SPMV = 1, 2, 3
+KERNELS = {"cfd": KERNEL_CFD_FLUX, "gather_scatter": KERNEL_GATHER_SCATTER, "spmv": KERNEL_SPMV}
+ROW = {KERNEL_CFD_FLUX: 5, KERNEL_GATHER_SCATTER: 1, KERNEL_SPMV: 1}
+MAX_PART_SIZE = 4096
+PERM_GATHER, PERM_SCATTER = 0, 1
+
+# every symbol include/epg.h declares (checked by tests/test_abi.py)
+SYMBOLS = ["epg_create", "epg_destroy", "epg_last_error", "epg_num_parts", "epg_partition_host", "epg_partition",
+           "epg_default_partition", "epg_load_count", "epg_remap", "epg_plan_destroy", "epg_plan_info",
+           "epg_permute_rows", "epg_run", "epg_run_naive"]
+
+
+class _Report(C.Structure):
+    _fields_ = [(f, C.c_int64) for f in ("k", "load_count", "touched", "cut_cost", "max_size", "min_size")]
+
+
+class _Layout(C.Structure):
+    _fields_ = [("edge_perm", C.c_void_p), ("part_edge_begin", C.c_void_p), ("vertex_perm", C.c_void_p),
+                ("part_vertex_begin", C.c_void_p), ("halo_begin", C.c_void_p), ("halo_ids", C.c_void_p),
+                ("halo_cap", C.c_int64), ("slots", C.c_void_p)]
+
+
+class _State(C.Structure):
+    _fields_ = [("state_in", C.c_void_p), ("state_out", C.c_void_p), ("edge_payload", C.c_void_p),
+                ("vertex_const", C.c_void_p)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libepg.so not built at {LIB_PATH}; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = C.CDLL(LIB_PATH)
+    P, i32, i64, st = C.c_void_p, C.c_int32, C.c_int64, C.c_int
+    sig = {
+        "epg_create": (st, [C.c_int, P, C.POINTER(P)]),
+        "epg_destroy": (None, [P]),
+        "epg_last_error": (C.c_char_p, [P]),
+        "epg_num_parts": (i64, [i64, i32]),
+        "epg_partition_host": (st, [P, i64, i32, i32, i32, P, C.c_char_p, i64]),
+        "epg_partition": (st, [P, P, i64, i32, i32, i32, P, C.POINTER(_Report)]),
+        "epg_default_partition": (st, [P, i64, i32, P]),
+        "epg_load_count": (st, [P, P, i64, i32, P, i64, P, C.POINTER(_Report)]),
+        "epg_remap": (st, [P, P, i64, i32, P, i64, C.POINTER(_Layout), C.POINTER(P)]),
+        "epg_plan_destroy": (None, [P]),
+        "epg_plan_info": (st, [P, P]),
+        "epg_permute_rows": (st, [P, P, P, i64, i32, P, i32]),
+        "epg_run": (st, [P, P, C.c_int, C.POINTER(_State), i32]),
+        "epg_run_naive": (st, [P, C.c_int, P, i64, i32, C.POINTER(_State), i32]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+class EpgError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"epg status {status}: {message}")
+        self.status = status
+        self.message = message
+
+
+@dataclass
+class Report:
+    k: int
+    load_count: int
+    touched: int
+    cut_cost: int
+    max_size: int
+    min_size: int
+
+    @property
+    def replication(self) -> float:
+        return self.load_count / self.touched
+
+    @property
+    def redundant_fraction(self) -> float:
+        return self.cut_cost / self.load_count
+
+
+def _rep(r: _Report) -> Report:
+    return Report(r.k, r.load_count, r.touched, r.cut_cost, r.max_size, r.min_size)
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, np.ndarray):
+        assert t.flags.c_contiguous
+        return t.ctypes.data
+    assert t.is_contiguous(), "tensors passed to libepg must be contiguous"
+    return t.data_ptr()
+
+
+def num_parts(m: int, part_size: int) -> int:
+    return int(lib.epg_num_parts(m, part_size))
+
+
+def partition_host(edges, n: int, part_size: int, shards: int = 1) -> np.ndarray:
+    """Host EPG-1 (epg_partition_host); edges int32 [m][2] numpy or CPU tensor."""
+    e = np.ascontiguousarray(edges.cpu().numpy() if isinstance(edges, torch.Tensor) else edges, dtype=np.int32)
+    m = e.shape[0]
+    part = np.zeros(max(m, 1), np.int32)
+    buf = C.create_string_buffer(512)
+    s = lib.epg_partition_host(e.ctypes.data if m else None, m, n, part_size, shards, part.ctypes.data, buf, 512)
+    if s != OK:
+        raise EpgError(s, buf.value.decode())
+    return part[:m]
+
+
+@dataclass
+class Layout:
+    edge_perm: torch.Tensor
+    part_edge_begin: torch.Tensor
+    vertex_perm: torch.Tensor
+    part_vertex_begin: torch.Tensor
+    halo_begin: torch.Tensor
+    halo_ids: torch.Tensor
+    slots: torch.Tensor
+
+
+class Plan:
+    def __init__(self, handle, ctx):
+        self.handle = handle
+        self.ctx = ctx
+        info = np.zeros(6, np.int64)
+        lib.epg_plan_info(handle, info.ctypes.data)
+        self.m, self.n, self.k, self.touched, self.cut_cost, self.shared = (int(x) for x in info)
+
+    def close(self):
+        if self.handle:
+            lib.epg_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Context:
+    """An epg_ctx bound to a CUDA device and stream (default: torch's current stream)."""
+
+    def __init__(self, device: int = 0, stream: torch.cuda.Stream | None = None):
+        self.device = torch.device("cuda", device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        h = C.c_void_p()
+        s = lib.epg_create(device, C.c_void_p(self.stream.cuda_stream), C.byref(h))
+        if s != OK:
+            raise EpgError(s, f"epg_create(device={device}) failed")
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            lib.epg_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, s: int):
+        if s != OK:
+            raise EpgError(s, lib.epg_last_error(self.handle).decode())
+
+    # -- partition -----------------------------------------------------------------
+    def partition(self, edges: torch.Tensor, n: int, part_size: int, shards: int = 1, out: torch.Tensor | None = None):
+        m = edges.shape[0]
+        if out is None:
+            out = torch.empty(m, dtype=torch.int32, device=edges.device)
+        r = _Report()
+        self._check(lib.epg_partition(self.handle, _ptr(edges), m, n, part_size, shards, _ptr(out), C.byref(r)))
+        return out, _rep(r)
+
+    def default_partition(self, m: int, part_size: int) -> torch.Tensor:
+        out = torch.empty(m, dtype=torch.int32, device=self.device)
+        self._check(lib.epg_default_partition(self.handle, m, part_size, _ptr(out)))
+        return out
+
+    def load_count(self, edges: torch.Tensor, n: int, part: torch.Tensor, k: int, per_part: bool = False):
+        pp = torch.empty(k, dtype=torch.int32, device=self.device) if per_part else None
+        r = _Report()
+        self._check(lib.epg_load_count(self.handle, _ptr(edges), edges.shape[0], n, _ptr(part), k, _ptr(pp), C.byref(r)))
+        return (_rep(r), pp) if per_part else _rep(r)
+
+    # -- remap ---------------------------------------------------------------------
+    def remap(self, edges: torch.Tensor, n: int, part: torch.Tensor, k: int, halo_cap: int | None = None):
+        m = edges.shape[0]
+        if halo_cap is None:
+            halo_cap = self.load_count(edges, n, part, k).cut_cost
+        d = self.device
+        i32 = torch.int32
+        L = Layout(torch.empty(m, dtype=i32, device=d), torch.empty(k + 1, dtype=i32, device=d),
+                   torch.empty(n, dtype=i32, device=d), torch.empty(k + 1, dtype=i32, device=d),
+                   torch.empty(k + 1, dtype=i32, device=d), torch.empty(max(halo_cap, 1), dtype=i32, device=d),
+                   torch.empty((m, 2), dtype=torch.uint16, device=d))
+        cl = _Layout(_ptr(L.edge_perm), _ptr(L.part_edge_begin), _ptr(L.vertex_perm), _ptr(L.part_vertex_begin),
+                     _ptr(L.halo_begin), _ptr(L.halo_ids), halo_cap, _ptr(L.slots))
+        h = C.c_void_p()
+        self._check(lib.epg_remap(self.handle, _ptr(edges), m, n, _ptr(part), k, C.byref(cl), C.byref(h)))
+        plan = Plan(h, self)
+        L.halo_ids = L.halo_ids[: plan.cut_cost]
+        return L, plan
+
+    def permute_rows(self, src: torch.Tensor, perm: torch.Tensor, mode: int, out: torch.Tensor | None = None):
+        rows = perm.shape[0]
+        if out is None:
+            out = torch.empty_like(src)
+        row_bytes = src[0].numel() * src.element_size() if src.dim() > 1 else src.element_size()
+        self._check(lib.epg_permute_rows(self.handle, _ptr(src), _ptr(out), rows, row_bytes, _ptr(perm), mode))
+        return out
+
+    # -- run -------------------------------------------------------------------------
+    def run(self, plan: Plan, kernel: int, state_in: torch.Tensor, state_out: torch.Tensor,
+            payload: torch.Tensor | None = None, vconst: torch.Tensor | None = None, steps: int = 1):
+        st = _State(_ptr(state_in), _ptr(state_out), _ptr(payload), _ptr(vconst))
+        self._check(lib.epg_run(self.handle, plan.handle, kernel, C.byref(st), steps))
+        return state_out if steps % 2 else state_in
+
+    def run_naive(self, kernel: int, edges: torch.Tensor, n: int, state_in: torch.Tensor, state_out: torch.Tensor,
+                  payload: torch.Tensor | None = None, vconst: torch.Tensor | None = None, steps: int = 1):
+        st = _State(_ptr(state_in), _ptr(state_out), _ptr(payload), _ptr(vconst))
+        self._check(lib.epg_run_naive(self.handle, kernel, _ptr(edges), edges.shape[0], n, C.byref(st), steps))
+        return state_out if steps % 2 else state_in

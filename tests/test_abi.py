@@ -1,0 +1,90 @@
+"""CPU checks of the boundary: libepg.so loads, exports every symbol include/epg.h
+declares, and its host EP partitioner (step a2, host C++) agrees with the oracle bit for
+bit. No CUDA compute is called here."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle as O
+import synth as S
+from conftest import ROOT, golden
+
+
+def _declared_symbols():
+    with open(os.path.join(ROOT, "include", "epg.h")) as f:
+        src = re.sub(r"/\*.*?\*/", "", f.read(), flags=re.S)
+    return sorted(set(re.findall(r"\b(epg_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1605_02043_b200 import epg
+    lib = ctypes.CDLL(epg.LIB_PATH)
+    declared = _declared_symbols()
+    assert len(declared) >= 14
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert sorted(epg.SYMBOLS) == declared
+
+
+def test_num_parts():
+    from paper_1605_02043_b200 import epg
+    for m, P in [(1, 1), (190245, 1024), (458168, 256), (10, 3)]:
+        assert epg.num_parts(m, P) == O.num_parts(m, P)
+    assert epg.num_parts(0, 5) == 0
+
+
+def test_host_partition_fixtures():
+    from paper_1605_02043_b200 import epg
+    g = golden("fig_mot.json")
+    e = np.array(g["topologies"]["star_plus_triangle"], np.int32)
+    assert epg.partition_host(e, 6, 3).tolist() == g["schedule_b"]
+    g2 = golden("two_triangle.json")
+    assert epg.partition_host(np.array(g2["edges"], np.int32), 6, 3).tolist() == g2["optimal_partition"]
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_host_partition_random_bitexact(seed):
+    from paper_1605_02043_b200 import epg
+    rng = np.random.default_rng(900 + seed)
+    m = int(rng.integers(1, 3000))
+    n = int(rng.integers(1, 1500))
+    n, e = S.random_multigraph(seed, m, n)
+    P = int(rng.integers(1, 300))
+    k = O.num_parts(m, P)
+    for G in (1, 2, 4, 8):
+        if G > k:
+            continue
+        assert np.array_equal(epg.partition_host(e, n, P, G), O.partition(e, n, P, G))
+
+
+@pytest.mark.parametrize("P", [256, 1024, 4096])
+def test_host_partition_mesh_bitexact(mesh_c1, P):
+    from paper_1605_02043_b200 import epg
+    M = mesh_c1
+    assert np.array_equal(epg.partition_host(M.edges, M.n, P), O.partition(M.edges, M.n, P))
+
+
+def test_host_partition_hierarchical_mesh(small_mesh):
+    from paper_1605_02043_b200 import epg
+    M = small_mesh
+    for G in (2, 4, 8):
+        assert np.array_equal(epg.partition_host(M.edges, M.n, 256, G), O.partition(M.edges, M.n, 256, G))
+
+
+def test_host_partition_errors():
+    from paper_1605_02043_b200 import epg
+    with pytest.raises(epg.EpgError) as ex:
+        epg.partition_host(np.array([[0, 1], [1, 7]], np.int32), 3, 2)
+    assert ex.value.status == epg.ERR_INPUT and "edge 1" in ex.value.message
+    with pytest.raises(epg.EpgError) as ex:
+        epg.partition_host(np.array([[0, 1]], np.int32), 2, 4097)
+    assert ex.value.status == epg.ERR_INFEASIBLE
+    with pytest.raises(epg.EpgError) as ex:
+        epg.partition_host(np.array([[0, 1]] * 4, np.int32), 2, 2, shards=4)
+    assert ex.value.status == epg.ERR_INFEASIBLE
+    with pytest.raises(epg.EpgError) as ex:
+        epg.partition_host(np.zeros((0, 2), np.int32), 2, 2)
+    assert ex.value.status == epg.ERR_INPUT
