@@ -210,6 +210,16 @@ epg_status epg_run(epg_ctx *ctx, const epg_plan *plan, epg_kernel kernel, epg_st
 epg_status epg_run_naive(epg_ctx *ctx, epg_kernel kernel, const int32_t *edges, int64_t m, int32_t n_vertices,
                          epg_state *state, int32_t steps);
 
+/* -- measurement -------------------------------------------------------------- */
+/* Kernel timing for bench.py: while enabled, epg_run / epg_run_naive record a CUDA event
+ * pair on the ctx stream around every kernel they launch. epg_profile_read synchronises
+ * the stream, returns the summed device time (ms) per kernel class since the previous
+ * read and resets the accumulators:
+ *   ms[0] edge kernel (staged, or naive edge pass), ms[1] finalise / naive update;
+ *   launches[0], launches[1] the matching launch counts. */
+epg_status epg_set_profiling(epg_ctx *ctx, int32_t enable);
+epg_status epg_profile_read(epg_ctx *ctx, float *ms2, int64_t *launches2);
+
 #ifdef __cplusplus
 }
 #endif

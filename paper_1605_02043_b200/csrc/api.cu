@@ -18,6 +18,33 @@ struct epg_ctx {
     std::string err;
     float *naive_F = nullptr;
     size_t naive_F_bytes = 0;
+    // profiling: event pairs around launches, per kernel class (0 edge, 1 finalise/update)
+    bool profiling = false;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_used;
+    cudaEvent_t take_event() {
+        if (ev_pool.empty()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            return e;
+        }
+        cudaEvent_t e = ev_pool.back();
+        ev_pool.pop_back();
+        return e;
+    }
+    // returns the start event (recorded) or nullptr when not profiling
+    cudaEvent_t prof_begin() {
+        if (!profiling) return nullptr;
+        cudaEvent_t a = take_event();
+        cudaEventRecord(a, stream);
+        return a;
+    }
+    void prof_end(int cls, cudaEvent_t a) {
+        if (!a) return;
+        cudaEvent_t b = take_event();
+        cudaEventRecord(b, stream);
+        ev_used.push_back({cls, {a, b}});
+    }
     epg_status fail(epg_status s, const std::string &msg) {
         err = msg;
         return s;
@@ -313,11 +340,16 @@ epg_status run_staged(epg_ctx *ctx, const epg_plan *pl, epg_state *state, int32_
     for (int32_t s = 0; s < steps; s++) {
         a.state_in = bufs[s & 1];
         a.state_out = bufs[(s + 1) & 1];
+        cudaEvent_t t0 = ctx->prof_begin();
         k_edge_staged<Fn, kThreads><<<(unsigned)pl->k, kThreads, smem, ctx->stream>>>(a);
-        if (fin_work > 0)
+        ctx->prof_end(0, t0);
+        if (fin_work > 0) {
+            cudaEvent_t t1 = ctx->prof_begin();
             k_finalise<Fn><<<grid_for(fin_work), kThreads, 0, ctx->stream>>>(
                 pl->shared_ids, pl->hv_off, pl->hv_list, pl->owner_buf, pl->halo_buf, a.state_in, a.state_out,
                 a.vconst, (int32_t)pl->S, pl->touched, pl->n);
+            ctx->prof_end(1, t1);
+        }
     }
     CHECK_LAUNCH();
     return EPG_OK;
@@ -342,9 +374,13 @@ epg_status run_naive(epg_ctx *ctx, const int32_t *edges, int64_t m, int64_t n, e
     const float *payload = static_cast<const float *>(state->edge_payload);
     const float *vc = static_cast<const float *>(state->vertex_const);
     for (int32_t s = 0; s < steps; s++) {
+        cudaEvent_t t0 = ctx->prof_begin();
         k_naive_edges<Fn><<<grid_for(m), kThreads, 0, ctx->stream>>>(edges, m, bufs[s & 1], payload, ctx->naive_F);
+        ctx->prof_end(0, t0);
+        cudaEvent_t t1 = ctx->prof_begin();
         k_naive_update<Fn><<<grid_for(n), kThreads, 0, ctx->stream>>>(n, bufs[s & 1], bufs[(s + 1) & 1], vc,
                                                                         ctx->naive_F);
+        ctx->prof_end(1, t1);
     }
     CHECK_LAUNCH();
     return EPG_OK;
@@ -388,6 +424,8 @@ void epg_destroy(epg_ctx *ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     if (ctx->naive_F) cudaFree(ctx->naive_F);
+    for (auto &u : ctx->ev_used) { cudaEventDestroy(u.second.first); cudaEventDestroy(u.second.second); }
+    for (auto e : ctx->ev_pool) cudaEventDestroy(e);
     delete ctx;
 }
 
@@ -648,6 +686,31 @@ epg_status epg_run_naive(epg_ctx *ctx, epg_kernel kernel, const int32_t *edges, 
         case EPG_KERNEL_GATHER_SCATTER: return run_naive<GatherScatter>(ctx, edges, m, n, state, steps);
         default: return run_naive<Spmv>(ctx, edges, m, n, state, steps);
     }
+}
+
+epg_status epg_set_profiling(epg_ctx *ctx, int32_t enable) {
+    if (!ctx) return EPG_ERR_STATE;
+    ctx->profiling = enable != 0;
+    return EPG_OK;
+}
+
+epg_status epg_profile_read(epg_ctx *ctx, float *ms2, int64_t *launches2) {
+    if (!ctx) return EPG_ERR_STATE;
+    if (!ms2 || !launches2) return ctx->fail(EPG_ERR_INPUT, "profile_read: NULL output");
+    CU(cudaSetDevice(ctx->device));
+    CU(cudaStreamSynchronize(ctx->stream));
+    ms2[0] = ms2[1] = 0.0f;
+    launches2[0] = launches2[1] = 0;
+    for (auto &u : ctx->ev_used) {
+        float ms = 0.0f;
+        CU(cudaEventElapsedTime(&ms, u.second.first, u.second.second));
+        ms2[u.first] += ms;
+        launches2[u.first] += 1;
+        ctx->ev_pool.push_back(u.second.first);
+        ctx->ev_pool.push_back(u.second.second);
+    }
+    ctx->ev_used.clear();
+    return EPG_OK;
 }
 
 }  // extern "C"

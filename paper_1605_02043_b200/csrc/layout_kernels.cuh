@@ -227,8 +227,10 @@ __global__ void __launch_bounds__(BLOCK) k_remap_part(const int32_t *__restrict_
         low[it] = (valid && key[it] < o0) ? 1 : 0;
     }
     int ndistinct;
-    Scan(ts.scan).ExclusiveSum(head, rank, ndistinct);  // rank among distinct ids = position in V_p
+    Scan(ts.scan).InclusiveSum(head, rank, ndistinct);  // rank among distinct ids = position in V_p
     __syncthreads();
+#pragma unroll
+    for (int it = 0; it < ITEMS; it++) rank[it] -= 1;     // (inclusive count of heads) - 1
     int nlow;
     Scan(ts.scan).ExclusiveSum(low, lowpos, nlow);      // nlow = #halo incidences
     (void)ndistinct;

@@ -26,7 +26,7 @@ PERM_GATHER, PERM_SCATTER = 0, 1
 # every symbol include/epg.h declares (checked by tests/test_abi.py)
 SYMBOLS = ["epg_create", "epg_destroy", "epg_last_error", "epg_num_parts", "epg_partition_host", "epg_partition",
            "epg_default_partition", "epg_load_count", "epg_remap", "epg_plan_destroy", "epg_plan_info",
-           "epg_permute_rows", "epg_run", "epg_run_naive"]
+           "epg_permute_rows", "epg_run", "epg_run_naive", "epg_set_profiling", "epg_profile_read"]
 
 
 class _Report(C.Structure):
@@ -64,6 +64,8 @@ def _load():
         "epg_permute_rows": (st, [P, P, P, i64, i32, P, i32]),
         "epg_run": (st, [P, P, C.c_int, C.POINTER(_State), i32]),
         "epg_run_naive": (st, [P, C.c_int, P, i64, i32, C.POINTER(_State), i32]),
+        "epg_set_profiling": (st, [P, i32]),
+        "epg_profile_read": (st, [P, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -241,6 +243,16 @@ class Context:
         st = _State(_ptr(state_in), _ptr(state_out), _ptr(payload), _ptr(vconst))
         self._check(lib.epg_run(self.handle, plan.handle, kernel, C.byref(st), steps))
         return state_out if steps % 2 else state_in
+
+    def set_profiling(self, enable: bool):
+        self._check(lib.epg_set_profiling(self.handle, 1 if enable else 0))
+
+    def profile_read(self):
+        """-> ((edge_ms, finalise_ms), (edge_launches, finalise_launches)) since the last read."""
+        ms = np.zeros(2, np.float32)
+        n = np.zeros(2, np.int64)
+        self._check(lib.epg_profile_read(self.handle, ms.ctypes.data, n.ctypes.data))
+        return (float(ms[0]), float(ms[1])), (int(n[0]), int(n[1]))
 
     def run_naive(self, kernel: int, edges: torch.Tensor, n: int, state_in: torch.Tensor, state_out: torch.Tensor,
                   payload: torch.Tensor | None = None, vconst: torch.Tensor | None = None, steps: int = 1):
