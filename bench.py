@@ -1,0 +1,390 @@
+#!/usr/bin/env python
+"""bench.py -- edges/s per time step of the partition-scheduled cfd edge kernel on B200.
+
+One JSON line (rank 0). Workload (BASELINE.json configs[1], the config its metric is
+quoted on): the missile.domn.0.2M-shaped synthetic mesh C2 (232,536 cells, 458,168
+interior faces), EP partitions of part_size 1024, cfd flux functor, fp32.
+
+A "step" is one time step of the hot path (steps a5+a6: staged edge kernel + boundary
+finalise) on resident inputs. Partitioning (a2), the cost kernel (a3) and the remap
+(a4) run once per mesh -- the paper amortises them over the kernel calls of the
+application loop -- and are timed separately ("setup").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c1|c2|c3] [--part-size P]
+
+N > 1 (torchrun): every rank runs an independent replica of the workload (weak
+scaling, no data-path collective); the sharded mesh with the NCCL halo exchange of
+SURVEY §8(e) is not built yet.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "edges/s per time step and DRAM bytes/edge vs default schedule; % of HBM roofline"
+WORKLOADS = {
+    "c1": "C1: Rodinia cfd fvcorr.domn.097K-shaped Kuhn tet mesh, 97,046 cells, 190,245 interior faces",
+    "c2": "C2: cfd missile.domn.0.2M-shaped Kuhn tet mesh, 232,536 cells, 458,168 interior faces",
+    "c3": "C3: synthetic 3D tetrahedral mesh, 64,000,000 cells",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=list(WORKLOADS), default="c2")
+    ap.add_argument("--part-size", type=int, default=1024)
+    ap.add_argument("--flush-mib", type=int, default=512)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="bounded oracle sample for cpu_baseline")
+    ap.add_argument("--no-comparators", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+def alg_bytes_per_step(m: int, touched: int) -> int:
+    """SURVEY §8(d) compulsory bytes of one cfd step: each edge record once (8 B ids +
+    12 B normal), each touched vertex read once (20 B state + 4 B dt) and written once (20 B)."""
+    return 20 * m + 44 * touched
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi sampled every 50 ms; only samples inside marked windows are kept."""
+
+    Q = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.lines = []
+        self.windows = []
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(index), "-lms", "50"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.time(), line.strip()))
+
+    def window(self):
+        return _Window(self)
+
+    def summary(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        inside = [ln for t, ln in self.lines if any(a <= t <= b for a, b in self.windows)]
+        samples = inside if inside else [ln for _, ln in self.lines[-5:]]
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in samples:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm), "in_window": bool(inside)}
+
+
+class _Window:
+    def __init__(self, s):
+        self.s = s
+
+    def __enter__(self):
+        self.a = time.time()
+
+    def __exit__(self, *exc):
+        self.s.windows.append((self.a, time.time()))
+
+
+# --------------------------------------------------------------------------------- oracle
+def oracle_steps(M, U, dt, steps: int, budget_s: float | None = None):
+    """Time the CPU oracle's fp64 cfd step (orc_cfd_step, single thread) as it stands."""
+    import oracle as O
+    done, t0 = 0, time.perf_counter()
+    while done < steps or (budget_s is not None and time.perf_counter() - t0 < budget_s):
+        O.cfd_step(M.edges, M.n, M.normals, U, dt)
+        done += 1
+        if budget_s is not None and done >= steps and time.perf_counter() - t0 >= budget_s:
+            break
+    return done, time.perf_counter() - t0
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import synth as S
+    M = S.config_mesh(args.config)
+    U, dt = S.cfd_state(M.n), S.cfd_dt(M.volume)
+    oracle_steps(M, U, dt, args.warmup)
+    steps, secs = oracle_steps(M, U, dt, args.steps)
+    v = M.m * steps / secs
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "edges/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.config], "part_size": args.part_size, "functor": "cfd_flux"},
+        "cpu_baseline": {"value": v, "unit": "edges/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{steps} full steps of the fp64 oracle cfd step (oracle/epg_oracle.c "
+                                   f"orc_cfd_step) on the {args.config} mesh, single thread"},
+        "e2e": {"value": v, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------------- ours
+def timed_steps(torch, ctx, stream, K, step_fn, flush):
+    """K steps, each bracketed by CUDA events on the library's stream, L2 flushed
+    (outside the events) before every step. Returns total device ms."""
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    for i in range(K):
+        flush()
+        evs[i][0].record(stream)
+        step_fn(i)
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    return sum(a.elapsed_time(b) for a, b in evs)
+
+
+def run_ours(args, rank, local_rank, world):
+    import torch
+    import torch.distributed as dist
+
+    import synth as S
+    from paper_1605_02043_b200 import epg
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.current_stream(dev)
+    ctx = epg.Context(local_rank, stream)
+    K, W, P = args.steps, args.warmup, args.part_size
+    clocks = ClockSampler(local_rank)
+
+    # ---------------- setup (once per mesh; amortised over steps)
+    t0 = time.perf_counter()
+    M = S.config_mesh(args.config)
+    U, dt = S.cfd_state(M.n), S.cfd_dt(M.volume)
+    t_gen = time.perf_counter() - t0
+    E = torch.from_numpy(M.edges).to(dev)
+    k = epg.num_parts(M.m, P)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    part, rep = ctx.partition(E, M.n, P)                      # host EPG-1 + GPU cost kernel
+    t_part = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    L, plan = ctx.remap(E, M.n, part, k, halo_cap=rep.cut_cost)
+    torch.cuda.synchronize()
+    t_remap = time.perf_counter() - t0
+    Ud = torch.from_numpy(U).to(dev)
+    nrm = ctx.permute_rows(torch.from_numpy(M.normals).to(dev), L.edge_perm, epg.PERM_GATHER)
+    dtn = ctx.permute_rows(torch.from_numpy(dt).to(dev), L.vertex_perm, epg.PERM_SCATTER)
+    bufs = [ctx.permute_rows(Ud, L.vertex_perm, epg.PERM_SCATTER), torch.empty_like(Ud)]
+    flushbuf = torch.empty(args.flush_mib * (1 << 20) // 4, dtype=torch.float32, device=dev)
+
+    def flush():
+        flushbuf.fill_(1.0)
+
+    def ep_step(i):
+        ctx.run(plan, epg.KERNEL_CFD_FLUX, bufs[i & 1], bufs[(i + 1) & 1], nrm, dtn, 1)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---------------- headline: resident inputs, L2 flushed between steps
+    for i in range(W):
+        ep_step(i)
+    barrier()
+    with clocks.window():
+        tot_ms = timed_steps(torch, ctx, stream, K, lambda i: ep_step(i + W), flush)
+    barrier()
+    step_ms = tot_ms / K
+    if world > 1:
+        t = torch.tensor([step_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_ms = float(t.item())
+    value = world * M.m / (step_ms * 1e-3)
+    launches = 2 * K
+
+    # ---------------- per-kernel breakdown (library events around each launch)
+    ctx.set_profiling(True)
+    ctx.profile_read()
+    timed_steps(torch, ctx, stream, K, lambda i: ep_step(i), flush)
+    (edge_ms, fin_ms), (n_edge, n_fin) = ctx.profile_read()
+    ctx.set_profiling(False)
+    edge_ms, fin_ms = edge_ms / max(n_edge, 1), fin_ms / max(n_fin, 1)
+
+    # ---------------- e2e: host (pinned) state in, result out, through the public API
+    Uh = torch.from_numpy(U).pin_memory()
+    Uout_h = torch.empty_like(Uh).pin_memory()
+    Ud_in = torch.empty_like(Ud)
+    Ud_out = torch.empty_like(Ud)
+    n_bytes = Uh.numel() * 4
+
+    def e2e_step(i):
+        Ud_in.copy_(Uh, non_blocking=True)
+        ctx.permute_rows(Ud_in, L.vertex_perm, epg.PERM_SCATTER, out=bufs[0])
+        ctx.run(plan, epg.KERNEL_CFD_FLUX, bufs[0], bufs[1], nrm, dtn, 1)
+        ctx.permute_rows(bufs[1], L.vertex_perm, epg.PERM_GATHER, out=Ud_out)
+        Uout_h.copy_(Ud_out, non_blocking=True)
+
+    for i in range(W):
+        e2e_step(i)
+    barrier()
+    with clocks.window():
+        e2e_ms = timed_steps(torch, ctx, stream, K, e2e_step, flush) / K
+    barrier()
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = world * M.m / (e2e_ms * 1e-3)
+
+    # ---------------- comparators on the same box: default schedule, staged and naive
+    comparators = None
+    if not args.no_comparators:
+        dpart = ctx.default_partition(M.m, P)
+        drep = ctx.load_count(E, M.n, dpart, k)
+        DL, dplan = ctx.remap(E, M.n, dpart, k, halo_cap=drep.cut_cost)
+        dnrm = ctx.permute_rows(torch.from_numpy(M.normals).to(dev), DL.edge_perm, epg.PERM_GATHER)
+        ddt = ctx.permute_rows(torch.from_numpy(dt).to(dev), DL.vertex_perm, epg.PERM_SCATTER)
+        dbufs = [ctx.permute_rows(Ud, DL.vertex_perm, epg.PERM_SCATTER), torch.empty_like(Ud)]
+
+        def def_step(i):
+            ctx.run(dplan, epg.KERNEL_CFD_FLUX, dbufs[i & 1], dbufs[(i + 1) & 1], dnrm, ddt, 1)
+
+        nbufs = [Ud.clone(), torch.empty_like(Ud)]
+        nrm0, dt0 = torch.from_numpy(M.normals).to(dev), torch.from_numpy(dt).to(dev)
+
+        def naive_step(i):
+            ctx.run_naive(epg.KERNEL_CFD_FLUX, E, M.n, nbufs[i & 1], nbufs[(i + 1) & 1], nrm0, dt0, 1)
+
+        out = {}
+        for name, fn, r in (("default_staged", def_step, drep), ("naive_original_order", naive_step, None)):
+            for i in range(W):
+                fn(i)
+            barrier()
+            ms = timed_steps(torch, ctx, stream, K, fn, flush) / K
+            out[name] = {"edges_per_s": M.m / (ms * 1e-3), "ms_per_step": ms}
+            if r is not None:
+                out[name].update({"load_count": r.load_count, "cut_cost": r.cut_cost,
+                                  "replication": r.replication})
+        best_default = max(out.values(), key=lambda d: d["edges_per_s"])["edges_per_s"]
+        out["ep_speedup_vs_best_default"] = (M.m / (step_ms * 1e-3)) / best_default
+        comparators = out
+
+    clk = clocks.summary()
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_src = measured_peaks()
+    B = alg_bytes_per_step(M.m, rep.touched)
+    kern_ms = edge_ms + fin_ms
+    achieved = B / (kern_ms * 1e-3) / 1e9
+    roofline = {
+        "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+        "traffic": None,
+        "kernel": "k_edge_staged + k_finalise (one cfd time step)",
+        "algorithmic_bytes_per_step": B,
+        "bytes_per_edge_algorithmic": B / M.m,
+        "edge_kernel_ms": edge_ms, "finalise_ms": fin_ms,
+        "peak_source": peak_src,
+    }
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        steps, secs = oracle_steps(M, U, dt, 1, budget_s=args.cpu_seconds)
+        cpu = {"value": M.m * steps / secs, "unit": "edges/s", "cores": 1, "kind": "oracle",
+               "sample": f"{steps} full steps of the fp64 oracle cfd step (oracle/epg_oracle.c orc_cfd_step) "
+                         f"on the {args.config} mesh, single thread, ~{args.cpu_seconds:.0f} s budget"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.config], "part_size": P, "k": k, "functor": "cfd_flux",
+                   "schedule": "EP (host EPG-1) + cpack remap", "step": "k_edge_staged + k_finalise",
+                   "l2": f"flushed between timed steps ({args.flush_mib} MiB write)",
+                   "parallelism": "replicas" if world > 1 else "single"},
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "edges/s", "h2d_bytes_per_step": n_bytes, "d2h_bytes_per_step": n_bytes,
+                "ms_per_step": e2e_ms,
+                "path": "pinned host U -> H2D -> epg_permute_rows -> epg_run -> epg_permute_rows -> D2H"},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "partition": {"load_count": rep.load_count, "touched": rep.touched, "cut_cost": rep.cut_cost,
+                      "replication": rep.replication, "redundant_fraction": rep.redundant_fraction,
+                      "max_size": rep.max_size, "min_size": rep.min_size, "shared_vertices": plan.shared,
+                      "host_partition_s": t_part, "remap_s": t_remap, "mesh_gen_s": t_gen},
+        "comparators": comparators,
+        "seeds": {"mesh": 1605, "state": 1606},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank, local_rank, world = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_ours(args, rank, local_rank, world)
+
+
+if __name__ == "__main__":
+    main()

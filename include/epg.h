@@ -210,6 +210,12 @@ epg_status epg_run(epg_ctx *ctx, const epg_plan *plan, epg_kernel kernel, epg_st
 epg_status epg_run_naive(epg_ctx *ctx, epg_kernel kernel, const int32_t *edges, int64_t m, int32_t n_vertices,
                          epg_state *state, int32_t steps);
 
+/* Kernel variant used by epg_run: 0 = automatic (the pipelined kernel when its stage
+ * buffers fit shared memory, else the one-CTA-per-partition kernel), 1 = one CTA per
+ * partition, 2 = pipelined only (EPG_ERR_INFEASIBLE if it does not fit). Both compute
+ * the same result; the variants differ in how partitions are staged. */
+epg_status epg_set_variant(epg_ctx *ctx, int32_t variant);
+
 /* -- measurement -------------------------------------------------------------- */
 /* Kernel timing for bench.py: while enabled, epg_run / epg_run_naive record a CUDA event
  * pair on the ctx stream around every kernel they launch. epg_profile_read synchronises

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libepg.so")
 SOURCES = ["api.cu", "partition.cpp"]
-DEPS = SOURCES + ["epg_internal.h", "functors.cuh", "layout_kernels.cuh", "run_kernels.cuh"]
+DEPS = SOURCES + ["epg_internal.h", "functors.cuh", "layout_kernels.cuh", "run_kernels.cuh", "pipelined_kernel.cuh", "ptx.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -11,6 +11,7 @@
 #include "epg_internal.h"
 #include "layout_kernels.cuh"
 #include "run_kernels.cuh"
+#include "pipelined_kernel.cuh"
 
 struct epg_ctx {
     int device = 0;
@@ -20,6 +21,7 @@ struct epg_ctx {
     size_t naive_F_bytes = 0;
     // profiling: event pairs around launches, per kernel class (0 edge, 1 finalise/update)
     bool profiling = false;
+    int variant = 0;  // 0 auto, 1 one CTA per partition, 2 pipelined TMA
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_used;
     cudaEvent_t take_event() {
@@ -61,6 +63,11 @@ struct epg_plan {
     uint32_t *slots = nullptr;
     uint16_t *inc = nullptr, *inc_off = nullptr;
     float *owner_buf = nullptr, *halo_buf = nullptr;
+    // pipelined kernel: per-partition descriptors and contiguous blobs
+    epg::PartDesc *desc = nullptr;
+    unsigned char *blob = nullptr;
+    int32_t *halo_pos = nullptr;
+    int Ocap = 0, blob_max = 0;
     std::vector<void *> allocs;
     ~epg_plan() {
         for (void *p : allocs) cudaFree(p);
@@ -319,7 +326,124 @@ epg_status launch_remap_part(epg_ctx *ctx, const int32_t *edges, const int32_t *
 }
 
 template <class Fn>
+epg_status run_one_cta_per_partition(epg_ctx *ctx, const epg_plan *pl, epg_state *state, int32_t steps);
+
+// descriptors + contiguous per-partition blobs for the pipelined kernel
+epg_status build_pipeline_blob(epg_ctx *ctx, epg_plan *pl) {
+    const int64_t k = pl->k, C = pl->C;
+    epg_status st;
+    if ((st = plan_alloc_t(pl, ctx, &pl->halo_pos, C)) || (st = plan_alloc_t(pl, ctx, &pl->desc, k))) return st;
+    if (C > 0) k_halo_pos<<<grid_for(C), kThreads, 0, ctx->stream>>>(pl->hv_list, C, pl->halo_pos);
+    Tmp units(ctx), off(ctx);
+    CU(units.alloc(sizeof(int32_t) * (k + 1)));
+    CU(off.alloc(sizeof(int32_t) * (k + 1)));
+    k_blob_sizes<<<grid_for(k + 1), kThreads, 0, ctx->stream>>>(pl->peb, pl->pvb, pl->hb, k, units.as<int32_t>());
+    CHECK_LAUNCH();
+    if ((st = exclusive_scan(ctx, units.as<int32_t>(), off.as<int32_t>(), k + 1))) return st;
+    int32_t total16 = 0;
+    if ((st = read_i32(ctx, off.as<int32_t>() + k, &total16))) return st;
+    if ((st = plan_alloc_t(pl, ctx, &pl->blob, 16 * (int64_t)total16 + 16))) return st;
+    k_build_blob<<<(unsigned)k, 256, 0, ctx->stream>>>(pl->peb, pl->pvb, pl->hb, pl->halo_ids, pl->halo_pos,
+                                                      pl->slots, pl->inc, pl->inc_off, off.as<int32_t>(), pl->blob,
+                                                      pl->desc);
+    CHECK_LAUNCH();
+    std::vector<int32_t> peb(k + 1), pvb(k + 1), hb(k + 1);
+    CU(cudaMemcpyAsync(peb.data(), pl->peb, sizeof(int32_t) * (k + 1), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(pvb.data(), pl->pvb, sizeof(int32_t) * (k + 1), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(hb.data(), pl->hb, sizeof(int32_t) * (k + 1), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    int ocap = 0, bmax = 0;
+    for (int64_t p = 0; p < k; p++) {
+        const int nO = pvb[p + 1] - pvb[p], nH = hb[p + 1] - hb[p], s = peb[p + 1] - peb[p];
+        ocap = std::max(ocap, nO);
+        bmax = std::max(bmax, (8 * nH + 8 * s + 2 * (nO + nH) + 15) & ~15);
+    }
+    pl->Ocap = ocap;
+    pl->blob_max = bmax;
+    return EPG_OK;
+}
+
+inline int up16i(int x) { return (x + 15) & ~15; }
+
+// shared-memory layout of the pipelined kernel for `nstage` stage buffers
+template <class Fn>
+size_t pipe_layout(const epg_plan *pl, bool has_payload, int nstage, PipeArgs *a) {
+    int off = up16i(pl->blob_max);
+    a->off_rows = off;
+    off += up16i(16 + 4 * Fn::ROW * pl->Lcap);
+    a->off_pay = off;
+    if (has_payload) off += up16i(16 + 4 * Fn::PAYW * pl->Scap);
+    a->off_vc = off;
+    if (Fn::kUsesConst) off += up16i(16 + 4 * pl->Ocap);
+    a->stage_bytes = off;
+    int w = nstage * off;
+    a->off_spd = w;
+    if (Fn::kDerived) w += up16i(4 * pl->Lcap);
+    a->off_phi = w;
+    w += up16i(4 * Fn::NPHI * pl->Scap);
+    a->nstage = nstage;
+    a->Scap = pl->Scap;
+    return (size_t)w;
+}
+
+constexpr int kPipeThreads = 512;
+
+template <class Fn>
+epg_status run_pipelined(epg_ctx *ctx, const epg_plan *pl, epg_state *state, int32_t steps, bool *fits) {
+    PipeArgs a{};
+    const bool has_payload = state->edge_payload != nullptr;
+    int dev_max = 0, sms = 0;
+    CU(cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    const size_t reserve = 1024;  // static shared memory (barriers, descriptors)
+    size_t smem = pipe_layout<Fn>(pl, has_payload, 2, &a);
+    if (smem + reserve > (size_t)dev_max) smem = pipe_layout<Fn>(pl, has_payload, 1, &a);
+    *fits = smem + reserve <= (size_t)dev_max;
+    if (!*fits) return EPG_OK;
+    CU(cudaFuncSetAttribute(k_edge_tma<Fn, kPipeThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_edge_tma<Fn, kPipeThreads>, kPipeThreads, smem));
+    const int64_t grid = std::min<int64_t>(pl->k, (int64_t)sms * std::max(occ, 1));
+    a.desc = pl->desc;
+    a.blob = pl->blob;
+    a.payload = static_cast<const float *>(state->edge_payload);
+    a.vconst = static_cast<const float *>(state->vertex_const);
+    a.halo_buf = pl->halo_buf;
+    a.k = pl->k;
+    float *bufs[2] = {static_cast<float *>(state->state_in), static_cast<float *>(state->state_out)};
+    const int64_t fin_work = pl->S + (pl->n - pl->touched);
+    for (int32_t s = 0; s < steps; s++) {
+        a.state_in = bufs[s & 1];
+        a.state_out = bufs[(s + 1) & 1];
+        cudaEvent_t t0 = ctx->prof_begin();
+        k_edge_tma<Fn, kPipeThreads><<<(unsigned)grid, kPipeThreads, smem, ctx->stream>>>(a);
+        ctx->prof_end(0, t0);
+        if (fin_work > 0) {
+            cudaEvent_t t1 = ctx->prof_begin();
+            k_finalise2<Fn><<<grid_for(fin_work), kThreads, 0, ctx->stream>>>(
+                pl->shared_ids, pl->hv_off, pl->halo_buf, a.state_in, a.state_out, a.vconst, (int32_t)pl->S,
+                pl->touched, pl->n);
+            ctx->prof_end(1, t1);
+        }
+    }
+    CHECK_LAUNCH();
+    return EPG_OK;
+}
+
+template <class Fn>
 epg_status run_staged(epg_ctx *ctx, const epg_plan *pl, epg_state *state, int32_t steps) {
+    if (ctx->variant != 1) {
+        bool fits = false;
+        epg_status st = run_pipelined<Fn>(ctx, pl, state, steps, &fits);
+        if (st || fits) return st;
+        if (ctx->variant == 2)
+            return ctx->fail(EPG_ERR_INFEASIBLE, "run: pipelined kernel does not fit shared memory");
+    }
+    return run_one_cta_per_partition<Fn>(ctx, pl, state, steps);
+}
+
+template <class Fn>
+epg_status run_one_cta_per_partition(epg_ctx *ctx, const epg_plan *pl, epg_state *state, int32_t steps) {
     const size_t smem = sizeof(float) * ((size_t)Fn::NV * pl->Lcap + (size_t)Fn::NPHI * pl->Scap);
     int dev_max = 0;
     CU(cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
@@ -625,6 +749,7 @@ epg_status epg_remap(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, c
         pl->Lcap = *std::max_element(dh.begin(), dh.end());
         pl->Scap = (int)smax;
     }
+    if ((st = build_pipeline_blob(ctx, pl))) return fail_plan(st);
     *plan_out = pl;
     return EPG_OK;
 }
@@ -686,6 +811,13 @@ epg_status epg_run_naive(epg_ctx *ctx, epg_kernel kernel, const int32_t *edges, 
         case EPG_KERNEL_GATHER_SCATTER: return run_naive<GatherScatter>(ctx, edges, m, n, state, steps);
         default: return run_naive<Spmv>(ctx, edges, m, n, state, steps);
     }
+}
+
+epg_status epg_set_variant(epg_ctx *ctx, int32_t variant) {
+    if (!ctx) return EPG_ERR_STATE;
+    if (variant < 0 || variant > 2) return ctx->fail(EPG_ERR_INPUT, "set_variant: 0 auto, 1 per-partition, 2 pipelined");
+    ctx->variant = variant;
+    return EPG_OK;
 }
 
 epg_status epg_set_profiling(epg_ctx *ctx, int32_t enable) {

@@ -116,6 +116,35 @@ struct CfdFlux {
             atomicAdd(F + 5 * (int64_t)b + c, -phi[c]);
         }
     }
+    // ---- pipelined (TMA-staged) kernel: rows are the staged AoS state rows, one derived
+    // float per local vertex (|u| + c); rinv and p are recomputed per endpoint.
+    static constexpr int PAYW = 3;
+    static constexpr bool kDerived = true;
+    __device__ __forceinline__ static float derive(const float *row) {
+        return cfd_derive(row[0], row[1], row[2], row[3], row[4]).speed;
+    }
+    __device__ __forceinline__ static CfdVertex load_row(const float *rows, int j, float speed) {
+        const float *r = rows + 5 * j;
+        CfdVertex d;
+        d.rho = r[0]; d.mx = r[1]; d.my = r[2]; d.mz = r[3]; d.E = r[4];
+        d.rinv = 1.0f / d.rho;
+        const float ux = d.mx * d.rinv, uy = d.my * d.rinv, uz = d.mz * d.rinv;
+        d.p = (kGamma - 1.0f) * (d.E - 0.5f * d.rho * (ux * ux + uy * uy + uz * uz));
+        d.speed = speed;
+        return d;
+    }
+    __device__ __forceinline__ static void edge2(const float *rows, const float *spd, int a, int b,
+                                                 const float *pay, int i, float *Phi, int Scap) {
+        float phi[5];
+        cfd_phi(load_row(rows, a, spd[a]), load_row(rows, b, spd[b]), pay[3 * i], pay[3 * i + 1], pay[3 * i + 2],
+                phi);
+#pragma unroll
+        for (int c = 0; c < 5; c++) Phi[c * Scap + i] = phi[c];
+    }
+    __device__ __forceinline__ static void finalise_add(float *__restrict__ out, const float acc[5], float dt) {
+#pragma unroll
+        for (int c = 0; c < 5; c++) out[c] = fmaf(dt, acc[c], out[c]);
+    }
     static constexpr bool kUsesConst = true;
 };
 
@@ -144,6 +173,18 @@ struct GatherScatter {
         atomicAdd(F + a, w * __ldg(x + b));
         atomicAdd(F + b, w * __ldg(x + a));
     }
+    static constexpr int PAYW = 1;
+    static constexpr bool kDerived = false;
+    __device__ __forceinline__ static float derive(const float *) { return 0.0f; }
+    __device__ __forceinline__ static void edge2(const float *rows, const float *, int a, int b, const float *pay,
+                                                 int i, float *Phi, int Scap) {
+        const float w = pay ? pay[i] : 1.0f;
+        Phi[i] = w * rows[b];
+        Phi[Scap + i] = w * rows[a];
+    }
+    __device__ __forceinline__ static void finalise_add(float *__restrict__ out, const float acc[1], float) {
+        out[0] += acc[0];
+    }
     static constexpr bool kUsesConst = false;
 };
 
@@ -167,6 +208,16 @@ struct Spmv {
                                                       const float *__restrict__ payload, int64_t e,
                                                       float *__restrict__ F) {
         atomicAdd(F + b, __ldg(payload + e) * __ldg(x + a));
+    }
+    static constexpr int PAYW = 1;
+    static constexpr bool kDerived = false;
+    __device__ __forceinline__ static float derive(const float *) { return 0.0f; }
+    __device__ __forceinline__ static void edge2(const float *rows, const float *, int a, int, const float *pay,
+                                                 int i, float *Phi, int) {
+        Phi[i] = pay[i] * rows[a];
+    }
+    __device__ __forceinline__ static void finalise_add(float *__restrict__ out, const float acc[1], float) {
+        out[0] += acc[0];
     }
     static constexpr bool kUsesConst = false;
 };

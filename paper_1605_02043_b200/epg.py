@@ -26,7 +26,8 @@ PERM_GATHER, PERM_SCATTER = 0, 1
 # every symbol include/epg.h declares (checked by tests/test_abi.py)
 SYMBOLS = ["epg_create", "epg_destroy", "epg_last_error", "epg_num_parts", "epg_partition_host", "epg_partition",
            "epg_default_partition", "epg_load_count", "epg_remap", "epg_plan_destroy", "epg_plan_info",
-           "epg_permute_rows", "epg_run", "epg_run_naive", "epg_set_profiling", "epg_profile_read"]
+           "epg_permute_rows", "epg_run", "epg_run_naive", "epg_set_variant", "epg_set_profiling",
+           "epg_profile_read"]
 
 
 class _Report(C.Structure):
@@ -64,6 +65,7 @@ def _load():
         "epg_permute_rows": (st, [P, P, P, i64, i32, P, i32]),
         "epg_run": (st, [P, P, C.c_int, C.POINTER(_State), i32]),
         "epg_run_naive": (st, [P, C.c_int, P, i64, i32, C.POINTER(_State), i32]),
+        "epg_set_variant": (st, [P, i32]),
         "epg_set_profiling": (st, [P, i32]),
         "epg_profile_read": (st, [P, P, P]),
     }
@@ -243,6 +245,10 @@ class Context:
         st = _State(_ptr(state_in), _ptr(state_out), _ptr(payload), _ptr(vconst))
         self._check(lib.epg_run(self.handle, plan.handle, kernel, C.byref(st), steps))
         return state_out if steps % 2 else state_in
+
+    def set_variant(self, variant: int):
+        """0 auto, 1 one CTA per partition, 2 pipelined TMA kernel."""
+        self._check(lib.epg_set_variant(self.handle, variant))
 
     def set_profiling(self, enable: bool):
         self._check(lib.epg_set_profiling(self.handle, 1 if enable else 0))

@@ -17,11 +17,14 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-5
 
 
-@pytest.fixture(scope="module")
-def ctx():
+@pytest.fixture(scope="module", params=[2, 1], ids=["pipelined", "per_partition"])
+def ctx(request):
+    """Both staged-kernel variants: 2 = persistent TMA-pipelined, 1 = one CTA per partition."""
     from paper_1605_02043_b200 import epg
     assert torch.cuda.is_available(), "GPU tests need a CUDA device"
-    return epg.Context(0)
+    c = epg.Context(0)
+    c.set_variant(request.param)
+    return c
 
 
 def dev(a, dtype=None):

@@ -1,0 +1,62 @@
+"""Run one cfd time step of each schedule variant on a mesh, for ncu capture.
+
+    ncu --metrics <...> -k regex:'k_edge|k_finalise|k_naive' python tools/ncu_variants.py --config c2
+
+Variants, in launch order: EP staged (k_edge_staged + k_finalise), default-map staged
+(same kernels), naive original order (k_naive_edges + k_naive_update). `--reps R`
+repeats the sequence (ncu -s can skip the first). Prints the per-variant kernel order.
+"""
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import synth as S  # noqa: E402
+from paper_1605_02043_b200 import epg  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--part-size", type=int, default=1024)
+    ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--variants", default="ep,default,naive")
+    a = ap.parse_args()
+    M = S.config_mesh(a.config)
+    U, dt = S.cfd_state(M.n), S.cfd_dt(M.volume)
+    ctx = epg.Context(0)
+    E = torch.from_numpy(M.edges).cuda()
+    k = epg.num_parts(M.m, a.part_size)
+    Ud = torch.from_numpy(U).cuda()
+    runs = []
+    for v in a.variants.split(","):
+        if v in ("ep", "default"):
+            part = ctx.partition(E, M.n, a.part_size)[0] if v == "ep" else ctx.default_partition(M.m, a.part_size)
+            L, plan = ctx.remap(E, M.n, part, k)
+            nrm = ctx.permute_rows(torch.from_numpy(M.normals).cuda(), L.edge_perm, epg.PERM_GATHER)
+            dtn = ctx.permute_rows(torch.from_numpy(dt).cuda(), L.vertex_perm, epg.PERM_SCATTER)
+            b = [ctx.permute_rows(Ud, L.vertex_perm, epg.PERM_SCATTER), torch.empty_like(Ud)]
+            runs.append((v, lambda plan=plan, b=b, nrm=nrm, dtn=dtn:
+                         ctx.run(plan, epg.KERNEL_CFD_FLUX, b[0], b[1], nrm, dtn, 1), plan))
+        else:
+            b = [Ud.clone(), torch.empty_like(Ud)]
+            nrm0, dt0 = torch.from_numpy(M.normals).cuda(), torch.from_numpy(dt).cuda()
+            runs.append((v, lambda b=b, nrm0=nrm0, dt0=dt0:
+                         ctx.run_naive(epg.KERNEL_CFD_FLUX, E, M.n, b[0], b[1], nrm0, dt0, 1), None))
+    torch.cuda.synchronize()
+    for r in range(a.reps):
+        for name, fn, plan in runs:
+            fn()
+            torch.cuda.synchronize()
+            if r == 0:
+                extra = f" k={plan.k} touched={plan.touched} C={plan.cut_cost} S={plan.shared}" if plan else ""
+                print(f"variant {name}: m={M.m} n={M.n}{extra}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
