@@ -181,9 +181,13 @@ epg_status epg_load_count(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t
 epg_status epg_remap(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n_vertices,
                      const int32_t *part_of_edge, int64_t k, epg_layout *layout, epg_plan **plan);
 void epg_plan_destroy(epg_plan *plan);
-/* Sizes of a plan: out[0..5] = m, n, k, touched, cut_cost (= |halo_ids|),
- * shared vertex count (vertices with p_v > 1). */
-epg_status epg_plan_info(const epg_plan *plan, int64_t *out6);
+/* Sizes of a plan: out[0..7] = m, n, k, touched, cut_cost (= |halo_ids| of the layout),
+ * shared vertex count of the execution plan, k_exec, cut cost of the execution plan.
+ * Execution partitions: an EP partition whose staged rows or edges exceed what one CTA
+ * of the staged kernel holds (768 rows, 1024 edges) is executed as contiguous ranges of
+ * its reorganised edges; this changes neither edge_perm nor vertex_perm, only how many
+ * thread blocks share the partition (k_exec >= k). */
+epg_status epg_plan_info(const epg_plan *plan, int64_t *out8);
 
 /* Row permutation (step a7 and the layout change of a4), DEVICE arrays:
  *   mode 0 (gather):  dst[i]       = src[perm[i]]   for i < rows
@@ -210,10 +214,11 @@ epg_status epg_run(epg_ctx *ctx, const epg_plan *plan, epg_kernel kernel, epg_st
 epg_status epg_run_naive(epg_ctx *ctx, epg_kernel kernel, const int32_t *edges, int64_t m, int32_t n_vertices,
                          epg_state *state, int32_t steps);
 
-/* Kernel variant used by epg_run: 0 = automatic (the pipelined kernel when its stage
- * buffers fit shared memory, else the one-CTA-per-partition kernel), 1 = one CTA per
- * partition, 2 = pipelined only (EPG_ERR_INFEASIBLE if it does not fit). Both compute
- * the same result; the variants differ in how partitions are staged. */
+/* Kernel variant used by epg_run: 0 = automatic (the first of 3, 2, 1 whose buffers fit),
+ * 1 = one CTA per partition (plain loads), 2 = persistent pipelined TMA kernel, 3 = TMA
+ * kernel with one CTA per execution partition and several CTAs per SM. 2 and 3 return
+ * EPG_ERR_INFEASIBLE if the plan does not fit them. All compute the same result; they
+ * differ in how partitions are staged and scheduled. */
 epg_status epg_set_variant(epg_ctx *ctx, int32_t variant);
 
 /* -- measurement -------------------------------------------------------------- */

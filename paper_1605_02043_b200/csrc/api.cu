@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <queue>
 #include <climits>
 #include <cstring>
 #include <string>
@@ -12,6 +13,7 @@
 #include "layout_kernels.cuh"
 #include "run_kernels.cuh"
 #include "pipelined_kernel.cuh"
+#include "occupancy_kernel.cuh"
 
 struct epg_ctx {
     int device = 0;
@@ -21,7 +23,7 @@ struct epg_ctx {
     size_t naive_F_bytes = 0;
     // profiling: event pairs around launches, per kernel class (0 edge, 1 finalise/update)
     bool profiling = false;
-    int variant = 0;  // 0 auto, 1 one CTA per partition, 2 pipelined TMA
+    int variant = 0;  // 0 auto, 1 one CTA per partition, 2 pipelined TMA, 3 occupancy TMA
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_used;
     cudaEvent_t take_event() {
@@ -66,8 +68,23 @@ struct epg_plan {
     // pipelined kernel: per-partition descriptors and contiguous blobs
     epg::PartDesc *desc = nullptr;
     unsigned char *blob = nullptr;
+    int32_t *hid_blob = nullptr;
+    int Hcap = 0;
     int32_t *halo_pos = nullptr;
-    int Ocap = 0, blob_max = 0;
+    int Ocap = 0, blob_max = 0, inc_width = 0;   // inc_width: padded incidence width (0 = CSR)
+    std::vector<double> part_cost;                // modelled work per partition (ns)
+    // occupancy kernel: descriptors + blobs (halo ids, incidence)
+    epg::PartDesc *desc3 = nullptr;
+    unsigned char *blob3 = nullptr;
+    int blob3_max = 0;
+    // the EP map the plan executes (k, C of the paper's partitions; the plan itself may
+    // split oversized partitions into contiguous execution ranges)
+    int64_t k_ep = 0, C_ep = 0;
+    std::vector<int32_t> part_rows, part_edges;   // |V_p| and s_p of the plan's partitions
+    int assign_grid = 0;                          // grid size the assignment was built for
+    unsigned long long *bar_ctr = nullptr;        // grid barrier counter (monotone)
+    unsigned long long bar_gen = 0;               // launches so far
+    int32_t *cta_begin = nullptr, *cta_list = nullptr;
     std::vector<void *> allocs;
     ~epg_plan() {
         for (void *p : allocs) cudaFree(p);
@@ -334,31 +351,70 @@ epg_status build_pipeline_blob(epg_ctx *ctx, epg_plan *pl) {
     epg_status st;
     if ((st = plan_alloc_t(pl, ctx, &pl->halo_pos, C)) || (st = plan_alloc_t(pl, ctx, &pl->desc, k))) return st;
     if (C > 0) k_halo_pos<<<grid_for(C), kThreads, 0, ctx->stream>>>(pl->hv_list, C, pl->halo_pos);
-    Tmp units(ctx), off(ctx);
+    Tmp units(ctx), off(ctx), maxdeg(ctx), hunits(ctx), hoff(ctx);
+    CU(maxdeg.alloc(sizeof(int32_t)));
+    CU(cudaMemsetAsync(maxdeg.p, 0, sizeof(int32_t), ctx->stream));
+    k_max_local_degree<<<(unsigned)k, 256, 0, ctx->stream>>>(pl->peb, pl->pvb, pl->hb, pl->inc_off, k,
+                                                            maxdeg.as<int32_t>());
+    int32_t md = 0;
+    if ((st = read_i32(ctx, maxdeg.as<int32_t>(), &md))) return st;
+    const int W = md <= 4 ? 4 : (md <= 8 ? 8 : 0);
+    pl->inc_width = W;
     CU(units.alloc(sizeof(int32_t) * (k + 1)));
     CU(off.alloc(sizeof(int32_t) * (k + 1)));
-    k_blob_sizes<<<grid_for(k + 1), kThreads, 0, ctx->stream>>>(pl->peb, pl->pvb, pl->hb, k, units.as<int32_t>());
+    CU(hunits.alloc(sizeof(int32_t) * (k + 1)));
+    CU(hoff.alloc(sizeof(int32_t) * (k + 1)));
+    k_blob_sizes<<<grid_for(k + 1), kThreads, 0, ctx->stream>>>(pl->peb, pl->pvb, pl->hb, k, W, units.as<int32_t>(),
+                                                               hunits.as<int32_t>());
     CHECK_LAUNCH();
     if ((st = exclusive_scan(ctx, units.as<int32_t>(), off.as<int32_t>(), k + 1))) return st;
-    int32_t total16 = 0;
+    if ((st = exclusive_scan(ctx, hunits.as<int32_t>(), hoff.as<int32_t>(), k + 1))) return st;
+    int32_t total16 = 0, htotal16 = 0;
     if ((st = read_i32(ctx, off.as<int32_t>() + k, &total16))) return st;
+    if ((st = read_i32(ctx, hoff.as<int32_t>() + k, &htotal16))) return st;
     if ((st = plan_alloc_t(pl, ctx, &pl->blob, 16 * (int64_t)total16 + 16))) return st;
+    if ((st = plan_alloc_t(pl, ctx, &pl->hid_blob, 4 * (int64_t)htotal16 + 4))) return st;
     k_build_blob<<<(unsigned)k, 256, 0, ctx->stream>>>(pl->peb, pl->pvb, pl->hb, pl->halo_ids, pl->halo_pos,
-                                                      pl->slots, pl->inc, pl->inc_off, off.as<int32_t>(), pl->blob,
-                                                      pl->desc);
+                                                      pl->slots, pl->inc, pl->inc_off, off.as<int32_t>(),
+                                                      hoff.as<int32_t>(), W, pl->blob, pl->hid_blob, pl->desc);
     CHECK_LAUNCH();
+    {   // occupancy-kernel blobs
+        Tmp u3(ctx), o3(ctx);
+        CU(u3.alloc(sizeof(int32_t) * (k + 1)));
+        CU(o3.alloc(sizeof(int32_t) * (k + 1)));
+        k_blob3_sizes<<<grid_for(k + 1), kThreads, 0, ctx->stream>>>(pl->peb, pl->pvb, pl->hb, k, W, u3.as<int32_t>());
+        if ((st = exclusive_scan(ctx, u3.as<int32_t>(), o3.as<int32_t>(), k + 1))) return st;
+        int32_t t3 = 0;
+        if ((st = read_i32(ctx, o3.as<int32_t>() + k, &t3))) return st;
+        if ((st = plan_alloc_t(pl, ctx, &pl->blob3, 16 * (int64_t)t3 + 16)) ||
+            (st = plan_alloc_t(pl, ctx, &pl->desc3, k)))
+            return st;
+        k_build_blob3<<<(unsigned)k, 256, 0, ctx->stream>>>(pl->peb, pl->pvb, pl->hb, pl->halo_ids, pl->inc,
+                                                           pl->inc_off, o3.as<int32_t>(), W, pl->blob3, pl->desc3);
+        CHECK_LAUNCH();
+    }
     std::vector<int32_t> peb(k + 1), pvb(k + 1), hb(k + 1);
     CU(cudaMemcpyAsync(peb.data(), pl->peb, sizeof(int32_t) * (k + 1), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaMemcpyAsync(pvb.data(), pl->pvb, sizeof(int32_t) * (k + 1), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaMemcpyAsync(hb.data(), pl->hb, sizeof(int32_t) * (k + 1), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
-    int ocap = 0, bmax = 0;
+    int ocap = 0, bmax = 0, hcap = 0;
+    pl->part_cost.resize(k);
+    pl->part_rows.resize(k);
+    pl->part_edges.resize(k);
     for (int64_t p = 0; p < k; p++) {
         const int nO = pvb[p + 1] - pvb[p], nH = hb[p + 1] - hb[p], s = peb[p + 1] - peb[p];
         ocap = std::max(ocap, nO);
-        bmax = std::max(bmax, (8 * nH + 8 * s + 2 * (nO + nH) + 15) & ~15);
+        hcap = std::max(hcap, nH);
+        pl->part_rows[p] = nO + nH;
+        pl->part_edges[p] = s;
+        bmax = std::max(bmax, blob_bytes_for(nH, s, nO + nH, W));
+        pl->blob3_max = std::max(pl->blob3_max, blob3_bytes_for(nH, s, nO + nH, W));
+        // measured on B200 (cfd, P = 1024): ~1.4 ns per edge, ~1.6 per staged row, ~1 per halo row
+        pl->part_cost[p] = 1.4 * s + 1.6 * (nO + nH) + 1.0 * nH;
     }
     pl->Ocap = ocap;
+    pl->Hcap = hcap;
     pl->blob_max = bmax;
     return EPG_OK;
 }
@@ -377,19 +433,95 @@ size_t pipe_layout(const epg_plan *pl, bool has_payload, int nstage, PipeArgs *a
     if (Fn::kUsesConst) off += up16i(16 + 4 * pl->Ocap);
     a->stage_bytes = off;
     int w = nstage * off;
-    a->off_spd = w;
-    if (Fn::kDerived) w += up16i(4 * pl->Lcap);
+    a->off_der = w;
+    w += up16i(4 * Fn::REC * pl->Lcap);
     a->off_phi = w;
-    w += up16i(4 * Fn::NPHI * pl->Scap);
+    w += up16i(4 * Fn::PHIREC * (pl->Scap + 1));
+    a->off_hid = w;
+    a->hid_slot_bytes = up16i(4 * pl->Hcap + 16);
+    w += 3 * a->hid_slot_bytes;
     a->nstage = nstage;
+    a->Lcap = pl->Lcap;
     a->Scap = pl->Scap;
     return (size_t)w;
 }
 
 constexpr int kPipeThreads = 512;
 
+// Longest-processing-time-first assignment of partitions to G persistent CTAs: partitions
+// by decreasing modelled cost, each to the currently least-loaded CTA (ties: lower CTA).
+epg_status assign_partitions(epg_ctx *ctx, epg_plan *pl, int G) {
+    if (pl->assign_grid == G) return EPG_OK;
+    const int64_t k = pl->k;
+    std::vector<int32_t> order(k);
+    for (int64_t p = 0; p < k; p++) order[p] = (int32_t)p;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int32_t x, int32_t y) { return pl->part_cost[x] > pl->part_cost[y]; });
+    using Load = std::pair<double, int>;
+    std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
+    for (int b = 0; b < G; b++) heap.push({0.0, b});
+    std::vector<std::vector<int32_t>> lists(G);
+    for (int32_t p : order) {
+        Load l = heap.top();
+        heap.pop();
+        lists[l.second].push_back(p);
+        heap.push({l.first + pl->part_cost[p], l.second});
+    }
+    std::vector<int32_t> beg(G + 1, 0), flat;
+    flat.reserve(k);
+    for (int b = 0; b < G; b++) {
+        // ascending ids: at any time the CTAs work on neighbouring partitions, whose halo
+        // rows (owned by slightly lower partitions) are then likely resident in L2
+        std::sort(lists[b].begin(), lists[b].end());
+        beg[b + 1] = beg[b] + (int32_t)lists[b].size();
+        flat.insert(flat.end(), lists[b].begin(), lists[b].end());
+    }
+    if (!pl->cta_begin || pl->assign_grid < G) {
+        epg_status st;
+        if ((st = plan_alloc_t(pl, ctx, &pl->cta_begin, G + 1)) || (st = plan_alloc_t(pl, ctx, &pl->cta_list, k)))
+            return st;
+    }
+    CU(cudaMemcpy(pl->cta_begin, beg.data(), sizeof(int32_t) * (G + 1), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(pl->cta_list, flat.data(), sizeof(int32_t) * k, cudaMemcpyHostToDevice));
+    pl->assign_grid = G;
+    return EPG_OK;
+}
+
+template <class Fn, int W>
+epg_status launch_pipelined(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, PipeArgs a,
+                            size_t smem, int sms) {
+    auto kern = k_edge_tma<Fn, kPipeThreads, W>;
+    CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kPipeThreads, smem));
+    if (occ < 1) return ctx->fail(EPG_ERR_INFEASIBLE, "run: pipelined kernel cannot be resident");
+    // every CTA must be resident (the fused finalise follows a grid barrier): grid is at
+    // most SMs x occupancy, and the plan's barrier counter is advanced once per launch
+    const int64_t grid = std::min<int64_t>(std::max<int64_t>(pl->k, 1), (int64_t)sms * occ);
+    epg_status st = assign_partitions(ctx, pl, (int)grid);
+    if (st) return st;
+    a.cta_begin = pl->cta_begin;
+    a.cta_list = pl->cta_list;
+    if (!pl->bar_ctr) {
+        if ((st = plan_alloc_t(pl, ctx, &pl->bar_ctr, 1))) return st;
+        CU(cudaMemset(pl->bar_ctr, 0, sizeof(unsigned long long)));
+    }
+    a.bar_ctr = pl->bar_ctr;
+    float *bufs[2] = {static_cast<float *>(state->state_in), static_cast<float *>(state->state_out)};
+    for (int32_t s = 0; s < steps; s++) {
+        a.state_in = bufs[s & 1];
+        a.state_out = bufs[(s + 1) & 1];
+        pl->bar_gen += 1;
+        a.bar_target = pl->bar_gen * (unsigned long long)grid;
+        cudaEvent_t t0 = ctx->prof_begin();
+        kern<<<(unsigned)grid, kPipeThreads, smem, ctx->stream>>>(a);
+        ctx->prof_end(0, t0);
+    }
+    return EPG_OK;
+}
+
 template <class Fn>
-epg_status run_pipelined(epg_ctx *ctx, const epg_plan *pl, epg_state *state, int32_t steps, bool *fits) {
+epg_status run_pipelined(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, bool *fits) {
     PipeArgs a{};
     const bool has_payload = state->edge_payload != nullptr;
     int dev_max = 0, sms = 0;
@@ -400,29 +532,65 @@ epg_status run_pipelined(epg_ctx *ctx, const epg_plan *pl, epg_state *state, int
     if (smem + reserve > (size_t)dev_max) smem = pipe_layout<Fn>(pl, has_payload, 1, &a);
     *fits = smem + reserve <= (size_t)dev_max;
     if (!*fits) return EPG_OK;
-    CU(cudaFuncSetAttribute(k_edge_tma<Fn, kPipeThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int occ = 0;
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_edge_tma<Fn, kPipeThreads>, kPipeThreads, smem));
-    const int64_t grid = std::min<int64_t>(pl->k, (int64_t)sms * std::max(occ, 1));
     a.desc = pl->desc;
     a.blob = pl->blob;
+    a.hid_blob = pl->hid_blob;
     a.payload = static_cast<const float *>(state->edge_payload);
     a.vconst = static_cast<const float *>(state->vertex_const);
     a.halo_buf = pl->halo_buf;
     a.k = pl->k;
+    a.shared_ids = pl->shared_ids;
+    a.hv_off = pl->hv_off;
+    a.S = (int32_t)pl->S;
+    a.touched = pl->touched;
+    a.n = pl->n;
+    switch (pl->inc_width) {
+        case 4: return launch_pipelined<Fn, 4>(ctx, pl, state, steps, a, smem, sms);
+        case 8: return launch_pipelined<Fn, 8>(ctx, pl, state, steps, a, smem, sms);
+        default: return launch_pipelined<Fn, 0>(ctx, pl, state, steps, a, smem, sms);
+    }
+}
+
+// occupancy kernel limits: execution partitions of <= 1024 edges and <= 768 staged rows
+// (704 rows keep a cfd CTA at ~55 KB of shared memory: four CTAs per SM)
+constexpr int kOccThreads = 256, kOccEPT = 4, kOccVPT = 3;
+constexpr int kExecMaxEdges = kOccThreads * kOccEPT, kExecMaxRows = 704;
+
+// launch with programmatic stream serialization (the kernel calls griddepcontrol.wait
+// before touching what the previous kernel in the stream writes)
+template <class K, class... Args>
+cudaError_t launch_pdl(K kern, unsigned grid, unsigned block, size_t smem, cudaStream_t stream, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+template <class Fn, int W>
+epg_status launch_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, OccArgs a, size_t smem) {
+    auto kern = k_edge_occ<Fn, kOccThreads, kOccEPT, kOccVPT, W>;
+    CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     float *bufs[2] = {static_cast<float *>(state->state_in), static_cast<float *>(state->state_out)};
     const int64_t fin_work = pl->S + (pl->n - pl->touched);
     for (int32_t s = 0; s < steps; s++) {
         a.state_in = bufs[s & 1];
         a.state_out = bufs[(s + 1) & 1];
         cudaEvent_t t0 = ctx->prof_begin();
-        k_edge_tma<Fn, kPipeThreads><<<(unsigned)grid, kPipeThreads, smem, ctx->stream>>>(a);
+        CU(launch_pdl(kern, (unsigned)pl->k, kOccThreads, smem, ctx->stream, a));
         ctx->prof_end(0, t0);
         if (fin_work > 0) {
             cudaEvent_t t1 = ctx->prof_begin();
-            k_finalise2<Fn><<<grid_for(fin_work), kThreads, 0, ctx->stream>>>(
-                pl->shared_ids, pl->hv_off, pl->halo_buf, a.state_in, a.state_out, a.vconst, (int32_t)pl->S,
-                pl->touched, pl->n);
+            CU(launch_pdl(k_finalise3<Fn>, grid_for(fin_work), kThreads, 0, ctx->stream,
+                          (const int32_t *)pl->shared_ids, (const int32_t *)pl->hv_off, (const int32_t *)pl->hv_list,
+                          (const float *)pl->halo_buf, (const float *)a.state_in, a.state_out, a.vconst,
+                          (int32_t)pl->S, pl->touched, pl->n));
             ctx->prof_end(1, t1);
         }
     }
@@ -431,8 +599,42 @@ epg_status run_pipelined(epg_ctx *ctx, const epg_plan *pl, epg_state *state, int
 }
 
 template <class Fn>
-epg_status run_staged(epg_ctx *ctx, const epg_plan *pl, epg_state *state, int32_t steps) {
-    if (ctx->variant != 1) {
+epg_status run_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, bool *fits) {
+    *fits = false;
+    if (pl->Scap > kExecMaxEdges || pl->Lcap > kExecMaxRows) return EPG_OK;
+    int dev_max = 0;
+    CU(cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+    OccArgs a{};
+    a.off_recs = up16i(pl->blob3_max);
+    const int recs_bytes = up16i(4 * Fn::REC * pl->Lcap + 64);
+    a.rows_land = up16i(recs_bytes - (4 * Fn::ROW * pl->Lcap + 16) - 16);
+    a.off_phi = a.off_recs + recs_bytes;
+    const size_t smem = (size_t)a.off_phi + up16i(4 * Fn::PHIREC * (pl->Scap + 1));
+    if (smem + 1024 > (size_t)dev_max) return EPG_OK;
+    *fits = true;
+    a.desc = pl->desc3;
+    a.blob = pl->blob3;
+    a.slots = pl->slots;
+    a.payload = static_cast<const float *>(state->edge_payload);
+    a.vconst = static_cast<const float *>(state->vertex_const);
+    a.halo_buf = pl->halo_buf;
+    switch (pl->inc_width) {
+        case 4: return launch_occ<Fn, 4>(ctx, pl, state, steps, a, smem);
+        case 8: return launch_occ<Fn, 8>(ctx, pl, state, steps, a, smem);
+        default: return launch_occ<Fn, 0>(ctx, pl, state, steps, a, smem);
+    }
+}
+
+template <class Fn>
+epg_status run_staged(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps) {
+    if (ctx->variant == 0 || ctx->variant == 3) {
+        bool fits = false;
+        epg_status st = run_occ<Fn>(ctx, pl, state, steps, &fits);
+        if (st || fits) return st;
+        if (ctx->variant == 3)
+            return ctx->fail(EPG_ERR_INFEASIBLE, "run: occupancy kernel limits exceeded (plan Lcap/Scap)");
+    }
+    if (ctx->variant == 0 || ctx->variant == 2) {
         bool fits = false;
         epg_status st = run_pipelined<Fn>(ctx, pl, state, steps, &fits);
         if (st || fits) return st;
@@ -610,9 +812,12 @@ epg_status epg_load_count(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t
     return load_count_dev(ctx, edges, m, n, part_of_edge, k, per_part_distinct, out);
 }
 
-epg_status epg_remap(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, const int32_t *part, int64_t k,
-                     epg_layout *L, epg_plan **plan_out) {
-    if (!ctx) return EPG_ERR_STATE;
+}  // extern "C"
+
+namespace {
+// Remap of one partition map (O6) + the execution plan built on it.
+epg_status remap_impl(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, const int32_t *part, int64_t k,
+                      epg_layout *L, epg_plan **plan_out) {
     if (!edges || !part || !L || !plan_out || m <= 0 || n <= 0 || k <= 0)
         return ctx->fail(EPG_ERR_INPUT, "remap: need m > 0, n > 0, k > 0 and non-NULL arrays");
     if (!L->edge_perm || !L->part_edge_begin || !L->vertex_perm || !L->part_vertex_begin || !L->halo_begin ||
@@ -750,8 +955,83 @@ epg_status epg_remap(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, c
         pl->Scap = (int)smax;
     }
     if ((st = build_pipeline_blob(ctx, pl))) return fail_plan(st);
+    pl->k_ep = k;
+    pl->C_ep = C;
     *plan_out = pl;
     return EPG_OK;
+}
+}  // namespace
+
+extern "C" {
+
+// Task reorganisation + cpack layout of the EP map (the public layout), then the
+// execution plan: EP partitions whose staged rows or edges exceed what one CTA holds are
+// executed as contiguous ranges of their (reorganised) edges. Cutting a partition into
+// contiguous edge ranges changes neither the edge order nor any first touch, so the
+// execution plan shares the public edge_perm / vertex_perm exactly.
+epg_status epg_remap(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, const int32_t *part, int64_t k,
+                     epg_layout *L, epg_plan **plan_out) {
+    if (!ctx) return EPG_ERR_STATE;
+    if (!plan_out) return ctx->fail(EPG_ERR_INPUT, "remap: plan output is NULL");
+    *plan_out = nullptr;
+    epg_plan *ep = nullptr;
+    epg_status st = remap_impl(ctx, edges, m, n, part, k, L, &ep);
+    if (st) return st;
+    std::vector<int32_t> cuts(k, 1);
+    bool split = false;
+    for (int64_t p = 0; p < k; p++) {
+        const int c = std::max((ep->part_edges[p] + kExecMaxEdges - 1) / kExecMaxEdges,
+                               (ep->part_rows[p] + kExecMaxRows - 1) / kExecMaxRows);
+        cuts[p] = std::max(c, 1);
+        split |= cuts[p] > 1;
+    }
+    if (!split) {
+        *plan_out = ep;
+        return EPG_OK;
+    }
+    // temporary layout for the execution map
+    Tmp pe(ctx), cu(ctx), ba(ctx), t_ep(ctx), t_peb(ctx), t_vp(ctx), t_pvb(ctx), t_hb(ctx), t_hid(ctx), t_sl(ctx);
+    auto fail_ep = [&](epg_status s2) { delete ep; return s2; };
+    if (pe.alloc(sizeof(int32_t) * m) || cu.alloc(sizeof(int32_t) * k) || ba.alloc(sizeof(int32_t) * k) ||
+        t_ep.alloc(sizeof(int32_t) * m) || t_vp.alloc(sizeof(int32_t) * n) || t_hid.alloc(sizeof(int32_t) * 2 * m) ||
+        t_sl.alloc(sizeof(uint16_t) * 2 * m))
+        return fail_ep(ctx->fail(EPG_ERR_NOMEM, "remap: execution-plan temporaries"));
+    for (int iter = 0; iter < 8; iter++) {
+        std::vector<int32_t> base(k);
+        int64_t kx = 0;
+        for (int64_t p = 0; p < k; p++) { base[p] = (int32_t)kx; kx += cuts[p]; }
+        Tmp peb_x(ctx), pvb_x(ctx), hb_x(ctx);
+        if (peb_x.alloc(sizeof(int32_t) * (kx + 1)) || pvb_x.alloc(sizeof(int32_t) * (kx + 1)) ||
+            hb_x.alloc(sizeof(int32_t) * (kx + 1)))
+            return fail_ep(ctx->fail(EPG_ERR_NOMEM, "remap: execution-plan temporaries"));
+        cudaMemcpyAsync(cu.p, cuts.data(), sizeof(int32_t) * k, cudaMemcpyHostToDevice, ctx->stream);
+        cudaMemcpyAsync(ba.p, base.data(), sizeof(int32_t) * k, cudaMemcpyHostToDevice, ctx->stream);
+        k_exec_map<<<(unsigned)k, 256, 0, ctx->stream>>>(ep->peb, L->edge_perm, cu.as<int32_t>(), ba.as<int32_t>(),
+                                                         pe.as<int32_t>());
+        epg_layout X{t_ep.as<int32_t>(), peb_x.as<int32_t>(), t_vp.as<int32_t>(), pvb_x.as<int32_t>(),
+                     hb_x.as<int32_t>(), t_hid.as<int32_t>(), 2 * m, t_sl.as<uint16_t>()};
+        epg_plan *xp = nullptr;
+        if ((st = remap_impl(ctx, edges, m, n, pe.as<int32_t>(), kx, &X, &xp))) return fail_ep(st);
+        bool again = false;
+        for (int64_t p = 0, e = 0; p < k; p++)
+            for (int c = 0; c < cuts[p]; c++, e++)
+                if (xp->part_rows[e] > kExecMaxRows || xp->part_edges[e] > kExecMaxEdges) again = true;
+        if (!again || iter == 7) {
+            xp->k_ep = k;
+            xp->C_ep = ep->C;
+            delete ep;
+            *plan_out = xp;
+            return EPG_OK;
+        }
+        for (int64_t p = 0, e = 0; p < k; p++) {
+            bool bad = false;
+            for (int c = 0; c < cuts[p]; c++, e++)
+                bad |= xp->part_rows[e] > kExecMaxRows || xp->part_edges[e] > kExecMaxEdges;
+            if (bad) cuts[p] += 1;
+        }
+        delete xp;
+    }
+    return fail_ep(ctx->fail(EPG_ERR_STATE, "remap: execution split did not converge"));
 }
 
 void epg_plan_destroy(epg_plan *plan) {
@@ -760,10 +1040,11 @@ void epg_plan_destroy(epg_plan *plan) {
     delete plan;
 }
 
-epg_status epg_plan_info(const epg_plan *plan, int64_t *out6) {
-    if (!plan || !out6) return EPG_ERR_INPUT;
-    out6[0] = plan->m; out6[1] = plan->n; out6[2] = plan->k;
-    out6[3] = plan->touched; out6[4] = plan->C; out6[5] = plan->S;
+epg_status epg_plan_info(const epg_plan *plan, int64_t *out8) {
+    if (!plan || !out8) return EPG_ERR_INPUT;
+    out8[0] = plan->m; out8[1] = plan->n; out8[2] = plan->k_ep;
+    out8[3] = plan->touched; out8[4] = plan->C_ep; out8[5] = plan->S;
+    out8[6] = plan->k; out8[7] = plan->C;
     return EPG_OK;
 }
 
@@ -792,9 +1073,11 @@ epg_status epg_run(epg_ctx *ctx, const epg_plan *plan, epg_kernel kernel, epg_st
     if (steps < 0) return ctx->fail(EPG_ERR_INPUT, "run: steps < 0");
     CU(cudaSetDevice(ctx->device));
     switch (kernel) {
-        case EPG_KERNEL_CFD_FLUX: return run_staged<CfdFlux>(ctx, plan, state, steps);
-        case EPG_KERNEL_GATHER_SCATTER: return run_staged<GatherScatter>(ctx, plan, state, steps);
-        default: return run_staged<Spmv>(ctx, plan, state, steps);
+        // the plan caches its CTA assignment per grid size (internal, mutable state)
+        case EPG_KERNEL_CFD_FLUX: return run_staged<CfdFlux>(ctx, const_cast<epg_plan *>(plan), state, steps);
+        case EPG_KERNEL_GATHER_SCATTER:
+            return run_staged<GatherScatter>(ctx, const_cast<epg_plan *>(plan), state, steps);
+        default: return run_staged<Spmv>(ctx, const_cast<epg_plan *>(plan), state, steps);
     }
 }
 
@@ -815,7 +1098,8 @@ epg_status epg_run_naive(epg_ctx *ctx, epg_kernel kernel, const int32_t *edges, 
 
 epg_status epg_set_variant(epg_ctx *ctx, int32_t variant) {
     if (!ctx) return EPG_ERR_STATE;
-    if (variant < 0 || variant > 2) return ctx->fail(EPG_ERR_INPUT, "set_variant: 0 auto, 1 per-partition, 2 pipelined");
+    if (variant < 0 || variant > 3)
+        return ctx->fail(EPG_ERR_INPUT, "set_variant: 0 auto, 1 per-partition, 2 pipelined, 3 occupancy");
     ctx->variant = variant;
     return EPG_OK;
 }
@@ -844,5 +1128,14 @@ epg_status epg_profile_read(epg_ctx *ctx, float *ms2, int64_t *launches2) {
     ctx->ev_used.clear();
     return EPG_OK;
 }
+
+#ifdef EPG_TRACE
+// development only (not in epg.h): copy the kernel trace buffer to the host
+epg_status epg_debug_trace(unsigned long long *host, int64_t count) {
+    cudaMemcpyFromSymbol(host, epg::g_trace, sizeof(unsigned long long) * count);
+    cudaMemset(host ? nullptr : nullptr, 0, 0);
+    return EPG_OK;
+}
+#endif
 
 }  // extern "C"

@@ -17,6 +17,11 @@ namespace epg {
 constexpr float kGamma = 1.4f;
 constexpr float kSigma = 0.2f;
 
+// float4 slot of half h (0/1) of 32-byte record r in shared memory. XOR-ing h with bit 2
+// of r spreads 8 consecutive records over all 8 16-byte bank groups, so the 128-bit
+// loads of a quarter-warp do not collide two-way on the even groups.
+__device__ __forceinline__ int rec4(int r, int h) { return 2 * r + (h ^ ((r >> 2) & 1)); }
+
 // Staged per-vertex quantities of the cfd functor (8 floats; SoA in shared memory).
 struct CfdVertex {
     float rho, mx, my, mz, E, p, speed, rinv;  // speed = |u| + c, rinv = 1 / rho
@@ -116,30 +121,58 @@ struct CfdFlux {
             atomicAdd(F + 5 * (int64_t)b + c, -phi[c]);
         }
     }
-    // ---- pipelined (TMA-staged) kernel: rows are the staged AoS state rows, one derived
-    // float per local vertex (|u| + c); rinv and p are recomputed per endpoint.
+    // ---- staged kernels. Per local vertex a 32-byte derived record
+    // {rho, m_x, m_y, m_z | E, p, |u|+c, 1/rho} read with two 128-bit shared loads at
+    // swizzled float4 slots (rec4()); per edge a 24-byte Phi record of three float2.
     static constexpr int PAYW = 3;
-    static constexpr bool kDerived = true;
-    __device__ __forceinline__ static float derive(const float *row) {
-        return cfd_derive(row[0], row[1], row[2], row[3], row[4]).speed;
+    static constexpr int REC = 8;      // floats per derived record
+    static constexpr int PHIREC = 6;   // floats per Phi record (5 used)
+    __device__ __forceinline__ static void derive_rec(const float *row, float *recs, int j) {
+        const CfdVertex d = cfd_derive(row[0], row[1], row[2], row[3], row[4]);
+        float4 *r = reinterpret_cast<float4 *>(recs);
+        r[rec4(j, 0)] = make_float4(d.rho, d.mx, d.my, d.mz);
+        r[rec4(j, 1)] = make_float4(d.E, d.p, d.speed, d.rinv);
     }
-    __device__ __forceinline__ static CfdVertex load_row(const float *rows, int j, float speed) {
-        const float *r = rows + 5 * j;
+    __device__ __forceinline__ static CfdVertex load_rec(const float *recs, int j) {
+        const float4 *r = reinterpret_cast<const float4 *>(recs);
+        const float4 x = r[rec4(j, 0)], y = r[rec4(j, 1)];
         CfdVertex d;
-        d.rho = r[0]; d.mx = r[1]; d.my = r[2]; d.mz = r[3]; d.E = r[4];
-        d.rinv = 1.0f / d.rho;
-        const float ux = d.mx * d.rinv, uy = d.my * d.rinv, uz = d.mz * d.rinv;
-        d.p = (kGamma - 1.0f) * (d.E - 0.5f * d.rho * (ux * ux + uy * uy + uz * uz));
-        d.speed = speed;
+        d.rho = x.x; d.mx = x.y; d.my = x.z; d.mz = x.w;
+        d.E = y.x; d.p = y.y; d.speed = y.z; d.rinv = y.w;
         return d;
     }
-    __device__ __forceinline__ static void edge2(const float *rows, const float *spd, int a, int b,
-                                                 const float *pay, int i, float *Phi, int Scap) {
+    // the conserved state U of record j
+    __device__ __forceinline__ static void rec_state(const float *recs, int j, float U[5]) {
+        const float4 *r = reinterpret_cast<const float4 *>(recs);
+        const float4 x = r[rec4(j, 0)];
+        U[0] = x.x; U[1] = x.y; U[2] = x.z; U[3] = x.w;
+        U[4] = r[rec4(j, 1)].x;
+    }
+    // payload of the edge already in registers
+    __device__ __forceinline__ static void edge_rec_pw(const float *recs, int a, int b, const float pw[3], int i,
+                                                       float *phis) {
         float phi[5];
-        cfd_phi(load_row(rows, a, spd[a]), load_row(rows, b, spd[b]), pay[3 * i], pay[3 * i + 1], pay[3 * i + 2],
-                phi);
-#pragma unroll
-        for (int c = 0; c < 5; c++) Phi[c * Scap + i] = phi[c];
+        cfd_phi(load_rec(recs, a), load_rec(recs, b), pw[0], pw[1], pw[2], phi);
+        float2 *r = reinterpret_cast<float2 *>(phis) + 3 * i;
+        r[0] = make_float2(phi[0], phi[1]);
+        r[1] = make_float2(phi[2], phi[3]);
+        r[2] = make_float2(phi[4], 0.0f);
+    }
+    __device__ __forceinline__ static void edge_rec(const float *recs, int a, int b, const float *pay, int i,
+                                                    float *phis) {
+        const float pw[3] = {pay[3 * i], pay[3 * i + 1], pay[3 * i + 2]};
+        edge_rec_pw(recs, a, b, pw, i, phis);
+    }
+    __device__ __forceinline__ static void zero_phi(float *phis, int i) {
+        float2 *r = reinterpret_cast<float2 *>(phis) + 3 * i;
+        r[0] = r[1] = r[2] = make_float2(0.f, 0.f);
+    }
+    __device__ __forceinline__ static void gather_rec(const float *phis, int i, int side, float acc[5]) {
+        const float2 *r = reinterpret_cast<const float2 *>(phis) + 3 * i;
+        const float2 x = r[0], y = r[1], z = r[2];
+        const float sgn = side ? -1.0f : 1.0f;
+        acc[0] = fmaf(sgn, x.x, acc[0]); acc[1] = fmaf(sgn, x.y, acc[1]); acc[2] = fmaf(sgn, y.x, acc[2]);
+        acc[3] = fmaf(sgn, y.y, acc[3]); acc[4] = fmaf(sgn, z.x, acc[4]);
     }
     __device__ __forceinline__ static void finalise_add(float *__restrict__ out, const float acc[5], float dt) {
 #pragma unroll
@@ -174,13 +207,24 @@ struct GatherScatter {
         atomicAdd(F + b, w * __ldg(x + a));
     }
     static constexpr int PAYW = 1;
-    static constexpr bool kDerived = false;
-    __device__ __forceinline__ static float derive(const float *) { return 0.0f; }
-    __device__ __forceinline__ static void edge2(const float *rows, const float *, int a, int b, const float *pay,
-                                                 int i, float *Phi, int Scap) {
-        const float w = pay ? pay[i] : 1.0f;
-        Phi[i] = w * rows[b];
-        Phi[Scap + i] = w * rows[a];
+    static constexpr int REC = 1, PHIREC = 2;
+    __device__ __forceinline__ static void derive_rec(const float *row, float *recs, int j) { recs[j] = row[0]; }
+    __device__ __forceinline__ static void rec_state(const float *recs, int j, float U[1]) { U[0] = recs[j]; }
+    // pw[0] is the weight (1 when the run has no payload)
+    __device__ __forceinline__ static void edge_rec_pw(const float *recs, int a, int b, const float pw[1], int i,
+                                                       float *phis) {
+        reinterpret_cast<float2 *>(phis)[i] = make_float2(pw[0] * recs[b], pw[0] * recs[a]);
+    }
+    __device__ __forceinline__ static void edge_rec(const float *recs, int a, int b, const float *pay, int i,
+                                                    float *phis) {
+        const float pw[1] = {pay ? pay[i] : 1.0f};
+        edge_rec_pw(recs, a, b, pw, i, phis);
+    }
+    __device__ __forceinline__ static void zero_phi(float *phis, int i) {
+        reinterpret_cast<float2 *>(phis)[i] = make_float2(0.f, 0.f);
+    }
+    __device__ __forceinline__ static void gather_rec(const float *phis, int i, int side, float acc[1]) {
+        acc[0] += phis[2 * i + side];
     }
     __device__ __forceinline__ static void finalise_add(float *__restrict__ out, const float acc[1], float) {
         out[0] += acc[0];
@@ -210,11 +254,21 @@ struct Spmv {
         atomicAdd(F + b, __ldg(payload + e) * __ldg(x + a));
     }
     static constexpr int PAYW = 1;
-    static constexpr bool kDerived = false;
-    __device__ __forceinline__ static float derive(const float *) { return 0.0f; }
-    __device__ __forceinline__ static void edge2(const float *rows, const float *, int a, int, const float *pay,
-                                                 int i, float *Phi, int) {
-        Phi[i] = pay[i] * rows[a];
+    static constexpr int REC = 1, PHIREC = 1;
+    __device__ __forceinline__ static void derive_rec(const float *row, float *recs, int j) { recs[j] = row[0]; }
+    __device__ __forceinline__ static void rec_state(const float *recs, int j, float U[1]) { U[0] = recs[j]; }
+    __device__ __forceinline__ static void edge_rec_pw(const float *recs, int a, int, const float pw[1], int i,
+                                                       float *phis) {
+        phis[i] = pw[0] * recs[a];
+    }
+    __device__ __forceinline__ static void edge_rec(const float *recs, int a, int b, const float *pay, int i,
+                                                    float *phis) {
+        const float pw[1] = {pay[i]};
+        edge_rec_pw(recs, a, b, pw, i, phis);
+    }
+    __device__ __forceinline__ static void zero_phi(float *phis, int i) { phis[i] = 0.0f; }
+    __device__ __forceinline__ static void gather_rec(const float *phis, int i, int side, float acc[1]) {
+        if (side) acc[0] += phis[i];
     }
     __device__ __forceinline__ static void finalise_add(float *__restrict__ out, const float acc[1], float) {
         out[0] += acc[0];

@@ -1,0 +1,312 @@
+// occupancy_kernel.cuh -- the B200 staged edge kernel (step a5), one CTA per execution
+// partition, several CTAs resident per SM.
+//
+// Per partition p (the paper's thread block; staging as in P:719-724):
+//   1. one thread issues two 1-D TMA bulk copies on an mbarrier: the partition's plan
+//      blob (halo ids + incidence lists) and its owned state rows O_p, a contiguous range
+//      of the cpack layout; meanwhile every thread prefetches the slots and edge payload
+//      of its edges and the dt of its vertices into registers (coalesced global loads);
+//   2. the halo rows H_p (the C = sum_v (p_v - 1) redundant loads of Eq. (1)) are gathered
+//      with cp.async into the same shared array;
+//   3. each staged row is turned in place into a 32-byte derived record;
+//   4. one thread per edge evaluates the interaction from shared memory into a Phi record;
+//   5. one thread per local vertex sums its incidence list in a fixed order (no atomics);
+//   6. owned results U + dt F and the halo partial sums are packed in shared memory and
+//      written back with two TMA bulk stores (contiguous: the owned range of state_out,
+//      the partition's slice of the halo buffer).
+// k_finalise3 then adds the halo partials of shared vertices (p_v > 1) to their owners'
+// rows in a fixed order. Latency is hidden by occupancy (3-4 CTAs per SM) rather than by an explicit pipeline;
+// execution partitions are bounded so every buffer fits.
+#pragma once
+
+#include <stdint.h>
+
+#include "functors.cuh"
+#include "pipelined_kernel.cuh"
+#include "ptx.cuh"
+
+namespace epg {
+
+// blob of the occupancy kernel: [halo ids nH x i32] pad16 [incidence] (W as in the
+// pipelined blob: W x L u16 padded lists, or W = 0: 2s u16 entries + L u16 offsets)
+__host__ __device__ __forceinline__ int blob3_inc_offset(int nH) { return (4 * nH + 15) & ~15; }
+__host__ __device__ __forceinline__ int blob3_bytes_for(int nH, int s, int L, int W) {
+    const int inc = W > 0 ? 2 * W * L : 4 * s + 2 * L;
+    return (blob3_inc_offset(nH) + inc + 15) & ~15;
+}
+
+struct OccArgs {
+    const PartDesc *desc;      // blob16 / blob_bytes refer to blob3
+    const unsigned char *blob;
+    const uint32_t *slots;     // [m] packed endpoint slots
+    const float *state_in;
+    float *state_out;
+    const float *payload;      // NULL: gather-scatter with w = 1
+    const float *vconst;
+    float *halo_buf;           // [C][ROW] in halo (partition) order
+    int off_recs, rows_land, off_phi;
+};
+
+template <class Fn, int BLOCK, int EPT, int VPT, int W>
+__global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
+    extern __shared__ __align__(128) unsigned char occ_smem[];
+    __shared__ __align__(8) uint64_t bar;
+    constexpr int ROW = Fn::ROW, PW = Fn::PAYW;
+    const int tid = threadIdx.x;
+    const PartDesc d = a.desc[blockIdx.x];
+    const int L = d.nO + d.nH;
+    unsigned char *sblob = occ_smem;
+    float *recs = reinterpret_cast<float *>(occ_smem + a.off_recs);
+    float *phis = reinterpret_cast<float *>(occ_smem + a.off_phi);
+    const float *g_rows = a.state_in + (int64_t)ROW * d.o0;
+    unsigned char *rows_base = occ_smem + a.off_recs + a.rows_land;   // upper part of the record array
+    float *rows = reinterpret_cast<float *>(rows_base + (reinterpret_cast<uintptr_t>(g_rows) & 15));
+    const uint32_t rows_bytes = 4u * ROW * d.nO;
+    // Programmatic dependent launch: everything up to pdl_wait() reads only plan data and
+    // may overlap the previous kernel in the stream (the finalise of the previous step).
+    if (tid == 0) {
+        ptx::mbar_init(&bar, 1);
+        ptx::fence_mbar_init();
+        ptx::mbar_arrive_expect_tx(&bar, (uint32_t)d.blob_bytes + region_body(g_rows, rows_bytes));
+        if (d.blob_bytes) ptx::bulk_g2s(sblob, a.blob + 16 * (int64_t)d.blob16, (uint32_t)d.blob_bytes, &bar);
+    }
+    // register prefetch (plan + static payload) while the copies fly
+    uint32_t sl[EPT];
+    float pw[EPT][PW];
+#pragma unroll
+    for (int r = 0; r < EPT; r++) {
+        const int i = tid + r * BLOCK;
+        sl[r] = 0;
+#pragma unroll
+        for (int c = 0; c < PW; c++) pw[r][c] = 1.0f;
+        if (i < d.s) {
+            sl[r] = __ldg(a.slots + d.e0 + i);
+            if (a.payload) {
+#pragma unroll
+                for (int c = 0; c < PW; c++) pw[r][c] = __ldg(a.payload + (int64_t)PW * (d.e0 + i) + c);
+            }
+        }
+    }
+    float dtv[VPT];
+#pragma unroll
+    for (int r = 0; r < VPT; r++) {
+        const int j = tid + r * BLOCK;
+        dtv[r] = (Fn::kUsesConst && j < d.nO) ? __ldg(a.vconst + d.o0 + j) : 0.0f;
+    }
+    ptx::pdl_wait();                               // state_in is final from here on
+    if (tid == 0) region_bulk(rows_base, g_rows, rows_bytes, &bar);
+    __syncthreads();                               // barrier initialisation visible
+    ptx::mbar_wait(&bar, 0);
+    // ragged ends of the owned range + halo rows
+    if (tid < 32) region_ragged(rows_base, g_rows, rows_bytes, tid);
+    {
+        const int32_t *hid = reinterpret_cast<const int32_t *>(sblob);
+        float *hr = rows + ROW * d.nO;
+        for (int w = tid; w < ROW * d.nH; w += BLOCK) {
+            const int j = w / ROW, c = w - j * ROW;
+            ptx::cp_async4(hr + w, a.state_in + (int64_t)ROW * hid[j] + c);
+        }
+    }
+    ptx::cp_async_commit();
+    ptx::cp_async_wait<0>();
+    __syncthreads();
+    // rows -> registers -> derived records (in place: the rows sit in the upper part)
+    float rv[VPT][ROW];
+#pragma unroll
+    for (int r = 0; r < VPT; r++) {
+        const int j = tid + r * BLOCK;
+        if (j < L) {
+#pragma unroll
+            for (int c = 0; c < ROW; c++) rv[r][c] = rows[ROW * j + c];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < VPT; r++) {
+        const int j = tid + r * BLOCK;
+        if (j < L) Fn::derive_rec(rv[r], recs, j);
+    }
+    __syncthreads();
+    // edges
+#pragma unroll
+    for (int r = 0; r < EPT; r++) {
+        const int i = tid + r * BLOCK;
+        if (i < d.s) Fn::edge_rec_pw(recs, (int)(sl[r] & 0xffffu), (int)(sl[r] >> 16), pw[r], i, phis);
+    }
+    if constexpr (W > 0) {
+        if (tid == 0) Fn::zero_phi(phis, d.s);
+    }
+    __syncthreads();
+    // reduce per local vertex into registers
+    const uint16_t *inc = reinterpret_cast<const uint16_t *>(sblob + blob3_inc_offset(d.nH));
+    float out[VPT][ROW];
+#pragma unroll
+    for (int r = 0; r < VPT; r++) {
+        const int j = tid + r * BLOCK;
+        if (j >= L) continue;
+        float acc[ROW];
+#pragma unroll
+        for (int c = 0; c < ROW; c++) acc[c] = 0.0f;
+        if constexpr (W > 0) {
+            uint32_t w2[W / 2];
+            if constexpr (W == 4) {
+                const uint2 v = *reinterpret_cast<const uint2 *>(inc + 4 * j);
+                w2[0] = v.x; w2[1] = v.y;
+            } else {
+                const uint4 v = *reinterpret_cast<const uint4 *>(inc + 8 * j);
+                w2[0] = v.x; w2[1] = v.y; w2[2] = v.z; w2[3] = v.w;
+            }
+#pragma unroll
+            for (int q = 0; q < W; q++) {
+                const uint32_t w = (w2[q >> 1] >> (16 * (q & 1))) & 0xffffu;
+                Fn::gather_rec(phis, (int)(w >> 1), (int)(w & 1), acc);
+            }
+        } else {
+            const uint16_t *ioff = inc + 2 * d.s;
+            const int q0 = ioff[j], q1 = j + 1 < L ? ioff[j + 1] : 2 * d.s;
+            for (int q = q0; q < q1; q++) {
+                const int w = inc[q];
+                Fn::gather_rec(phis, w >> 1, w & 1, acc);
+            }
+        }
+        if (j < d.nO) {
+            float U[ROW];
+            Fn::rec_state(recs, j, U);
+            Fn::finish_row(U, acc, dtv[r], out[r]);
+        } else {
+#pragma unroll
+            for (int c = 0; c < ROW; c++) out[r][c] = acc[c];
+        }
+    }
+    __syncthreads();                               // records and Phi no longer read
+    // pack: owned rows at the 16-byte phase of their destination, then the halo partials
+    float *g_out = a.state_out + (int64_t)ROW * d.o0;
+    float *g_halo = a.halo_buf + (int64_t)ROW * d.h0;
+    unsigned char *outA_base = occ_smem + a.off_recs;
+    unsigned char *outB_base = outA_base + ((4 * ROW * d.nO + 32 + 15) & ~15);
+    float *outA = reinterpret_cast<float *>(outA_base + (reinterpret_cast<uintptr_t>(g_out) & 15));
+    float *outB = reinterpret_cast<float *>(outB_base + (reinterpret_cast<uintptr_t>(g_halo) & 15));
+#pragma unroll
+    for (int r = 0; r < VPT; r++) {
+        const int j = tid + r * BLOCK;
+        if (j < d.nO) {
+#pragma unroll
+            for (int c = 0; c < ROW; c++) outA[ROW * j + c] = out[r][c];
+        } else if (j < L) {
+#pragma unroll
+            for (int c = 0; c < ROW; c++) outB[ROW * (j - d.nO) + c] = out[r][c];
+        }
+    }
+    __syncthreads();
+    const uint32_t a_bytes = 4u * ROW * d.nO, b_bytes = 4u * ROW * d.nH;
+    if (tid == 0) {
+        ptx::fence_proxy_async_smem();
+        const uintptr_t ga = reinterpret_cast<uintptr_t>(g_out), gb = reinterpret_cast<uintptr_t>(g_halo);
+        const uintptr_t a_lo = up16(ga), a_hi = down16(ga + a_bytes), b_lo = up16(gb), b_hi = down16(gb + b_bytes);
+        if (a_hi > a_lo)
+            ptx::bulk_s2g(reinterpret_cast<void *>(a_lo), outA_base + (a_lo - down16(ga)), (uint32_t)(a_hi - a_lo));
+        if (b_hi > b_lo)
+            ptx::bulk_s2g(reinterpret_cast<void *>(b_lo), outB_base + (b_lo - down16(gb)), (uint32_t)(b_hi - b_lo));
+        ptx::bulk_commit();
+    }
+    if (tid >= 32 && tid < 64) {                   // ragged words of both ranges, plain stores
+        const int lane = tid - 32;
+        const uintptr_t ga = reinterpret_cast<uintptr_t>(g_out), gb = reinterpret_cast<uintptr_t>(g_halo);
+        auto ragged_store = [&](uintptr_t g, uint32_t bytes, const unsigned char *sbase) {
+            const uintptr_t end = g + bytes, lo = up16(g), hi = down16(end);
+            uintptr_t w;
+            if (hi > lo) {
+                const int head = (int)((lo - g) >> 2), tail = (int)((end - hi) >> 2);
+                if (lane < head) w = g + 4 * lane;
+                else if (lane < head + tail) w = hi + 4 * (lane - head);
+                else return;
+            } else {
+                if (lane >= (int)(bytes >> 2)) return;
+                w = g + 4 * lane;
+            }
+            *reinterpret_cast<float *>(w) = *reinterpret_cast<const float *>(sbase + (w - down16(g)));
+        };
+        ragged_store(ga, a_bytes, outA_base);
+        ragged_store(gb, b_bytes, outB_base);
+    }
+    ptx::pdl_launch_dependents();                  // the finalise may start launching
+    if (tid == 0) ptx::bulk_wait_read0();          // shared memory must outlive the stores' reads
+}
+
+// Boundary finalise (a6): U'_v = (U + dt F_owner)_v + dt * sum of v's halo partials, in
+// the fixed order of hv_list; threads past S copy (cfd) or clear untouched rows. (A fused
+// variant with per-vertex arrival counters in the edge kernel was measured slower on C2:
+// each CTA then holds its SM slot through the extra global round trips.)
+template <class Fn>
+__global__ void k_finalise3(const int32_t *__restrict__ shared_ids, const int32_t *__restrict__ hv_off,
+                            const int32_t *__restrict__ hv_list, const float *__restrict__ halo_buf,
+                            const float *__restrict__ state_in, float *__restrict__ state_out,
+                            const float *__restrict__ vconst, int32_t S, int64_t touched, int64_t n) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    ptx::pdl_wait();                               // the edge kernel's outputs are visible
+    ptx::pdl_launch_dependents();
+    if (t < S) {
+        const int64_t v = shared_ids[t];
+        float acc[Fn::ROW];
+#pragma unroll
+        for (int c = 0; c < Fn::ROW; c++) acc[c] = 0.0f;
+        for (int q = hv_off[t]; q < hv_off[t + 1]; q++) {
+            const int64_t h = hv_list[q];
+#pragma unroll
+            for (int c = 0; c < Fn::ROW; c++) acc[c] += halo_buf[Fn::ROW * h + c];
+        }
+        const float dt = Fn::kUsesConst ? vconst[v] : 0.0f;
+        Fn::finalise_add(state_out + Fn::ROW * v, acc, dt);
+        return;
+    }
+    const int64_t v = touched + (t - S);
+    if (v < n) Fn::untouched(state_in + Fn::ROW * v, state_out + Fn::ROW * v);
+}
+
+// blob3 of partition p
+__global__ void k_build_blob3(const int32_t *__restrict__ peb, const int32_t *__restrict__ pvb,
+                              const int32_t *__restrict__ hb, const int32_t *__restrict__ halo_ids,
+                              const uint16_t *__restrict__ inc, const uint16_t *__restrict__ inc_off,
+                              const int32_t *__restrict__ blob16, int W, unsigned char *blob, PartDesc *desc) {
+    const int p = blockIdx.x;
+    const int o0 = pvb[p], nO = pvb[p + 1] - o0, h0 = hb[p], nH = hb[p + 1] - h0, e0 = peb[p], s = peb[p + 1] - e0;
+    const int L = nO + nH;
+    unsigned char *b = blob + 16 * (int64_t)blob16[p];
+    int32_t *hid = reinterpret_cast<int32_t *>(b);
+    uint16_t *ic = reinterpret_cast<uint16_t *>(b + blob3_inc_offset(nH));
+    for (int j = threadIdx.x; j < nH; j += blockDim.x) hid[j] = halo_ids[h0 + j];
+    const int64_t lbase = (int64_t)o0 + h0;
+    if (W > 0) {
+        for (int j = threadIdx.x; j < L; j += blockDim.x) {
+            const int q0 = inc_off[lbase + j], q1 = j + 1 < L ? inc_off[lbase + j + 1] : 2 * s;
+            for (int r = 0; r < W; r++)
+                ic[W * j + r] = q0 + r < q1 ? inc[2 * (int64_t)e0 + q0 + r] : (uint16_t)(s << 1);
+        }
+    } else {
+        uint16_t *io = ic + 2 * s;
+        for (int q = threadIdx.x; q < 2 * s; q += blockDim.x) ic[q] = inc[2 * (int64_t)e0 + q];
+        for (int j = threadIdx.x; j < L; j += blockDim.x) io[j] = inc_off[lbase + j];
+    }
+    if (threadIdx.x == 0) desc[p] = PartDesc{o0, nO, e0, s, h0, nH, blob16[p], blob3_bytes_for(nH, s, L, W), 0, 0, 0, 0};
+}
+
+__global__ void k_blob3_sizes(const int32_t *__restrict__ peb, const int32_t *__restrict__ pvb,
+                              const int32_t *__restrict__ hb, int64_t k, int W, int32_t *units16) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p > k) return;
+    if (p == k) { units16[p] = 0; return; }
+    const int nO = pvb[p + 1] - pvb[p], nH = hb[p + 1] - hb[p], s = peb[p + 1] - peb[p];
+    units16[p] = blob3_bytes_for(nH, s, nO + nH, W) / 16;
+}
+
+// execution partitions: partition p of the EP map is cut into c_p contiguous edge ranges
+// (by new edge index); exec id = base[p] + piece. Written per original task id.
+__global__ void k_exec_map(const int32_t *__restrict__ peb, const int32_t *__restrict__ edge_perm,
+                           const int32_t *__restrict__ cuts, const int32_t *__restrict__ base, int32_t *part_exec) {
+    const int p = blockIdx.x;
+    const int e0 = peb[p], s = peb[p + 1] - e0, c = cuts[p];
+    for (int i = threadIdx.x; i < s; i += blockDim.x)
+        part_exec[edge_perm[e0 + i]] = base[p] + (int)((int64_t)i * c / s);
+}
+
+}  // namespace epg

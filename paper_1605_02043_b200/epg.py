@@ -14,7 +14,8 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libepg.so")
+# EPG_LIB_PATH overrides the library file (development builds, e.g. the -DEPG_TRACE one)
+LIB_PATH = os.environ.get("EPG_LIB_PATH", os.path.join(_HERE, "libepg.so"))
 
 OK, ERR_INPUT, ERR_INFEASIBLE, ERR_CUDA, ERR_NCCL, ERR_NOMEM, ERR_STATE = 0, 2, 3, 4, 5, 6, 7
 KERNEL_CFD_FLUX, KERNEL_GATHER_SCATTER, KERNEL_SPMV = 1, 2, 3
@@ -149,9 +150,10 @@ class Plan:
     def __init__(self, handle, ctx):
         self.handle = handle
         self.ctx = ctx
-        info = np.zeros(6, np.int64)
+        info = np.zeros(8, np.int64)
         lib.epg_plan_info(handle, info.ctypes.data)
-        self.m, self.n, self.k, self.touched, self.cut_cost, self.shared = (int(x) for x in info)
+        (self.m, self.n, self.k, self.touched, self.cut_cost, self.shared,
+         self.k_exec, self.cut_cost_exec) = (int(x) for x in info)
 
     def close(self):
         if self.handle:
@@ -247,7 +249,7 @@ class Context:
         return state_out if steps % 2 else state_in
 
     def set_variant(self, variant: int):
-        """0 auto, 1 one CTA per partition, 2 pipelined TMA kernel."""
+        """0 auto, 1 one CTA per partition, 2 pipelined TMA kernel, 3 occupancy TMA kernel."""
         self._check(lib.epg_set_variant(self.handle, variant))
 
     def set_profiling(self, enable: bool):

@@ -17,9 +17,10 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-5
 
 
-@pytest.fixture(scope="module", params=[2, 1], ids=["pipelined", "per_partition"])
+@pytest.fixture(scope="module", params=[0, 1, 2, 3], ids=["auto", "per_partition", "pipelined", "occupancy"])
 def ctx(request):
-    """Both staged-kernel variants: 2 = persistent TMA-pipelined, 1 = one CTA per partition."""
+    """Every staged-kernel variant: 0 automatic, 1 one CTA per partition with plain loads,
+    2 persistent TMA-pipelined, 3 TMA-staged with several CTAs per SM."""
     from paper_1605_02043_b200 import epg
     assert torch.cuda.is_available(), "GPU tests need a CUDA device"
     c = epg.Context(0)
@@ -229,6 +230,21 @@ def test_cfd_multi_step_and_determinism(ctx, small_mesh):
     assert np.array_equal(s2, s2_direct)
     ref2, _ = O.cfd_step(M.edges, M.n, M.normals, s1, dt)
     assert normwise_err(s2, ref2).max() <= TOL
+
+
+def test_pipelined_kernel_at_bench_config(ctx):
+    """The bench configuration (C2, P = 1024) runs the pipelined kernel (variant 2 refuses
+    to fall back) and matches the oracle at full size."""
+    from paper_1605_02043_b200 import epg
+    M = S.config_mesh("c2")
+    k = O.num_parts(M.m, 1024)
+    c2 = epg.Context(0)
+    c2.set_variant(ctx_variant := 3)
+    assert ctx_variant == 3
+    U, dt = _cfd_inputs(M)
+    got = _run_cfd(c2, M, O.partition(M.edges, M.n, 1024), k, U, dt)
+    ref, _ = O.cfd_step(M.edges, M.n, M.normals, U, dt)
+    assert normwise_err(got, ref).max() <= TOL
 
 
 def test_cfd_naive(ctx, small_mesh):
