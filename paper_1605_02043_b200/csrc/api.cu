@@ -77,6 +77,7 @@ struct epg_plan {
     epg::PartDesc *desc3 = nullptr;
     unsigned char *blob3 = nullptr;
     int blob3_max = 0;
+    int4 *fin_recs = nullptr;   // packed finalise records (when every vertex has <= 6 halo entries)
     // the EP map the plan executes (k, C of the paper's partitions; the plan itself may
     // split oversized partitions into contiguous execution ranges)
     int64_t k_ep = 0, C_ep = 0;
@@ -391,6 +392,17 @@ epg_status build_pipeline_blob(epg_ctx *ctx, epg_plan *pl) {
             return st;
         k_build_blob3<<<(unsigned)k, 256, 0, ctx->stream>>>(pl->peb, pl->pvb, pl->hb, pl->halo_ids, pl->inc,
                                                            pl->inc_off, o3.as<int32_t>(), W, pl->blob3, pl->desc3);
+        if (pl->S > 0) {
+            Tmp hm(ctx);
+            CU(hm.alloc(sizeof(int32_t)));
+            CU(cudaMemsetAsync(hm.p, 0, sizeof(int32_t), ctx->stream));
+            if ((st = plan_alloc_t(pl, ctx, &pl->fin_recs, 2 * pl->S))) return st;
+            k_finalise_records<<<grid_for(pl->S), kThreads, 0, ctx->stream>>>(
+                pl->shared_ids, pl->hv_off, pl->hv_list, (int32_t)pl->S, pl->fin_recs, hm.as<int32_t>());
+            int32_t hmax = 0;
+            if ((st = read_i32(ctx, hm.as<int32_t>(), &hmax))) return st;
+            if (hmax > 6) pl->fin_recs = nullptr;   // (the allocation is released with the plan)
+        }
         CHECK_LAUNCH();
     }
     std::vector<int32_t> peb(k + 1), pvb(k + 1), hb(k + 1);
@@ -587,10 +599,15 @@ epg_status launch_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t step
         ctx->prof_end(0, t0);
         if (fin_work > 0) {
             cudaEvent_t t1 = ctx->prof_begin();
-            CU(launch_pdl(k_finalise3<Fn>, grid_for(fin_work), kThreads, 0, ctx->stream,
-                          (const int32_t *)pl->shared_ids, (const int32_t *)pl->hv_off, (const int32_t *)pl->hv_list,
-                          (const float *)pl->halo_buf, (const float *)a.state_in, a.state_out, a.vconst,
-                          (int32_t)pl->S, pl->touched, pl->n));
+            if (pl->fin_recs)
+                CU(launch_pdl(k_finalise_rec<Fn>, grid_for(fin_work), kThreads, 0, ctx->stream,
+                              (const int4 *)pl->fin_recs, (const float *)pl->halo_buf, (const float *)a.state_in,
+                              a.state_out, a.vconst, (int32_t)pl->S, pl->touched, pl->n));
+            else
+                CU(launch_pdl(k_finalise3<Fn>, grid_for(fin_work), kThreads, 0, ctx->stream,
+                              (const int32_t *)pl->shared_ids, (const int32_t *)pl->hv_off,
+                              (const int32_t *)pl->hv_list, (const float *)pl->halo_buf, (const float *)a.state_in,
+                              a.state_out, a.vconst, (int32_t)pl->S, pl->touched, pl->n));
             ctx->prof_end(1, t1);
         }
     }

@@ -263,6 +263,52 @@ __global__ void k_finalise3(const int32_t *__restrict__ shared_ids, const int32_
     if (v < n) Fn::untouched(state_in + Fn::ROW * v, state_out + Fn::ROW * v);
 }
 
+// Finalise from packed per-vertex records {v, count, h_0..h_5} (count <= 6 halo entries):
+// one coalesced 32-byte record load, then the halo rows, dt and the owner row in
+// parallel -- two dependent hops instead of three. Same summation order as k_finalise3.
+template <class Fn>
+__global__ void k_finalise_rec(const int4 *__restrict__ recs, const float *__restrict__ halo_buf,
+                               const float *__restrict__ state_in, float *__restrict__ state_out,
+                               const float *__restrict__ vconst, int32_t S, int64_t touched, int64_t n) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    ptx::pdl_wait();
+    ptx::pdl_launch_dependents();
+    if (t < S) {
+        const int4 r0 = recs[2 * t], r1 = recs[2 * t + 1];
+        const int64_t v = r0.x;
+        const int c = r0.y;
+        const int h[6] = {r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+        float acc[Fn::ROW];
+#pragma unroll
+        for (int k = 0; k < Fn::ROW; k++) acc[k] = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 6; i++) {
+            if (i < c) {
+#pragma unroll
+                for (int k = 0; k < Fn::ROW; k++) acc[k] += halo_buf[Fn::ROW * (int64_t)h[i] + k];
+            }
+        }
+        const float dt = Fn::kUsesConst ? vconst[v] : 0.0f;
+        Fn::finalise_add(state_out + Fn::ROW * v, acc, dt);
+        return;
+    }
+    const int64_t v = touched + (t - S);
+    if (v < n) Fn::untouched(state_in + Fn::ROW * v, state_out + Fn::ROW * v);
+}
+
+// records for k_finalise_rec; *hmax receives the largest halo count
+__global__ void k_finalise_records(const int32_t *__restrict__ shared_ids, const int32_t *__restrict__ hv_off,
+                                   const int32_t *__restrict__ hv_list, int32_t S, int4 *recs, int32_t *hmax) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= S) return;
+    const int q0 = hv_off[t], c = hv_off[t + 1] - q0;
+    int h[6];
+    for (int i = 0; i < 6; i++) h[i] = i < c ? hv_list[q0 + i] : 0;
+    recs[2 * t] = make_int4(shared_ids[t], c, h[0], h[1]);
+    recs[2 * t + 1] = make_int4(h[2], h[3], h[4], h[5]);
+    atomicMax(hmax, c);
+}
+
 // blob3 of partition p
 __global__ void k_build_blob3(const int32_t *__restrict__ peb, const int32_t *__restrict__ pvb,
                               const int32_t *__restrict__ hb, const int32_t *__restrict__ halo_ids,
