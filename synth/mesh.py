@@ -65,8 +65,8 @@ def _tet_vertices(cell: np.ndarray, N: int, h: float):
     return v0, v1, v2, v3
 
 
-def _faces(N: int):
-    """All interior faces of the full N^3 Kuhn box as (cell_a, cell_b, kind).
+def _faces(N: int, c0: int = 0, c1: int | None = None):
+    """Interior faces of the N^3 Kuhn box with first cell in [c0, c1), as (cell_a, cell_b, kind).
 
     kind 1: face opposite v1 of a (shared with the tet of the same cube, pi0<->pi1);
     kind 2: face opposite v2 of a (same cube, pi1<->pi2);
@@ -74,7 +74,8 @@ def _faces(N: int):
     Intra-cube pairs are emitted once (q < q'); cross-cube faces once, from the v0 side.
     """
     ncell = 6 * N ** 3
-    cell = np.arange(ncell, dtype=np.int64)
+    c1 = ncell if c1 is None else c1
+    cell = np.arange(c0, c1, dtype=np.int64)
     q = cell % 6
     base = cell - q
     out_a, out_b, out_k = [], [], []
@@ -83,49 +84,67 @@ def _faces(N: int):
         sel = q < q2
         out_a.append(cell[sel]); out_b.append((base + q2)[sel]); out_k.append(np.full(int(sel.sum()), kind, np.int8))
     c = cell // 6
-    coord = np.stack([c % N, (c // N) % N, c // (N * N)], axis=1)
     ax = PERMS[q, 0]
-    ok = coord[np.arange(ncell), ax] < N - 1
     stride = np.array([1, N, N * N], dtype=np.int64)
+    coord_ax = (c // stride[ax]) % N
+    ok = coord_ax < N - 1
     nb = (c + stride[ax]) * 6 + ROT[q]
     out_a.append(cell[ok]); out_b.append(nb[ok]); out_k.append(np.zeros(int(ok.sum()), np.int8))
     return np.concatenate(out_a), np.concatenate(out_b), np.concatenate(out_k)
 
 
-def kuhn_mesh(nbox: int, n_keep: int | None = None, seed: int = 1605, relabel: bool = True) -> Mesh:
+def _normals(a, kind, N, h):
+    """Area-normal of the face `kind` of cells a, oriented out of a (float64 [len, 3])."""
+    v0, v1, v2, v3 = _tet_vertices(a, N, h)
+    k0 = (kind == 0)[:, None]
+    k1 = (kind == 1)[:, None]
+    f0 = np.where(k0, v1, v0)
+    f1 = np.where(k0, v2, np.where(k1, v2, v1))
+    opp = np.where(k0, v0, np.where(k1, v1, v2))
+    nrm = 0.5 * np.cross(f1 - f0, v3 - f0)
+    flip = np.einsum("ij,ij->i", nrm, f0 - opp) < 0
+    nrm[flip] *= -1.0
+    return nrm
+
+
+def kuhn_mesh(nbox: int, n_keep: int | None = None, seed: int = 1605, relabel: bool = True,
+              chunk: int = 1 << 23) -> Mesh:
     N = int(nbox)
     ncell = 6 * N ** 3
     n = ncell if n_keep is None else int(n_keep)
     if not (1 <= n <= ncell):
         raise ValueError(f"n_keep must be in [1, {ncell}]")
     h = 1.0 / N
-    a, b, kind = _faces(N)
-    keep = (a < n) & (b < n)
-    a, b, kind = a[keep], b[keep], kind[keep]
-    # area-normal of the shared face, oriented out of cell a
-    v0, v1, v2, v3 = _tet_vertices(a, N, h)
-    f0 = np.where((kind == 0)[:, None], v1, v0)
-    f1 = np.where((kind == 1)[:, None], v2, v1)
-    f1 = np.where((kind == 0)[:, None], v2, f1)
-    f2 = v3
-    opp = np.where((kind == 0)[:, None], v0, np.where((kind == 1)[:, None], v1, v2))
-    del v0, v1, v2, v3
-    nrm = 0.5 * np.cross(f1 - f0, f2 - f0)
-    flip = np.einsum("ij,ij->i", nrm, f0 - opp) < 0
-    nrm[flip] *= -1.0
-    del f0, f1, f2, opp
     if relabel:
         order = random_permutation(seed, n)          # order[j] = old id of new id j
         new = np.empty(n, dtype=np.int64)
         new[order] = np.arange(n, dtype=np.int64)
-        a, b = new[a], new[b]
-    swap = a > b
-    lo = np.where(swap, b, a)
-    hi = np.where(swap, a, b)
-    nrm[swap] *= -1.0
-    idx = np.lexsort((hi, lo))
-    edges = np.stack([lo[idx], hi[idx]], axis=1).astype(np.int32)
-    normals = nrm[idx].astype(np.float32)
+        del order
+    los, his, nrms = [], [], []
+    # faces are emitted from their first cell, which is < n when both cells are kept
+    for c0 in range(0, n, chunk):
+        a, b, kind = _faces(N, c0, min(n, c0 + chunk))
+        keep = b < n
+        a, b, kind = a[keep], b[keep], kind[keep]
+        nrm = _normals(a, kind, N, h)
+        if relabel:
+            a, b = new[a], new[b]
+        swap = a > b
+        nrm[swap] *= -1.0
+        los.append(np.where(swap, b, a).astype(np.int32))
+        his.append(np.where(swap, a, b).astype(np.int32))
+        nrms.append(nrm.astype(np.float32))
+        del a, b, kind, nrm, swap
+    lo = np.concatenate(los); del los
+    hi = np.concatenate(his); del his
+    nrm = np.concatenate(nrms); del nrms
+    idx = np.argsort(lo.astype(np.int64) * n + hi, kind="stable")
+    edges = np.empty((lo.size, 2), dtype=np.int32)
+    edges[:, 0] = lo[idx]
+    edges[:, 1] = hi[idx]
+    del lo, hi
+    normals = nrm[idx]
+    del nrm, idx
     volume = np.full(n, h ** 3 / 6.0)
     return Mesh(n=n, m=int(edges.shape[0]), edges=edges, normals=normals, volume=volume, h=h, seed=seed)
 
