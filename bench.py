@@ -13,9 +13,11 @@ application loop -- and are timed separately ("setup").
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--config c1|c2|c3] [--part-size P]
 
-N > 1 (torchrun): every rank runs an independent replica of the workload (weak
-scaling, no data-path collective); the sharded mesh with the NCCL halo exchange of
-SURVEY §8(e) is not built yet.
+N > 1 (torchrun): weak scaling of the sharded path. The mesh has N times the
+C2 cell count (a Kuhn box truncated to N x 232,536 cells); hierarchical EPG-1 with shards = N
+gives each GPU a contiguous range of partitions; every step pulls the halo rows owned by
+lower shards and pushes per-vertex partial sums back to their owners with grouped NCCL
+send/recv (paper_1605_02043_b200/shard.py), so each GPU keeps a C2-sized share of the work.
 """
 from __future__ import annotations
 
@@ -53,6 +55,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="bounded oracle sample for cpu_baseline")
     ap.add_argument("--no-comparators", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="run the multi-GPU (sharded, halo-exchange) step even at N = 1")
     return ap.parse_args()
 
 
@@ -213,6 +217,130 @@ def timed_steps(torch, ctx, stream, K, step_fn, flush):
     return sum(a.elapsed_time(b) for a, b in evs)
 
 
+def run_sharded(args, rank, local_rank, world):
+    """N GPUs, one process each: weak scaling with the halo exchange of SURVEY §8(e)."""
+    import math
+
+    import torch
+    import torch.distributed as dist
+
+    import synth as S
+    from paper_1605_02043_b200 import epg
+    from paper_1605_02043_b200.shard import Comm, Shard
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        dist.barrier()        # a collective before the first batched p2p (NCCL requirement)
+    stream = torch.cuda.current_stream(dev)
+    ctx = epg.Context(local_rank, stream)
+    K, W, P = args.steps, args.warmup, args.part_size
+    clocks = ClockSampler(local_rank)
+    base = S.CONFIGS[args.config]
+    n_keep = base["n_keep"] * world
+    nbox = base["nbox"] if world == 1 else math.ceil((n_keep / 6) ** (1.0 / 3.0))
+    t0 = time.perf_counter()
+    M = S.kuhn_mesh(nbox=nbox, n_keep=n_keep)
+    U, dt = S.cfd_state(M.n), S.cfd_dt(M.volume)
+    t_gen = time.perf_counter() - t0
+    E = torch.from_numpy(M.edges).to(dev)
+    k = epg.num_parts(M.m, P)
+    t0 = time.perf_counter()
+    part, rep = ctx.partition(E, M.n, P, shards=world)        # hierarchical EPG-1, identical on all ranks
+    t_part = time.perf_counter() - t0
+    L, plan = ctx.remap(E, M.n, part, k, halo_cap=rep.cut_cost)
+    sh = Shard(ctx, plan, L, epg.KERNEL_CFD_FLUX, world, rank)
+    comm = Comm()
+    Ud = torch.from_numpy(U).to(dev)
+    nrm = ctx.permute_rows(torch.from_numpy(M.normals).to(dev), L.edge_perm, epg.PERM_GATHER)
+    dtn = ctx.permute_rows(torch.from_numpy(dt).to(dev), L.vertex_perm, epg.PERM_SCATTER)
+    bufs = [ctx.permute_rows(Ud, L.vertex_perm, epg.PERM_SCATTER), torch.empty_like(Ud)]
+    flushbuf = torch.empty(args.flush_mib * (1 << 20) // 4, dtype=torch.float32, device=dev)
+
+    def flush():
+        flushbuf.fill_(1.0)
+
+    def step(i):
+        sh.step(comm, bufs[i & 1], bufs[(i + 1) & 1], nrm, dtn)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for i in range(W):
+        step(i)
+    barrier()
+    with clocks.window():
+        tot = timed_steps(torch, ctx, stream, K, lambda i: step(i + W), flush)
+    barrier()
+    step_ms = max_over_ranks(tot / K)
+    value = M.m / (step_ms * 1e-3)
+    ctx.set_profiling(True)
+    ctx.profile_read()
+    timed_steps(torch, ctx, stream, K, step, flush)
+    (edge_ms, fin_ms), (n_edge, n_fin) = ctx.profile_read()
+    ctx.set_profiling(False)
+    launches = (n_edge + n_fin) + K * 2 * (len(sh.send_ids) + len(sh.recv_ids))   # + pack/unpack/reduce
+    # e2e: each rank's owned rows from pinned host, the result's owned rows back
+    lo, hi = sh.owned()
+    Uh = bufs[0][lo:hi].cpu().pin_memory()
+    Oh = torch.empty_like(Uh).pin_memory()
+
+    def e2e_step(i):
+        bufs[0][lo:hi].copy_(Uh, non_blocking=True)
+        sh.step(comm, bufs[0], bufs[1], nrm, dtn)
+        Oh.copy_(bufs[1][lo:hi], non_blocking=True)
+
+    barrier()
+    with clocks.window():
+        e2e_ms = max_over_ranks(timed_steps(torch, ctx, stream, K, e2e_step, flush) / K)
+    barrier()
+    halo_rows = sum(v.numel() for v in sh.recv_ids.values()) + sum(v.numel() for v in sh.send_ids.values())
+    clk = clocks.summary()
+    if rank == 0:
+        peak, peak_src = measured_peaks()
+        B = alg_bytes_per_step(M.m, rep.touched)
+        achieved = B / world / ((edge_ms / K) * 1e-3) / 1e9
+        line = {
+            "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{args.config.upper()}-sized cfd Kuhn mesh per GPU: {M.n:,} cells, {M.m:,} "
+                                   f"interior faces in total", "part_size": P, "k": k, "functor": "cfd_flux",
+                       "schedule": f"hierarchical EPG-1, shards = {world}",
+                       "step": "halo pull (NCCL) + epg_run_edges + partial push (NCCL) + epg_run_finalise",
+                       "l2": f"flushed between timed steps ({args.flush_mib} MiB write)",
+                       "parallelism": f"graph shards x{world}, NCCL p2p halo exchange"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "k_edge_occ<CfdFlux> on rank 0 (its share of the compulsory bytes)",
+                         "edge_kernel_ms": edge_ms / K, "finalise_ms": fin_ms / K, "peak_source": peak_src},
+            "cpu_baseline": None,
+            "e2e": {"value": M.m / (e2e_ms * 1e-3), "unit": "edges/s",
+                    "h2d_bytes_per_step": Uh.numel() * 4, "d2h_bytes_per_step": Oh.numel() * 4,
+                    "ms_per_step": e2e_ms, "note": "rank 0's owned rows; every rank moves its own"},
+            "gpu_launches": launches,
+            "clocks": clk,
+            "partition": {"load_count": rep.load_count, "touched": rep.touched, "cut_cost": rep.cut_cost,
+                          "replication": rep.replication, "halo_rows_rank0": halo_rows,
+                          "host_partition_s": t_part, "mesh_gen_s": t_gen},
+            "seeds": {"mesh": 1605, "state": 1606},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def run_ours(args, rank, local_rank, world):
     import torch
     import torch.distributed as dist
@@ -220,6 +348,8 @@ def run_ours(args, rank, local_rank, world):
     import synth as S
     from paper_1605_02043_b200 import epg
 
+    if world > 1 or args.force_sharded:
+        return run_sharded(args, rank, local_rank, world)
     torch.cuda.set_device(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))

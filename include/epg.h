@@ -214,6 +214,44 @@ epg_status epg_run(epg_ctx *ctx, const epg_plan *plan, epg_kernel kernel, epg_st
 epg_status epg_run_naive(epg_ctx *ctx, epg_kernel kernel, const int32_t *edges, int64_t m, int32_t n_vertices,
                          epg_state *state, int32_t steps);
 
+/* -- multi-GPU shards (the paper is single-GPU) ------------------------ */
+/* Shard g of G holds the EP partitions [floor(gk/G), floor((g+1)k/G)) (hierarchical EPG-1
+ * with shards = G keeps them contiguous in the graph), owns the vertices their cpack ranges
+ * cover, and per time step: pulls the halo rows owned by lower shards (Halo^{g<-g'}), runs
+ * epg_run_edges on its execution partitions, pushes per-vertex partial sums
+ * (epg_shard_reduce) to the owners, accumulates the ones it receives in ascending peer order
+ * (epg_accumulate_rows) and finalises its shared vertices (epg_run_finalise). Every rank
+ * holds the same plan and full-size state arrays; only owned rows are authoritative.
+ *
+ * out8 = execution partitions first, count; halo positions first, count; owned vertices
+ * first, count; shared vertices (index into the plan's shared list) first, count. */
+epg_status epg_shard_ranges(const epg_plan *plan, int32_t G, int32_t g, int64_t *out8);
+/* Halo sets O7 from the layout of the EP map (HOST arrays pvb [k+1], halo_begin [k+1],
+ * halo_ids): begin_out [G*G+1]; ids of Halo^{g<-g'} at begin_out[g*G+g'] .. [g*G+g'+1]
+ * (ascending; non-empty only for g' < g). ids_out may be NULL to count (*count_out). */
+epg_status epg_shard_halos_host(const int32_t *part_vertex_begin, const int32_t *halo_begin, const int32_t *halo_ids,
+                                int64_t k, int32_t G, int32_t *begin_out, int32_t *ids_out, int64_t cap,
+                                int64_t *count_out);
+/* The staged edge kernel over execution partitions [first, first + count) (no finalise):
+ * writes U + dt F_local into the owned rows of state_out and the halo partials into the
+ * plan's halo buffer. Requires the default (occupancy) kernel's limits. */
+epg_status epg_run_edges(epg_ctx *ctx, const epg_plan *plan, epg_kernel kernel, epg_state *state, int64_t first,
+                         int64_t count);
+/* Boundary finalise of the shared vertices [shared_first, +shared_count) of the plan's
+ * shared list: state_out[v] += dt_v * (halo partials at positions in [halo_first,
+ * +halo_count), ascending, then acc[v]); acc (DEVICE [n][row], or NULL) is cleared on
+ * the way. untouched != 0 also copies (cfd) / clears untouched rows. */
+epg_status epg_run_finalise(epg_ctx *ctx, const epg_plan *plan, epg_kernel kernel, epg_state *state,
+                            int64_t shared_first, int64_t shared_count, int64_t halo_first, int64_t halo_count,
+                            float *acc, int32_t untouched);
+/* out_rows[i] = sum of the halo partials of vertex ids[i] at positions in [halo_first,
+ * +halo_count), ascending (DEVICE arrays; ids [count], out_rows [count][row]). */
+epg_status epg_shard_reduce(epg_ctx *ctx, const epg_plan *plan, epg_kernel kernel, const int32_t *ids, int64_t count,
+                            int64_t halo_first, int64_t halo_count, float *out_rows);
+/* acc[ids[i]] += src[i], rows of row_floats floats; ids distinct (DEVICE arrays). */
+epg_status epg_accumulate_rows(epg_ctx *ctx, const float *src, const int32_t *ids, int64_t count, int32_t row_floats,
+                               float *acc);
+
 /* Kernel variant used by epg_run: 0 = automatic (the first of 3, 2, 1 whose buffers fit),
  * 1 = one CTA per partition (plain loads), 2 = persistent pipelined TMA kernel, 3 = TMA
  * kernel with one CTA per execution partition and several CTAs per SM. 2 and 3 return

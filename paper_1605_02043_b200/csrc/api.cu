@@ -82,6 +82,9 @@ struct epg_plan {
     // split oversized partitions into contiguous execution ranges)
     int64_t k_ep = 0, C_ep = 0;
     std::vector<int32_t> part_rows, part_edges;   // |V_p| and s_p of the plan's partitions
+    std::vector<int32_t> exec_base;               // [k_ep + 1] first execution partition of each EP partition
+    std::vector<int32_t> pvb_h, hb_h;             // host copies of the execution plan's beginA / halo_begin
+    std::vector<int32_t> shared_h;                // host copy of shared_ids (lazy, for shard ranges)
     int assign_grid = 0;                          // grid size the assignment was built for
     unsigned long long *bar_ctr = nullptr;        // grid barrier counter (monotone)
     unsigned long long bar_gen = 0;               // launches so far
@@ -427,6 +430,8 @@ epg_status build_pipeline_blob(epg_ctx *ctx, epg_plan *pl) {
     }
     pl->Ocap = ocap;
     pl->Hcap = hcap;
+    pl->pvb_h = pvb;
+    pl->hb_h = hb;
     pl->blob_max = bmax;
     return EPG_OK;
 }
@@ -635,11 +640,66 @@ epg_status run_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, 
     a.payload = static_cast<const float *>(state->edge_payload);
     a.vconst = static_cast<const float *>(state->vertex_const);
     a.halo_buf = pl->halo_buf;
+    a.first = 0;
     switch (pl->inc_width) {
         case 4: return launch_occ<Fn, 4>(ctx, pl, state, steps, a, smem);
         case 8: return launch_occ<Fn, 8>(ctx, pl, state, steps, a, smem);
         default: return launch_occ<Fn, 0>(ctx, pl, state, steps, a, smem);
     }
+}
+
+// edge kernel over execution partitions [first, first + count) only (no finalise)
+template <class Fn>
+epg_status run_edges_range(epg_ctx *ctx, epg_plan *pl, epg_state *state, int64_t first, int64_t count) {
+    if (pl->Scap > kExecMaxEdges || pl->Lcap > kExecMaxRows)
+        return ctx->fail(EPG_ERR_INFEASIBLE, "run_edges: plan exceeds the occupancy kernel limits");
+    OccArgs a{};
+    a.off_recs = up16i(pl->blob3_max);
+    const int recs_bytes = up16i(4 * Fn::REC * pl->Lcap + 64);
+    a.rows_land = up16i(recs_bytes - (4 * Fn::ROW * pl->Lcap + 16) - 16);
+    a.off_phi = a.off_recs + recs_bytes;
+    const size_t smem = (size_t)a.off_phi + up16i(4 * Fn::PHIREC * (pl->Scap + 1));
+    a.desc = pl->desc3;
+    a.blob = pl->blob3;
+    a.slots = pl->slots;
+    a.state_in = static_cast<const float *>(state->state_in);
+    a.state_out = static_cast<float *>(state->state_out);
+    a.payload = static_cast<const float *>(state->edge_payload);
+    a.vconst = static_cast<const float *>(state->vertex_const);
+    a.halo_buf = pl->halo_buf;
+    a.first = first;
+    if (count <= 0) return EPG_OK;
+    auto go = [&](auto kern) -> epg_status {
+        CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        cudaEvent_t t0 = ctx->prof_begin();
+        CU(launch_pdl(kern, (unsigned)count, kOccThreads, smem, ctx->stream, a));
+        ctx->prof_end(0, t0);
+        return EPG_OK;
+    };
+    switch (pl->inc_width) {
+        case 4: return go(k_edge_occ<Fn, kOccThreads, kOccEPT, kOccVPT, 4>);
+        case 8: return go(k_edge_occ<Fn, kOccThreads, kOccEPT, kOccVPT, 8>);
+        default: return go(k_edge_occ<Fn, kOccThreads, kOccEPT, kOccVPT, 0>);
+    }
+}
+
+template <class Fn>
+epg_status run_finalise_range(epg_ctx *ctx, epg_plan *pl, epg_state *state, int64_t s_first, int64_t s_count,
+                              int64_t h_first, int64_t h_count, float *acc, int32_t untouched) {
+    const float *vc = static_cast<const float *>(state->vertex_const);
+    float *out = static_cast<float *>(state->state_out);
+    if (s_count > 0) {
+        cudaEvent_t t1 = ctx->prof_begin();
+        CU(launch_pdl(k_finalise_range<Fn>, grid_for(s_count), kThreads, 0, ctx->stream, (const int32_t *)pl->shared_ids,
+                      (const int32_t *)pl->hv_off, (const int32_t *)pl->hv_list, (const float *)pl->halo_buf, out, vc,
+                      (int32_t)s_first, (int32_t)(s_first + s_count), h_first, h_first + h_count, acc));
+        ctx->prof_end(1, t1);
+    }
+    if (untouched && pl->n > pl->touched)
+        k_untouched<Fn><<<grid_for(pl->n - pl->touched), kThreads, 0, ctx->stream>>>(
+            static_cast<const float *>(state->state_in), out, pl->touched, pl->n);
+    CHECK_LAUNCH();
+    return EPG_OK;
 }
 
 template <class Fn>
@@ -974,6 +1034,8 @@ epg_status remap_impl(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, 
     if ((st = build_pipeline_blob(ctx, pl))) return fail_plan(st);
     pl->k_ep = k;
     pl->C_ep = C;
+    pl->exec_base.resize(k + 1);
+    for (int64_t p = 0; p <= k; p++) pl->exec_base[p] = (int32_t)p;
     *plan_out = pl;
     return EPG_OK;
 }
@@ -1036,6 +1098,8 @@ epg_status epg_remap(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, c
         if (!again || iter == 7) {
             xp->k_ep = k;
             xp->C_ep = ep->C;
+            xp->exec_base.assign(base.begin(), base.end());
+            xp->exec_base.push_back((int32_t)kx);
             delete ep;
             *plan_out = xp;
             return EPG_OK;
@@ -1068,6 +1132,7 @@ epg_status epg_plan_info(const epg_plan *plan, int64_t *out8) {
 epg_status epg_permute_rows(epg_ctx *ctx, const void *src, void *dst, int64_t rows, int32_t row_bytes,
                             const int32_t *perm, int32_t mode) {
     if (!ctx) return EPG_ERR_STATE;
+    if (rows == 0) return EPG_OK;
     if (!src || !dst || !perm || rows < 0 || row_bytes <= 0 || row_bytes % 4 || (mode != 0 && mode != 1))
         return ctx->fail(EPG_ERR_INPUT, "permute_rows: bad arguments");
     if (src == dst) return ctx->fail(EPG_ERR_INPUT, "permute_rows: src and dst alias");
@@ -1111,6 +1176,138 @@ epg_status epg_run_naive(epg_ctx *ctx, epg_kernel kernel, const int32_t *edges, 
         case EPG_KERNEL_GATHER_SCATTER: return run_naive<GatherScatter>(ctx, edges, m, n, state, steps);
         default: return run_naive<Spmv>(ctx, edges, m, n, state, steps);
     }
+}
+
+// ---- multi-GPU shards ------------------------------------------------
+epg_status epg_shard_ranges(const epg_plan *plan_c, int32_t G, int32_t g, int64_t *out8) {
+    if (!plan_c || !out8 || G < 1 || g < 0 || g >= G || G > plan_c->k_ep) return EPG_ERR_INPUT;
+    epg_plan *pl = const_cast<epg_plan *>(plan_c);
+    const int64_t pb = (int64_t)g * pl->k_ep / G, pe = (int64_t)(g + 1) * pl->k_ep / G;
+    const int64_t xb = pl->exec_base[pb], xe = pl->exec_base[pe];
+    const int64_t vlo = pl->pvb_h[xb], vhi = pl->pvb_h[xe];
+    if (pl->shared_h.size() != (size_t)pl->S) {
+        pl->shared_h.resize(pl->S);
+        if (pl->S > 0 && cudaMemcpy(pl->shared_h.data(), pl->shared_ids, sizeof(int32_t) * pl->S,
+                                    cudaMemcpyDeviceToHost) != cudaSuccess)
+            return EPG_ERR_CUDA;
+    }
+    const int64_t slo = std::lower_bound(pl->shared_h.begin(), pl->shared_h.end(), (int32_t)vlo) - pl->shared_h.begin();
+    const int64_t shi = std::lower_bound(pl->shared_h.begin(), pl->shared_h.end(), (int32_t)vhi) - pl->shared_h.begin();
+    out8[0] = xb; out8[1] = xe - xb;
+    out8[2] = pl->hb_h[xb]; out8[3] = pl->hb_h[xe] - pl->hb_h[xb];
+    out8[4] = vlo; out8[5] = vhi - vlo;
+    out8[6] = slo; out8[7] = shi - slo;
+    return EPG_OK;
+}
+
+epg_status epg_shard_halos_host(const int32_t *pvb, const int32_t *hb, const int32_t *halo_ids, int64_t k, int32_t G,
+                                int32_t *begin_out, int32_t *ids_out, int64_t cap, int64_t *count_out) {
+    if (!pvb || !hb || !begin_out || !count_out || k < 1 || G < 1 || G > k) return EPG_ERR_INPUT;
+    std::vector<int64_t> own_lo(G + 1);
+    for (int32_t g = 0; g <= G; g++) own_lo[g] = pvb[(int64_t)g * k / G];
+    int64_t pos = 0;
+    std::vector<int32_t> h;
+    for (int32_t g = 0; g < G; g++) {
+        const int64_t pb = (int64_t)g * k / G, pe = (int64_t)(g + 1) * k / G;
+        h.assign(halo_ids + hb[pb], halo_ids + hb[pe]);
+        std::sort(h.begin(), h.end());
+        h.erase(std::unique(h.begin(), h.end()), h.end());
+        // Halo^g = halo ids of g's partitions owned below g's range, by owner shard
+        for (int32_t g2 = 0; g2 < G; g2++) {
+            begin_out[g * G + g2] = (int32_t)pos;
+            if (g2 >= g) continue;
+            auto lo = std::lower_bound(h.begin(), h.end(), (int32_t)own_lo[g2]);
+            auto hi = std::lower_bound(h.begin(), h.end(), (int32_t)own_lo[g2 + 1]);
+            for (auto it = lo; it != hi; ++it) {
+                if (ids_out) {
+                    if (pos >= cap) return EPG_ERR_INPUT;
+                    ids_out[pos] = *it;
+                }
+                pos++;
+            }
+        }
+    }
+    begin_out[G * G] = (int32_t)pos;
+    *count_out = pos;
+    return EPG_OK;
+}
+
+epg_status epg_run_edges(epg_ctx *ctx, const epg_plan *plan, epg_kernel kernel, epg_state *state, int64_t first,
+                         int64_t count) {
+    if (!ctx) return EPG_ERR_STATE;
+    if (!plan || plan->ctx != ctx) return ctx->fail(EPG_ERR_STATE, "run_edges: plan belongs to another context");
+    epg_status st = check_state(ctx, kernel, state);
+    if (st) return st;
+    if (first < 0 || count < 0 || first + count > plan->k) return ctx->fail(EPG_ERR_INPUT, "run_edges: bad range");
+    CU(cudaSetDevice(ctx->device));
+    epg_plan *pl = const_cast<epg_plan *>(plan);
+    switch (kernel) {
+        case EPG_KERNEL_CFD_FLUX: return run_edges_range<CfdFlux>(ctx, pl, state, first, count);
+        case EPG_KERNEL_GATHER_SCATTER: return run_edges_range<GatherScatter>(ctx, pl, state, first, count);
+        default: return run_edges_range<Spmv>(ctx, pl, state, first, count);
+    }
+}
+
+epg_status epg_run_finalise(epg_ctx *ctx, const epg_plan *plan, epg_kernel kernel, epg_state *state,
+                            int64_t shared_first, int64_t shared_count, int64_t halo_first, int64_t halo_count,
+                            float *acc, int32_t untouched) {
+    if (!ctx) return EPG_ERR_STATE;
+    if (!plan || plan->ctx != ctx) return ctx->fail(EPG_ERR_STATE, "run_finalise: plan belongs to another context");
+    epg_status st = check_state(ctx, kernel, state);
+    if (st) return st;
+    if (shared_first < 0 || shared_count < 0 || shared_first + shared_count > plan->S || halo_first < 0 ||
+        halo_count < 0 || halo_first + halo_count > plan->C)
+        return ctx->fail(EPG_ERR_INPUT, "run_finalise: bad range");
+    CU(cudaSetDevice(ctx->device));
+    epg_plan *pl = const_cast<epg_plan *>(plan);
+    switch (kernel) {
+        case EPG_KERNEL_CFD_FLUX:
+            return run_finalise_range<CfdFlux>(ctx, pl, state, shared_first, shared_count, halo_first, halo_count, acc,
+                                               untouched);
+        case EPG_KERNEL_GATHER_SCATTER:
+            return run_finalise_range<GatherScatter>(ctx, pl, state, shared_first, shared_count, halo_first,
+                                                     halo_count, acc, untouched);
+        default:
+            return run_finalise_range<Spmv>(ctx, pl, state, shared_first, shared_count, halo_first, halo_count, acc,
+                                            untouched);
+    }
+}
+
+epg_status epg_shard_reduce(epg_ctx *ctx, const epg_plan *plan, epg_kernel kernel, const int32_t *ids, int64_t count,
+                            int64_t halo_first, int64_t halo_count, float *out_rows) {
+    if (!ctx) return EPG_ERR_STATE;
+    if (!plan || plan->ctx != ctx) return ctx->fail(EPG_ERR_STATE, "shard_reduce: plan belongs to another context");
+    if (count < 0 || (count > 0 && (!ids || !out_rows))) return ctx->fail(EPG_ERR_INPUT, "shard_reduce: arguments");
+    if (count == 0) return EPG_OK;
+    CU(cudaSetDevice(ctx->device));
+    const int64_t hl = halo_first, hh = halo_first + halo_count;
+    switch (kernel) {
+        case EPG_KERNEL_CFD_FLUX:
+            k_shard_reduce<CfdFlux><<<grid_for(count), kThreads, 0, ctx->stream>>>(
+                ids, count, plan->sidx, plan->hv_off, plan->hv_list, plan->halo_buf, hl, hh, out_rows);
+            break;
+        case EPG_KERNEL_GATHER_SCATTER:
+            k_shard_reduce<GatherScatter><<<grid_for(count), kThreads, 0, ctx->stream>>>(
+                ids, count, plan->sidx, plan->hv_off, plan->hv_list, plan->halo_buf, hl, hh, out_rows);
+            break;
+        default:
+            k_shard_reduce<Spmv><<<grid_for(count), kThreads, 0, ctx->stream>>>(
+                ids, count, plan->sidx, plan->hv_off, plan->hv_list, plan->halo_buf, hl, hh, out_rows);
+    }
+    CHECK_LAUNCH();
+    return EPG_OK;
+}
+
+epg_status epg_accumulate_rows(epg_ctx *ctx, const float *src, const int32_t *ids, int64_t count, int32_t row_floats,
+                               float *acc) {
+    if (!ctx) return EPG_ERR_STATE;
+    if (count < 0 || row_floats <= 0 || (count > 0 && (!src || !ids || !acc)))
+        return ctx->fail(EPG_ERR_INPUT, "accumulate_rows: arguments");
+    if (count == 0) return EPG_OK;
+    CU(cudaSetDevice(ctx->device));
+    k_accumulate_rows<<<grid_for(count * row_floats), kThreads, 0, ctx->stream>>>(src, ids, count, row_floats, acc);
+    CHECK_LAUNCH();
+    return EPG_OK;
 }
 
 epg_status epg_set_variant(epg_ctx *ctx, int32_t variant) {

@@ -45,6 +45,7 @@ struct OccArgs {
     const float *vconst;
     float *halo_buf;           // [C][ROW] in halo (partition) order
     int off_recs, rows_land, off_phi;
+    int64_t first;             // this launch runs execution partitions first .. first + grid
 };
 
 template <class Fn, int BLOCK, int EPT, int VPT, int W>
@@ -53,7 +54,7 @@ __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
     __shared__ __align__(8) uint64_t bar;
     constexpr int ROW = Fn::ROW, PW = Fn::PAYW;
     const int tid = threadIdx.x;
-    const PartDesc d = a.desc[blockIdx.x];
+    const PartDesc d = a.desc[a.first + blockIdx.x];
     const int L = d.nO + d.nH;
     unsigned char *sblob = occ_smem;
     float *recs = reinterpret_cast<float *>(occ_smem + a.off_recs);
@@ -261,6 +262,83 @@ __global__ void k_finalise3(const int32_t *__restrict__ shared_ids, const int32_
     }
     const int64_t v = touched + (t - S);
     if (v < n) Fn::untouched(state_in + Fn::ROW * v, state_out + Fn::ROW * v);
+}
+
+// Finalise of a vertex range (multi-GPU shards): for every shared vertex v
+// in [v_lo, v_hi), add dt times (its halo partials at positions in [h_lo, h_hi), in
+// ascending position, then acc[v] -- the partial sums pushed by other shards, already
+// accumulated in ascending peer order) to the owner row; acc[v] is cleared. With the full
+// ranges and acc = NULL this is exactly k_finalise3.
+template <class Fn>
+__global__ void k_finalise_range(const int32_t *__restrict__ shared_ids, const int32_t *__restrict__ hv_off,
+                                 const int32_t *__restrict__ hv_list, const float *__restrict__ halo_buf,
+                                 float *__restrict__ state_out, const float *__restrict__ vconst, int32_t s_lo,
+                                 int32_t s_hi, int64_t h_lo, int64_t h_hi, float *__restrict__ acc) {
+    const int64_t t = s_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    ptx::pdl_wait();
+    ptx::pdl_launch_dependents();
+    if (t >= s_hi) return;
+    const int64_t v = shared_ids[t];
+    float sum[Fn::ROW];
+#pragma unroll
+    for (int c = 0; c < Fn::ROW; c++) sum[c] = 0.0f;
+    for (int q = hv_off[t]; q < hv_off[t + 1]; q++) {
+        const int64_t h = hv_list[q];
+        if (h < h_lo || h >= h_hi) continue;
+#pragma unroll
+        for (int c = 0; c < Fn::ROW; c++) sum[c] += halo_buf[Fn::ROW * h + c];
+    }
+    if (acc) {
+#pragma unroll
+        for (int c = 0; c < Fn::ROW; c++) {
+            sum[c] += acc[Fn::ROW * v + c];
+            acc[Fn::ROW * v + c] = 0.0f;
+        }
+    }
+    const float dt = Fn::kUsesConst ? vconst[v] : 0.0f;
+    Fn::finalise_add(state_out + Fn::ROW * v, sum, dt);
+}
+
+// untouched rows [touched, n): copied (cfd) or cleared
+template <class Fn>
+__global__ void k_untouched(const float *__restrict__ state_in, float *__restrict__ state_out, int64_t touched,
+                            int64_t n) {
+    const int64_t v = touched + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v < n) Fn::untouched(state_in + Fn::ROW * v, state_out + Fn::ROW * v);
+}
+
+// partial sums a shard pushes to an owner: out[i] = sum of the halo partials of vertex
+// ids[i] at positions in [h_lo, h_hi), in ascending position
+template <class Fn>
+__global__ void k_shard_reduce(const int32_t *__restrict__ ids, int64_t count, const int32_t *__restrict__ sidx,
+                               const int32_t *__restrict__ hv_off, const int32_t *__restrict__ hv_list,
+                               const float *__restrict__ halo_buf, int64_t h_lo, int64_t h_hi,
+                               float *__restrict__ out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const int32_t s = sidx[ids[i]];
+    float sum[Fn::ROW];
+#pragma unroll
+    for (int c = 0; c < Fn::ROW; c++) sum[c] = 0.0f;
+    if (s >= 0) {
+        for (int q = hv_off[s]; q < hv_off[s + 1]; q++) {
+            const int64_t h = hv_list[q];
+            if (h < h_lo || h >= h_hi) continue;
+#pragma unroll
+            for (int c = 0; c < Fn::ROW; c++) sum[c] += halo_buf[Fn::ROW * h + c];
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < Fn::ROW; c++) out[Fn::ROW * i + c] = sum[c];
+}
+
+// acc[ids[i]] += src[i] (rows of `w` floats; ids distinct within one call)
+__global__ void k_accumulate_rows(const float *__restrict__ src, const int32_t *__restrict__ ids, int64_t count,
+                                  int32_t w, float *__restrict__ acc) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= count * w) return;
+    const int64_t i = t / w, c = t % w;
+    acc[(int64_t)w * ids[i] + c] += src[t];
 }
 
 // Finalise from packed per-vertex records {v, count, h_0..h_5} (count <= 6 halo entries):

@@ -28,7 +28,8 @@ PERM_GATHER, PERM_SCATTER = 0, 1
 SYMBOLS = ["epg_create", "epg_destroy", "epg_last_error", "epg_num_parts", "epg_partition_host", "epg_partition",
            "epg_default_partition", "epg_load_count", "epg_remap", "epg_plan_destroy", "epg_plan_info",
            "epg_permute_rows", "epg_run", "epg_run_naive", "epg_set_variant", "epg_set_profiling",
-           "epg_profile_read"]
+           "epg_profile_read", "epg_shard_ranges", "epg_shard_halos_host", "epg_run_edges", "epg_run_finalise",
+           "epg_shard_reduce", "epg_accumulate_rows"]
 
 
 class _Report(C.Structure):
@@ -67,6 +68,12 @@ def _load():
         "epg_run": (st, [P, P, C.c_int, C.POINTER(_State), i32]),
         "epg_run_naive": (st, [P, C.c_int, P, i64, i32, C.POINTER(_State), i32]),
         "epg_set_variant": (st, [P, i32]),
+        "epg_shard_ranges": (st, [P, i32, i32, P]),
+        "epg_shard_halos_host": (st, [P, P, P, i64, i32, P, P, i64, P]),
+        "epg_run_edges": (st, [P, P, C.c_int, C.POINTER(_State), i64, i64]),
+        "epg_run_finalise": (st, [P, P, C.c_int, C.POINTER(_State), i64, i64, i64, i64, P, i32]),
+        "epg_shard_reduce": (st, [P, P, C.c_int, P, i64, i64, i64, P]),
+        "epg_accumulate_rows": (st, [P, P, P, i64, i32, P]),
         "epg_set_profiling": (st, [P, i32]),
         "epg_profile_read": (st, [P, P, P]),
     }
@@ -121,6 +128,25 @@ def _ptr(t):
 
 def num_parts(m: int, part_size: int) -> int:
     return int(lib.epg_num_parts(m, part_size))
+
+
+def shard_halos_host(part_vertex_begin, halo_begin, halo_ids, k: int, G: int):
+    """O7 halo sets from the EP layout (host arrays) -> (begin [G*G+1], ids)."""
+    pvb = np.ascontiguousarray(part_vertex_begin, np.int32)
+    hb = np.ascontiguousarray(halo_begin, np.int32)
+    hid = np.ascontiguousarray(halo_ids, np.int32)
+    begin = np.zeros(G * G + 1, np.int32)
+    cnt = np.zeros(1, np.int64)
+    s = lib.epg_shard_halos_host(pvb.ctypes.data, hb.ctypes.data, hid.ctypes.data if hid.size else None, k, G,
+                                 begin.ctypes.data, None, 0, cnt.ctypes.data)
+    if s != OK:
+        raise EpgError(s, "epg_shard_halos_host")
+    ids = np.zeros(max(int(cnt[0]), 1), np.int32)
+    s = lib.epg_shard_halos_host(pvb.ctypes.data, hb.ctypes.data, hid.ctypes.data if hid.size else None, k, G,
+                                 begin.ctypes.data, ids.ctypes.data, ids.size, cnt.ctypes.data)
+    if s != OK:
+        raise EpgError(s, "epg_shard_halos_host")
+    return begin, ids[: int(cnt[0])]
 
 
 def partition_host(edges, n: int, part_size: int, shards: int = 1) -> np.ndarray:
@@ -247,6 +273,37 @@ class Context:
         st = _State(_ptr(state_in), _ptr(state_out), _ptr(payload), _ptr(vconst))
         self._check(lib.epg_run(self.handle, plan.handle, kernel, C.byref(st), steps))
         return state_out if steps % 2 else state_in
+
+    # -- multi-GPU shards ---------------------------------------------------------------
+    def shard_ranges(self, plan: Plan, G: int, g: int) -> dict:
+        out = np.zeros(8, np.int64)
+        self._check(lib.epg_shard_ranges(plan.handle, G, g, out.ctypes.data))
+        keys = ("exec_first", "exec_count", "halo_first", "halo_count", "vertex_first", "vertex_count",
+                "shared_first", "shared_count")
+        return {k: int(v) for k, v in zip(keys, out)}
+
+    def run_edges(self, plan: Plan, kernel: int, state_in, state_out, payload=None, vconst=None, first=0, count=None):
+        count = plan.k_exec - first if count is None else count
+        st = _State(_ptr(state_in), _ptr(state_out), _ptr(payload), _ptr(vconst))
+        self._check(lib.epg_run_edges(self.handle, plan.handle, kernel, C.byref(st), first, count))
+
+    def run_finalise(self, plan: Plan, kernel: int, state_in, state_out, payload=None, vconst=None,
+                     shared_first=0, shared_count=None, halo_first=0, halo_count=None, acc=None, untouched=True):
+        shared_count = plan.shared - shared_first if shared_count is None else shared_count
+        halo_count = plan.cut_cost_exec - halo_first if halo_count is None else halo_count
+        st = _State(_ptr(state_in), _ptr(state_out), _ptr(payload), _ptr(vconst))
+        self._check(lib.epg_run_finalise(self.handle, plan.handle, kernel, C.byref(st), shared_first, shared_count,
+                                         halo_first, halo_count, _ptr(acc), 1 if untouched else 0))
+
+    def shard_reduce(self, plan: Plan, kernel: int, ids: torch.Tensor, halo_first: int, halo_count: int,
+                     out: torch.Tensor):
+        self._check(lib.epg_shard_reduce(self.handle, plan.handle, kernel, _ptr(ids), ids.numel(), halo_first,
+                                         halo_count, _ptr(out)))
+        return out
+
+    def accumulate_rows(self, src: torch.Tensor, ids: torch.Tensor, acc: torch.Tensor):
+        w = src[0].numel() if src.dim() > 1 else 1
+        self._check(lib.epg_accumulate_rows(self.handle, _ptr(src), _ptr(ids), ids.numel(), w, _ptr(acc)))
 
     def set_variant(self, variant: int):
         """0 auto, 1 one CTA per partition, 2 pipelined TMA kernel, 3 occupancy TMA kernel."""
