@@ -460,8 +460,16 @@ def run_ours(args, rank, local_rank, world):
         def naive_step(i):
             ctx.run_naive(epg.KERNEL_CFD_FLUX, E, M.n, nbufs[i & 1], nbufs[(i + 1) & 1], nrm0, dt0, 1)
 
+        # the paper's hardware-cache variant: EP order + cpack layout, no staging
+        Ex = ctx.remapped_edges(E, L)
+        hbufs = [bufs[0].clone(), torch.empty_like(Ud)]
+
+        def hwcache_step(i):
+            ctx.run_naive(epg.KERNEL_CFD_FLUX, Ex, M.n, hbufs[i & 1], hbufs[(i + 1) & 1], nrm, dtn, 1)
+
         out = {}
-        for name, fn, r in (("default_staged", def_step, drep), ("naive_original_order", naive_step, None)):
+        for name, fn, r in (("default_staged", def_step, drep), ("naive_original_order", naive_step, None),
+                            ("ep_hardware_cache", hwcache_step, None)):
             for i in range(W):
                 fn(i)
             barrier()
@@ -470,7 +478,7 @@ def run_ours(args, rank, local_rank, world):
             if r is not None:
                 out[name].update({"load_count": r.load_count, "cut_cost": r.cut_cost,
                                   "replication": r.replication})
-        best_default = max(out.values(), key=lambda d: d["edges_per_s"])["edges_per_s"]
+        best_default = max(out[k]["edges_per_s"] for k in ("default_staged", "naive_original_order"))
         out["ep_speedup_vs_best_default"] = (M.m / (step_ms * 1e-3)) / best_default
         comparators = out
 

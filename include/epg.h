@@ -198,6 +198,14 @@ epg_status epg_plan_info(const epg_plan *plan, int64_t *out8);
 epg_status epg_permute_rows(epg_ctx *ctx, const void *src, void *dst, int64_t rows, int32_t row_bytes,
                             const int32_t *perm, int32_t mode);
 
+/* The reorganised task list in the new vertex ids ("opt_indexA", P:755-757 / P:1343):
+ * out[i] = (vertex_perm[edges[edge_perm[i]][0]], vertex_perm[edges[edge_perm[i]][1]]).
+ * With epg_run_naive on these edges and the cpack-ordered state this is the paper's
+ * hardware-cache variant: the EP order and layout, operands through the
+ * read-only cache path instead of shared-memory staging.  All DEVICE, out [m][2]. */
+epg_status epg_remapped_edges(epg_ctx *ctx, const int32_t *edges, int64_t m, const int32_t *edge_perm,
+                              const int32_t *vertex_perm, int32_t *out);
+
 /* -- run (steps a5 + a6) ------------------------------------------------------ */
 /* `steps` time steps of the partition-scheduled kernel: one CTA per
  * partition stages V_p (owned rows O_p contiguous, halo rows H_p gathered) into

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <queue>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -570,8 +571,19 @@ epg_status run_pipelined(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t s
 
 // occupancy kernel limits: execution partitions of <= 1024 edges and <= 768 staged rows
 // (704 rows keep a cfd CTA at ~55 KB of shared memory: four CTAs per SM)
-constexpr int kOccThreads = 256, kOccEPT = 4, kOccVPT = 3;
-constexpr int kExecMaxEdges = kOccThreads * kOccEPT, kExecMaxRows = 704;
+constexpr int kOccThreads = 256, kOccEPT = 4;
+constexpr int kExecMaxEdges = kOccThreads * kOccEPT;
+// staged-row cap of an execution partition: 704 (default) keeps 4 CTAs/SM; up to 1024
+// (3 CTAs/SM, fewer split partitions) via EPG_EXEC_MAX_ROWS, read once
+int exec_max_rows() {
+    static int v = [] {
+        const char *e = std::getenv("EPG_EXEC_MAX_ROWS");
+        int x = e ? std::atoi(e) : 704;
+        return std::min(1024, std::max(64, x));
+    }();
+    return v;
+}
+#define kExecMaxRows exec_max_rows()
 
 // launch with programmatic stream serialization (the kernel calls griddepcontrol.wait
 // before touching what the previous kernel in the stream writes)
@@ -590,9 +602,9 @@ cudaError_t launch_pdl(K kern, unsigned grid, unsigned block, size_t smem, cudaS
     return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
-template <class Fn, int W>
+template <class Fn, int W, int VPT>
 epg_status launch_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, OccArgs a, size_t smem) {
-    auto kern = k_edge_occ<Fn, kOccThreads, kOccEPT, kOccVPT, W>;
+    auto kern = k_edge_occ<Fn, kOccThreads, kOccEPT, VPT, W>;
     CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     float *bufs[2] = {static_cast<float *>(state->state_in), static_cast<float *>(state->state_out)};
     const int64_t fin_work = pl->S + (pl->n - pl->touched);
@@ -641,10 +653,14 @@ epg_status run_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, 
     a.vconst = static_cast<const float *>(state->vertex_const);
     a.halo_buf = pl->halo_buf;
     a.first = 0;
+    const bool v4 = pl->Lcap > 3 * kOccThreads;
     switch (pl->inc_width) {
-        case 4: return launch_occ<Fn, 4>(ctx, pl, state, steps, a, smem);
-        case 8: return launch_occ<Fn, 8>(ctx, pl, state, steps, a, smem);
-        default: return launch_occ<Fn, 0>(ctx, pl, state, steps, a, smem);
+        case 4: return v4 ? launch_occ<Fn, 4, 4>(ctx, pl, state, steps, a, smem)
+                          : launch_occ<Fn, 4, 3>(ctx, pl, state, steps, a, smem);
+        case 8: return v4 ? launch_occ<Fn, 8, 4>(ctx, pl, state, steps, a, smem)
+                          : launch_occ<Fn, 8, 3>(ctx, pl, state, steps, a, smem);
+        default: return v4 ? launch_occ<Fn, 0, 4>(ctx, pl, state, steps, a, smem)
+                           : launch_occ<Fn, 0, 3>(ctx, pl, state, steps, a, smem);
     }
 }
 
@@ -676,10 +692,11 @@ epg_status run_edges_range(epg_ctx *ctx, epg_plan *pl, epg_state *state, int64_t
         ctx->prof_end(0, t0);
         return EPG_OK;
     };
+    const bool v4 = pl->Lcap > 3 * kOccThreads;
     switch (pl->inc_width) {
-        case 4: return go(k_edge_occ<Fn, kOccThreads, kOccEPT, kOccVPT, 4>);
-        case 8: return go(k_edge_occ<Fn, kOccThreads, kOccEPT, kOccVPT, 8>);
-        default: return go(k_edge_occ<Fn, kOccThreads, kOccEPT, kOccVPT, 0>);
+        case 4: return v4 ? go(k_edge_occ<Fn, kOccThreads, kOccEPT, 4, 4>) : go(k_edge_occ<Fn, kOccThreads, kOccEPT, 3, 4>);
+        case 8: return v4 ? go(k_edge_occ<Fn, kOccThreads, kOccEPT, 4, 8>) : go(k_edge_occ<Fn, kOccThreads, kOccEPT, 3, 8>);
+        default: return v4 ? go(k_edge_occ<Fn, kOccThreads, kOccEPT, 4, 0>) : go(k_edge_occ<Fn, kOccThreads, kOccEPT, 3, 0>);
     }
 }
 
@@ -1306,6 +1323,17 @@ epg_status epg_accumulate_rows(epg_ctx *ctx, const float *src, const int32_t *id
     if (count == 0) return EPG_OK;
     CU(cudaSetDevice(ctx->device));
     k_accumulate_rows<<<grid_for(count * row_floats), kThreads, 0, ctx->stream>>>(src, ids, count, row_floats, acc);
+    CHECK_LAUNCH();
+    return EPG_OK;
+}
+
+epg_status epg_remapped_edges(epg_ctx *ctx, const int32_t *edges, int64_t m, const int32_t *edge_perm,
+                              const int32_t *vertex_perm, int32_t *out) {
+    if (!ctx) return EPG_ERR_STATE;
+    if (m <= 0 || !edges || !edge_perm || !vertex_perm || !out)
+        return ctx->fail(EPG_ERR_INPUT, "remapped_edges: arguments");
+    CU(cudaSetDevice(ctx->device));
+    k_remapped_edges<<<grid_for(m), kThreads, 0, ctx->stream>>>(edges, edge_perm, vertex_perm, m, out);
     CHECK_LAUNCH();
     return EPG_OK;
 }

@@ -272,4 +272,14 @@ __global__ void k_hv_off(const int32_t *__restrict__ sorted_ids, int64_t C, cons
     if (r == 0 || sorted_ids[r] != sorted_ids[r - 1]) hv_off[sidx[sorted_ids[r]]] = (int32_t)r;
 }
 
+// opt_indexA in global ids: new edge i -> (vertex_perm[u], vertex_perm[v]) of task edge_perm[i]
+__global__ void k_remapped_edges(const int32_t *__restrict__ edges, const int32_t *__restrict__ edge_perm,
+                                 const int32_t *__restrict__ vertex_perm, int64_t m, int32_t *out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const int64_t e = edge_perm[i];
+    out[2 * i] = vertex_perm[edges[2 * e]];
+    out[2 * i + 1] = vertex_perm[edges[2 * e + 1]];
+}
+
 }  // namespace epg

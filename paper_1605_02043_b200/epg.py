@@ -29,7 +29,7 @@ SYMBOLS = ["epg_create", "epg_destroy", "epg_last_error", "epg_num_parts", "epg_
            "epg_default_partition", "epg_load_count", "epg_remap", "epg_plan_destroy", "epg_plan_info",
            "epg_permute_rows", "epg_run", "epg_run_naive", "epg_set_variant", "epg_set_profiling",
            "epg_profile_read", "epg_shard_ranges", "epg_shard_halos_host", "epg_run_edges", "epg_run_finalise",
-           "epg_shard_reduce", "epg_accumulate_rows"]
+           "epg_shard_reduce", "epg_accumulate_rows", "epg_remapped_edges"]
 
 
 class _Report(C.Structure):
@@ -74,6 +74,7 @@ def _load():
         "epg_run_finalise": (st, [P, P, C.c_int, C.POINTER(_State), i64, i64, i64, i64, P, i32]),
         "epg_shard_reduce": (st, [P, P, C.c_int, P, i64, i64, i64, P]),
         "epg_accumulate_rows": (st, [P, P, P, i64, i32, P]),
+        "epg_remapped_edges": (st, [P, P, i64, P, P, P]),
         "epg_set_profiling": (st, [P, i32]),
         "epg_profile_read": (st, [P, P, P]),
     }
@@ -258,6 +259,12 @@ class Context:
         plan = Plan(h, self)
         L.halo_ids = L.halo_ids[: plan.cut_cost]
         return L, plan
+
+    def remapped_edges(self, edges: torch.Tensor, layout: Layout) -> torch.Tensor:
+        out = torch.empty_like(edges)
+        self._check(lib.epg_remapped_edges(self.handle, _ptr(edges), edges.shape[0], _ptr(layout.edge_perm),
+                                           _ptr(layout.vertex_perm), _ptr(out)))
+        return out
 
     def permute_rows(self, src: torch.Tensor, perm: torch.Tensor, mode: int, out: torch.Tensor | None = None):
         rows = perm.shape[0]

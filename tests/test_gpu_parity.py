@@ -257,6 +257,27 @@ def test_cfd_naive(ctx, small_mesh):
     assert normwise_err(out.cpu().numpy(), ref).max() <= TOL
 
 
+def test_cfd_hardware_cache_variant(ctx, small_mesh):
+    """EP order + cpack layout through the unstaged kernel == the oracle."""
+    from paper_1605_02043_b200 import epg
+    M = small_mesh
+    k = O.num_parts(M.m, 512)
+    E = dev(M.edges)
+    L, plan = ctx.remap(E, M.n, dev(O.partition(M.edges, M.n, 512)), k)
+    Ex = ctx.remapped_edges(E, L)
+    ref_lay = O.remap(M.edges, M.n, O.partition(M.edges, M.n, 512), k)
+    assert np.array_equal(Ex.cpu().numpy(), ref_lay.vertex_perm[M.edges[ref_lay.edge_perm]])
+    U, dt = _cfd_inputs(M)
+    Un = ctx.permute_rows(dev(U), L.vertex_perm, epg.PERM_SCATTER)
+    nrm = ctx.permute_rows(dev(M.normals), L.edge_perm, epg.PERM_GATHER)
+    dtn = ctx.permute_rows(dev(dt), L.vertex_perm, epg.PERM_SCATTER)
+    out = torch.empty_like(Un)
+    ctx.run_naive(epg.KERNEL_CFD_FLUX, Ex, M.n, Un, out, nrm, dtn)
+    got = ctx.permute_rows(out, L.vertex_perm, epg.PERM_GATHER).cpu().numpy()
+    ref, _ = O.cfd_step(M.edges, M.n, M.normals, U, dt)
+    assert normwise_err(got, ref).max() <= TOL
+
+
 def test_cfd_untouched_vertices(ctx):
     """Isolated vertices (degree 0) keep their state (O8)."""
     M = S.kuhn_mesh(nbox=5, n_keep=700)

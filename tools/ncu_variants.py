@@ -54,7 +54,8 @@ def main():
             fn()
             torch.cuda.synchronize()
             if r == 0:
-                extra = f" k={plan.k} touched={plan.touched} C={plan.cut_cost} S={plan.shared}" if plan else ""
+                extra = (f" k={plan.k} k_exec={plan.k_exec} touched={plan.touched} C={plan.cut_cost} "
+                         f"C_exec={plan.cut_cost_exec} S={plan.shared}") if plan else ""
                 print(f"variant {name}: m={M.m} n={M.n}{extra}", flush=True)
 
 
