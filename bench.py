@@ -40,7 +40,57 @@ WORKLOADS = {
     "c1": "C1: Rodinia cfd fvcorr.domn.097K-shaped Kuhn tet mesh, 97,046 cells, 190,245 interior faces",
     "c2": "C2: cfd missile.domn.0.2M-shaped Kuhn tet mesh, 232,536 cells, 458,168 interior faces",
     "c3": "C3: synthetic 3D tetrahedral mesh, 64,000,000 cells",
+    "c4": "C4: R-MAT scale 24 (n = 16,777,216, m = 134,217,728, a = 0.57, b = c = 0.19), gather-scatter",
+    "c5": "C5 per-GPU share: SpMV of a 2D 5-point Laplacian on a 3536^2 grid (12.5M rows, 62.5M nnz = 1/8 "
+          "of the 500M-nnz 8-GPU config) as a bipartite COO data-affinity graph",
 }
+
+
+class Workload:
+    """One configuration: graph, functor, inputs in original order, compulsory bytes, oracle."""
+
+    def __init__(self, config: str):
+        import synth as S
+        self.config = config
+        t0 = time.perf_counter()
+        if config in ("c1", "c2", "c3"):
+            M = S.config_mesh(config)
+            self.n, self.m, self.edges = M.n, M.m, M.edges
+            self.kernel, self.functor = 1, "cfd_flux"
+            self.state, self.payload, self.vconst = S.cfd_state(M.n), M.normals, S.cfd_dt(M.volume)
+            self.per_edge, self.per_vertex = 20, 44     # 8 B ids + 12 B normal; 20 B read, 4 B dt, 20 B write
+        elif config == "c4":
+            self.n, self.edges = S.rmat(24)
+            self.m = self.edges.shape[0]
+            self.kernel, self.functor = 2, "gather_scatter"
+            self.state, self.payload, self.vconst = S.int_vector(1608, self.n, 0, 7), None, None
+            self.per_edge, self.per_vertex = 8, 8       # 8 B ids; 4 B x read, 4 B y write
+        elif config == "c5":
+            self.n, self.edges, w = S.stencil2d_spmv(3536)
+            self.m = self.edges.shape[0]
+            N = self.n // 2
+            self.kernel, self.functor = 3, "spmv"
+            self.state = np.concatenate([S.int_vector(1609, N, -8, 8), np.zeros(N, np.float32)])
+            self.payload, self.vconst = w, None
+            self.per_edge, self.per_vertex = 12, 4      # 8 B ids + 4 B value; 4 B x or y per vertex
+        else:
+            raise ValueError(config)
+        self.gen_s = time.perf_counter() - t0
+
+    def alg_bytes(self, touched: int) -> int:
+        """SURVEY §8(d) compulsory bytes of one step."""
+        return self.per_edge * self.m + self.per_vertex * touched
+
+    def oracle_step(self):
+        import oracle as O
+        if self.kernel == 1:
+            return O.cfd_step(self.edges, self.n, self.payload, self.state, self.vconst)
+        if self.kernel == 2:
+            return O.gather_scatter(self.edges, self.n, self.state)
+        return O.spmv(self.edges, self.n, self.payload, self.state)
+
+    def oracle_name(self):
+        return {1: "orc_cfd_step", 2: "orc_gather_scatter", 3: "orc_spmv"}[self.kernel]
 
 
 def parse():
@@ -49,7 +99,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=list(WORKLOADS), default="c2")
+    ap.add_argument("--config", choices=["c1", "c2", "c3", "c4", "c5"], default="c2")
     ap.add_argument("--part-size", type=int, default=1024)
     ap.add_argument("--flush-mib", type=int, default=512)
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="bounded oracle sample for cpu_baseline")
@@ -169,12 +219,11 @@ class _Window:
 
 
 # --------------------------------------------------------------------------------- oracle
-def oracle_steps(M, U, dt, steps: int, budget_s: float | None = None):
-    """Time the CPU oracle's fp64 cfd step (orc_cfd_step, single thread) as it stands."""
-    import oracle as O
+def oracle_steps(w: "Workload", steps: int, budget_s: float | None = None):
+    """Time the CPU oracle's fp64 step of the workload's functor (single thread) as it stands."""
     done, t0 = 0, time.perf_counter()
     while done < steps or (budget_s is not None and time.perf_counter() - t0 < budget_s):
-        O.cfd_step(M.edges, M.n, M.normals, U, dt)
+        w.oracle_step()
         done += 1
         if budget_s is not None and done >= steps and time.perf_counter() - t0 >= budget_s:
             break
@@ -184,20 +233,18 @@ def oracle_steps(M, U, dt, steps: int, budget_s: float | None = None):
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    import synth as S
-    M = S.config_mesh(args.config)
-    U, dt = S.cfd_state(M.n), S.cfd_dt(M.volume)
-    oracle_steps(M, U, dt, args.warmup)
-    steps, secs = oracle_steps(M, U, dt, args.steps)
-    v = M.m * steps / secs
+    w = Workload(args.config)
+    oracle_steps(w, args.warmup)
+    steps, secs = oracle_steps(w, args.steps)
+    v = w.m * steps / secs
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "edges/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.config], "part_size": args.part_size, "functor": "cfd_flux"},
+        "config": {"workload": WORKLOADS[args.config], "part_size": args.part_size, "functor": w.functor},
         "cpu_baseline": {"value": v, "unit": "edges/s", "cores": 1, "kind": "oracle",
-                         "sample": f"{steps} full steps of the fp64 oracle cfd step (oracle/epg_oracle.c "
-                                   f"orc_cfd_step) on the {args.config} mesh, single thread"},
+                         "sample": f"{steps} full steps of the fp64 oracle ({w.oracle_name()} in oracle/epg_oracle.c) "
+                                   f"on the {args.config} workload, single thread"},
         "e2e": {"value": v, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -252,9 +299,11 @@ def run_sharded(args, rank, local_rank, world):
     L, plan = ctx.remap(E, M.n, part, k, halo_cap=rep.cut_cost)
     sh = Shard(ctx, plan, L, epg.KERNEL_CFD_FLUX, world, rank)
     comm = Comm()
-    Ud = torch.from_numpy(U).to(dev)
-    nrm = ctx.permute_rows(torch.from_numpy(M.normals).to(dev), L.edge_perm, epg.PERM_GATHER)
-    dtn = ctx.permute_rows(torch.from_numpy(dt).to(dev), L.vertex_perm, epg.PERM_SCATTER)
+    Ud = torch.from_numpy(M.state).to(dev)
+    pay0 = None if M.payload is None else torch.from_numpy(M.payload).to(dev)
+    vc0 = None if M.vconst is None else torch.from_numpy(M.vconst).to(dev)
+    nrm = None if pay0 is None else ctx.permute_rows(pay0, L.edge_perm, epg.PERM_GATHER)
+    dtn = None if vc0 is None else ctx.permute_rows(vc0, L.vertex_perm, epg.PERM_SCATTER)
     bufs = [ctx.permute_rows(Ud, L.vertex_perm, epg.PERM_SCATTER), torch.empty_like(Ud)]
     flushbuf = torch.empty(args.flush_mib * (1 << 20) // 4, dtype=torch.float32, device=dev)
 
@@ -359,11 +408,10 @@ def run_ours(args, rank, local_rank, world):
     K, W, P = args.steps, args.warmup, args.part_size
     clocks = ClockSampler(local_rank)
 
-    # ---------------- setup (once per mesh; amortised over steps)
-    t0 = time.perf_counter()
-    M = S.config_mesh(args.config)
-    U, dt = S.cfd_state(M.n), S.cfd_dt(M.volume)
-    t_gen = time.perf_counter() - t0
+    # ---------------- setup (once per graph; amortised over steps)
+    M = Workload(args.config)
+    t_gen = M.gen_s
+    KER = M.kernel
     E = torch.from_numpy(M.edges).to(dev)
     k = epg.num_parts(M.m, P)
     torch.cuda.synchronize()
@@ -374,17 +422,23 @@ def run_ours(args, rank, local_rank, world):
     L, plan = ctx.remap(E, M.n, part, k, halo_cap=rep.cut_cost)
     torch.cuda.synchronize()
     t_remap = time.perf_counter() - t0
-    Ud = torch.from_numpy(U).to(dev)
-    nrm = ctx.permute_rows(torch.from_numpy(M.normals).to(dev), L.edge_perm, epg.PERM_GATHER)
-    dtn = ctx.permute_rows(torch.from_numpy(dt).to(dev), L.vertex_perm, epg.PERM_SCATTER)
+    Ud = torch.from_numpy(M.state).to(dev)
+    pay0 = None if M.payload is None else torch.from_numpy(M.payload).to(dev)
+    vc0 = None if M.vconst is None else torch.from_numpy(M.vconst).to(dev)
+    nrm = None if pay0 is None else ctx.permute_rows(pay0, L.edge_perm, epg.PERM_GATHER)
+    dtn = None if vc0 is None else ctx.permute_rows(vc0, L.vertex_perm, epg.PERM_SCATTER)
     bufs = [ctx.permute_rows(Ud, L.vertex_perm, epg.PERM_SCATTER), torch.empty_like(Ud)]
     flushbuf = torch.empty(args.flush_mib * (1 << 20) // 4, dtype=torch.float32, device=dev)
 
     def flush():
         flushbuf.fill_(1.0)
 
+    # gather-scatter / SpMV read x and write y: keep x fixed (state_in) across steps
+    pingpong = KER == epg.KERNEL_CFD_FLUX
+
     def ep_step(i):
-        ctx.run(plan, epg.KERNEL_CFD_FLUX, bufs[i & 1], bufs[(i + 1) & 1], nrm, dtn, 1)
+        j = i & 1 if pingpong else 0
+        ctx.run(plan, KER, bufs[j], bufs[1 - j], nrm, dtn, 1)
 
     def barrier():
         torch.cuda.synchronize()
@@ -416,7 +470,7 @@ def run_ours(args, rank, local_rank, world):
     edge_ms, fin_ms = edge_ms / K, fin_ms / K         # per step
 
     # ---------------- e2e: host (pinned) state in, result out, through the public API
-    Uh = torch.from_numpy(U).pin_memory()
+    Uh = torch.from_numpy(M.state).pin_memory()
     Uout_h = torch.empty_like(Uh).pin_memory()
     Ud_in = torch.empty_like(Ud)
     Ud_out = torch.empty_like(Ud)
@@ -425,7 +479,7 @@ def run_ours(args, rank, local_rank, world):
     def e2e_step(i):
         Ud_in.copy_(Uh, non_blocking=True)
         ctx.permute_rows(Ud_in, L.vertex_perm, epg.PERM_SCATTER, out=bufs[0])
-        ctx.run(plan, epg.KERNEL_CFD_FLUX, bufs[0], bufs[1], nrm, dtn, 1)
+        ctx.run(plan, KER, bufs[0], bufs[1], nrm, dtn, 1)
         ctx.permute_rows(bufs[1], L.vertex_perm, epg.PERM_GATHER, out=Ud_out)
         Uout_h.copy_(Ud_out, non_blocking=True)
 
@@ -447,25 +501,27 @@ def run_ours(args, rank, local_rank, world):
         dpart = ctx.default_partition(M.m, P)
         drep = ctx.load_count(E, M.n, dpart, k)
         DL, dplan = ctx.remap(E, M.n, dpart, k, halo_cap=drep.cut_cost)
-        dnrm = ctx.permute_rows(torch.from_numpy(M.normals).to(dev), DL.edge_perm, epg.PERM_GATHER)
-        ddt = ctx.permute_rows(torch.from_numpy(dt).to(dev), DL.vertex_perm, epg.PERM_SCATTER)
+        dnrm = None if pay0 is None else ctx.permute_rows(pay0, DL.edge_perm, epg.PERM_GATHER)
+        ddt = None if vc0 is None else ctx.permute_rows(vc0, DL.vertex_perm, epg.PERM_SCATTER)
         dbufs = [ctx.permute_rows(Ud, DL.vertex_perm, epg.PERM_SCATTER), torch.empty_like(Ud)]
 
+        def pp(i):
+            return (i & 1) if pingpong else 0
+
         def def_step(i):
-            ctx.run(dplan, epg.KERNEL_CFD_FLUX, dbufs[i & 1], dbufs[(i + 1) & 1], dnrm, ddt, 1)
+            ctx.run(dplan, KER, dbufs[pp(i)], dbufs[1 - pp(i)], dnrm, ddt, 1)
 
         nbufs = [Ud.clone(), torch.empty_like(Ud)]
-        nrm0, dt0 = torch.from_numpy(M.normals).to(dev), torch.from_numpy(dt).to(dev)
 
         def naive_step(i):
-            ctx.run_naive(epg.KERNEL_CFD_FLUX, E, M.n, nbufs[i & 1], nbufs[(i + 1) & 1], nrm0, dt0, 1)
+            ctx.run_naive(KER, E, M.n, nbufs[pp(i)], nbufs[1 - pp(i)], pay0, vc0, 1)
 
         # the paper's hardware-cache variant: EP order + cpack layout, no staging
         Ex = ctx.remapped_edges(E, L)
         hbufs = [bufs[0].clone(), torch.empty_like(Ud)]
 
         def hwcache_step(i):
-            ctx.run_naive(epg.KERNEL_CFD_FLUX, Ex, M.n, hbufs[i & 1], hbufs[(i + 1) & 1], nrm, dtn, 1)
+            ctx.run_naive(KER, Ex, M.n, hbufs[pp(i)], hbufs[1 - pp(i)], nrm, dtn, 1)
 
         out = {}
         for name, fn, r in (("default_staged", def_step, drep), ("naive_original_order", naive_step, None),
@@ -489,7 +545,7 @@ def run_ours(args, rank, local_rank, world):
         return
 
     peak, peak_src = measured_peaks()
-    B = alg_bytes_per_step(M.m, rep.touched)
+    B = M.alg_bytes(rep.touched)
     # every compulsory byte of the step (edge records, each touched row read and written
     # once) is moved by the edge kernel; the finalise only re-touches shared rows
     achieved = B / (edge_ms * 1e-3) / 1e9
@@ -499,7 +555,8 @@ def run_ours(args, rank, local_rank, world):
     roofline = {
         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
         "traffic": traffic,
-        "kernel": "k_edge_occ<CfdFlux> (staged edge kernel; the step adds k_finalise_rec)",
+        "kernel": f"k_edge_occ<{ {1: 'CfdFlux', 2: 'GatherScatter', 3: 'Spmv'}[KER]}> "
+                  "(staged edge kernel; the step adds the boundary finalise)",
         "algorithmic_bytes_per_launch": B,
         "bytes_per_edge_algorithmic": B / M.m,
         "edge_kernel_ms": edge_ms, "finalise_ms": fin_ms,
@@ -512,16 +569,17 @@ def run_ours(args, rank, local_rank, world):
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        steps, secs = oracle_steps(M, U, dt, 1, budget_s=args.cpu_seconds)
+        steps, secs = oracle_steps(M, 1, budget_s=args.cpu_seconds)
         cpu = {"value": M.m * steps / secs, "unit": "edges/s", "cores": 1, "kind": "oracle",
-               "sample": f"{steps} full steps of the fp64 oracle cfd step (oracle/epg_oracle.c orc_cfd_step) "
-                         f"on the {args.config} mesh, single thread, ~{args.cpu_seconds:.0f} s budget"}
+               "sample": f"{steps} full steps of the fp64 oracle ({M.oracle_name()} in oracle/epg_oracle.c) "
+                         f"on the {args.config} workload, single thread, ~{args.cpu_seconds:.0f} s budget"}
 
     line = {
         "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.config], "part_size": P, "k": k, "functor": "cfd_flux",
+        "config": {"workload": WORKLOADS[args.config], "part_size": P, "k": k, "k_exec": plan.k_exec,
+                   "functor": M.functor,
                    "schedule": "EP (host EPG-1) + cpack remap", "step": "epg_run(steps=1): staged edge kernel + boundary finalise",
                    "l2": f"flushed between timed steps ({args.flush_mib} MiB write)",
                    "parallelism": "replicas" if world > 1 else "single"},
@@ -529,7 +587,7 @@ def run_ours(args, rank, local_rank, world):
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "edges/s", "h2d_bytes_per_step": n_bytes, "d2h_bytes_per_step": n_bytes,
                 "ms_per_step": e2e_ms,
-                "path": "pinned host U -> H2D -> epg_permute_rows -> epg_run -> epg_permute_rows -> D2H"},
+                "path": "pinned host state -> H2D -> epg_permute_rows -> epg_run -> epg_permute_rows -> D2H"},
         "gpu_launches": launches,
         "clocks": clk,
         "partition": {"load_count": rep.load_count, "touched": rep.touched, "cut_cost": rep.cut_cost,
@@ -538,7 +596,7 @@ def run_ours(args, rank, local_rank, world):
                       "host_partition_s": t_part, "remap_s": t_remap, "mesh_gen_s": t_gen},
         "comparators": comparators,
         "bytes_per_edge_ncu": variants,
-        "seeds": {"mesh": 1605, "state": 1606},
+        "seeds": {"mesh": 1605, "state": 1606, "rmat": 1607, "x": [1608, 1609]},
     }
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -79,6 +79,10 @@ struct epg_plan {
     unsigned char *blob3 = nullptr;
     int blob3_max = 0;
     int4 *fin_recs = nullptr;   // packed finalise records (when every vertex has <= 6 halo entries)
+    int32_t *heavy = nullptr;   // shared vertices with more than kBlockHalo halo entries
+    int64_t n_heavy = 0;
+    int32_t *medium = nullptr;  // shared vertices with (kHeavyHalo, kBlockHalo] halo entries
+    int64_t n_medium = 0;
     // the EP map the plan executes (k, C of the paper's partitions; the plan itself may
     // split oversized partitions into contiguous execution ranges)
     int64_t k_ep = 0, C_ep = 0;
@@ -101,6 +105,8 @@ namespace {
 using namespace epg;
 
 constexpr int kThreads = 256;
+constexpr int kHeavyHalo = 8;      // halo entries above which a shared vertex leaves the thread path
+constexpr int kBlockHalo = 1024;   // ... and above which a whole CTA (not a warp) finalises it
 
 inline unsigned grid_for(int64_t work, int threads = kThreads) {
     return (unsigned)std::max<int64_t>(1, (work + threads - 1) / threads);
@@ -406,6 +412,24 @@ epg_status build_pipeline_blob(epg_ctx *ctx, epg_plan *pl) {
             int32_t hmax = 0;
             if ((st = read_i32(ctx, hm.as<int32_t>(), &hmax))) return st;
             if (hmax > 6) pl->fin_recs = nullptr;   // (the allocation is released with the plan)
+            if (hmax > kHeavyHalo) {                // hubs: list them for the block-per-vertex finalise
+                std::vector<int32_t> off(pl->S + 1), hv, md;
+                CU(cudaMemcpy(off.data(), pl->hv_off, sizeof(int32_t) * (pl->S + 1), cudaMemcpyDeviceToHost));
+                for (int64_t t = 0; t < pl->S; t++) {
+                    const int c = off[t + 1] - off[t];
+                    if (c > kBlockHalo) hv.push_back((int32_t)t);
+                    else if (c > kHeavyHalo) md.push_back((int32_t)t);
+                }
+                pl->n_heavy = (int64_t)hv.size();
+                pl->n_medium = (int64_t)md.size();
+                if ((st = plan_alloc_t(pl, ctx, &pl->heavy, pl->n_heavy)) ||
+                    (st = plan_alloc_t(pl, ctx, &pl->medium, pl->n_medium)))
+                    return st;
+                if (pl->n_heavy)
+                    CU(cudaMemcpy(pl->heavy, hv.data(), sizeof(int32_t) * pl->n_heavy, cudaMemcpyHostToDevice));
+                if (pl->n_medium)
+                    CU(cudaMemcpy(pl->medium, md.data(), sizeof(int32_t) * pl->n_medium, cudaMemcpyHostToDevice));
+            }
         }
         CHECK_LAUNCH();
     }
@@ -624,7 +648,17 @@ epg_status launch_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t step
                 CU(launch_pdl(k_finalise3<Fn>, grid_for(fin_work), kThreads, 0, ctx->stream,
                               (const int32_t *)pl->shared_ids, (const int32_t *)pl->hv_off,
                               (const int32_t *)pl->hv_list, (const float *)pl->halo_buf, (const float *)a.state_in,
-                              a.state_out, a.vconst, (int32_t)pl->S, pl->touched, pl->n));
+                              a.state_out, a.vconst, (int32_t)pl->S, pl->touched, pl->n, (int32_t)kHeavyHalo));
+            if (pl->n_medium > 0)
+                CU(launch_pdl(k_finalise_warp<Fn>, (unsigned)((pl->n_medium + 7) / 8), 256u, 0, ctx->stream,
+                              (const int32_t *)pl->medium, pl->n_medium, (const int32_t *)pl->shared_ids,
+                              (const int32_t *)pl->hv_off, (const int32_t *)pl->hv_list,
+                              (const float *)pl->halo_buf, a.state_out, a.vconst));
+            if (pl->n_heavy > 0)
+                CU(launch_pdl(k_finalise_heavy<Fn, 256>, (unsigned)pl->n_heavy, 256u, 0, ctx->stream,
+                              (const int32_t *)pl->heavy, (const int32_t *)pl->shared_ids,
+                              (const int32_t *)pl->hv_off, (const int32_t *)pl->hv_list,
+                              (const float *)pl->halo_buf, a.state_out, a.vconst));
             ctx->prof_end(1, t1);
         }
     }

@@ -242,11 +242,13 @@ template <class Fn>
 __global__ void k_finalise3(const int32_t *__restrict__ shared_ids, const int32_t *__restrict__ hv_off,
                             const int32_t *__restrict__ hv_list, const float *__restrict__ halo_buf,
                             const float *__restrict__ state_in, float *__restrict__ state_out,
-                            const float *__restrict__ vconst, int32_t S, int64_t touched, int64_t n) {
+                            const float *__restrict__ vconst, int32_t S, int64_t touched, int64_t n,
+                            int32_t heavy) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     ptx::pdl_wait();                               // the edge kernel's outputs are visible
     ptx::pdl_launch_dependents();
     if (t < S) {
+        if (hv_off[t + 1] - hv_off[t] > heavy) return;        // k_finalise_heavy's vertex
         const int64_t v = shared_ids[t];
         float acc[Fn::ROW];
 #pragma unroll
@@ -262,6 +264,83 @@ __global__ void k_finalise3(const int32_t *__restrict__ shared_ids, const int32_
     }
     const int64_t v = touched + (t - S);
     if (v < n) Fn::untouched(state_in + Fn::ROW * v, state_out + Fn::ROW * v);
+}
+
+// Heavy shared vertices (more than `heavy` halo entries: the hubs of power-law graphs),
+// one CTA each: thread t sums entries t, t + BLOCK, ... in order, then a fixed-shape tree
+// reduction in shared memory -- deterministic, and a hub no longer serialises on one thread.
+template <class Fn, int BLOCK>
+__global__ void __launch_bounds__(BLOCK) k_finalise_heavy(const int32_t *__restrict__ heavy_list,
+                                                          const int32_t *__restrict__ shared_ids,
+                                                          const int32_t *__restrict__ hv_off,
+                                                          const int32_t *__restrict__ hv_list,
+                                                          const float *__restrict__ halo_buf,
+                                                          float *__restrict__ state_out,
+                                                          const float *__restrict__ vconst) {
+    __shared__ float red[Fn::ROW][BLOCK];
+    ptx::pdl_wait();
+    const int s = heavy_list[blockIdx.x];
+    const int q0 = hv_off[s], q1 = hv_off[s + 1];
+    float acc[Fn::ROW];
+#pragma unroll
+    for (int c = 0; c < Fn::ROW; c++) acc[c] = 0.0f;
+    for (int q = q0 + threadIdx.x; q < q1; q += BLOCK) {
+        const int64_t h = hv_list[q];
+#pragma unroll
+        for (int c = 0; c < Fn::ROW; c++) acc[c] += halo_buf[Fn::ROW * h + c];
+    }
+#pragma unroll
+    for (int c = 0; c < Fn::ROW; c++) red[c][threadIdx.x] = acc[c];
+    __syncthreads();
+    for (int w = BLOCK / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+#pragma unroll
+            for (int c = 0; c < Fn::ROW; c++) red[c][threadIdx.x] += red[c][threadIdx.x + w];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const int64_t v = shared_ids[s];
+        float tot[Fn::ROW];
+#pragma unroll
+        for (int c = 0; c < Fn::ROW; c++) tot[c] = red[c][0];
+        Fn::finalise_add(state_out + Fn::ROW * v, tot, Fn::kUsesConst ? vconst[v] : 0.0f);
+    }
+}
+
+// Medium shared vertices, one warp each (8 per CTA): lane l sums entries l, l + 32, ... in
+// order, then a fixed xor-shuffle tree -- deterministic.
+template <class Fn>
+__global__ void __launch_bounds__(256) k_finalise_warp(const int32_t *__restrict__ list, int64_t count,
+                                                       const int32_t *__restrict__ shared_ids,
+                                                       const int32_t *__restrict__ hv_off,
+                                                       const int32_t *__restrict__ hv_list,
+                                                       const float *__restrict__ halo_buf,
+                                                       float *__restrict__ state_out,
+                                                       const float *__restrict__ vconst) {
+    ptx::pdl_wait();
+    const int64_t wi = blockIdx.x * 8ll + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (wi >= count) return;
+    const int s = list[wi];
+    const int q0 = hv_off[s], q1 = hv_off[s + 1];
+    float acc[Fn::ROW];
+#pragma unroll
+    for (int c = 0; c < Fn::ROW; c++) acc[c] = 0.0f;
+    for (int q = q0 + lane; q < q1; q += 32) {
+        const int64_t h = hv_list[q];
+#pragma unroll
+        for (int c = 0; c < Fn::ROW; c++) acc[c] += halo_buf[Fn::ROW * h + c];
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+        for (int c = 0; c < Fn::ROW; c++) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], off);
+    }
+    if (lane == 0) {
+        const int64_t v = shared_ids[s];
+        Fn::finalise_add(state_out + Fn::ROW * v, acc, Fn::kUsesConst ? vconst[v] : 0.0f);
+    }
 }
 
 // Finalise of a vertex range (multi-GPU shards): for every shared vertex v

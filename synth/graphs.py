@@ -48,3 +48,54 @@ def int_vector(seed: int, n: int, lo: int, hi: int) -> np.ndarray:
     """Integer-valued float32 vector, entries uniform in {lo..hi} (exact in fp32 sums)."""
     r = splitmix64(seed, np.arange(n, dtype=np.uint64))
     return (lo + (r % np.uint64(hi - lo + 1)).astype(np.int64)).astype(np.float32)
+
+
+def rmat(scale: int, edge_factor: int = 8, seed: int = 1607, a=0.57, b=0.19, c=0.19, chunk: int = 1 << 22):
+    """R-MAT edge list (Chakrabarti et al.): n = 2^scale vertices, m = edge_factor * n edges,
+    quadrant probabilities (a, b, c, d = 1 - a - b - c) per level; duplicates and self-loops
+    kept ('avg degree 16' read as 2m/n = 16, i.e. edge_factor 8).
+
+    Level l of edge e uses 16 bits of SplitMix64 draw (e * ceil(scale/4) + l // 4)."""
+    n = 1 << scale
+    m = edge_factor * n
+    per = (scale + 3) // 4
+    ta, tab, tabc = int(a * 65536), int((a + b) * 65536), int((a + b + c) * 65536)
+    out = np.empty((m, 2), dtype=np.int32)
+    for e0 in range(0, m, chunk):
+        e1 = min(m, e0 + chunk)
+        cnt = e1 - e0
+        base = (np.arange(e0, e1, dtype=np.uint64) * np.uint64(per))
+        u = np.zeros(cnt, np.int64)
+        v = np.zeros(cnt, np.int64)
+        for w in range(per):
+            r = splitmix64(seed, base + np.uint64(w))
+            for j in range(4):
+                lvl = 4 * w + j
+                if lvl >= scale:
+                    break
+                q = ((r >> np.uint64(16 * j)) & np.uint64(0xFFFF)).astype(np.int64)
+                bit = np.int64(1) << np.int64(scale - 1 - lvl)
+                down = (q >= tab)                  # quadrants c, d: row bit set
+                right = ((q >= ta) & (q < tab)) | (q >= tabc)   # quadrants b, d: column bit set
+                u += bit * down
+                v += bit * right
+        out[e0:e1, 0] = u
+        out[e0:e1, 1] = v
+    return n, out
+
+
+def stencil2d_spmv(g: int):
+    """2D 5-point Laplacian on a g x g grid as the bipartite data-affinity graph of SpMV
+    (P:859-861): vertices 0..N-1 are x_j (columns), N..2N-1 are y_i (rows), one edge
+    (j, N + i) per nonzero A[i, j] in row-major (CUSP) order; values 4 / -1."""
+    N = g * g
+    i = np.arange(N, dtype=np.int64)
+    r, c = i // g, i % g
+    cols, vals, rows = [], [], []
+    for dr, dc, val in ((-1, 0, -1.0), (0, -1, -1.0), (0, 0, 4.0), (0, 1, -1.0), (1, 0, -1.0)):
+        ok = (r + dr >= 0) & (r + dr < g) & (c + dc >= 0) & (c + dc < g)
+        rows.append(i[ok]); cols.append((i + dr * g + dc)[ok]); vals.append(np.full(int(ok.sum()), val, np.float32))
+    rows = np.concatenate(rows); cols = np.concatenate(cols); vals = np.concatenate(vals)
+    order = np.lexsort((cols, rows))
+    edges = np.stack([cols[order], N + rows[order]], axis=1).astype(np.int32)
+    return 2 * N, edges, vals[order]

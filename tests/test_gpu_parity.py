@@ -354,3 +354,31 @@ def test_single_edge_and_p1(ctx):
     x = S.int_vector(4, n, 0, 7)
     got = _run_scalar(ctx, epg.KERNEL_GATHER_SCATTER, e, n, O.partition(e, n, 1), 300, x, None)
     assert np.array_equal(got.astype(np.float64), O.gather_scatter(e, n, x))
+
+
+@pytest.mark.parametrize("P", [512, 1024])
+def test_rmat_gather_scatter_exact(ctx, P):
+    """C4's shape at scale 14 (hubs, self-loops, duplicates): EP partition through the
+    library, staged kernel, integer-valued x -> bit-exact vs the oracle."""
+    from paper_1605_02043_b200 import epg
+    n, e = S.rmat(14)
+    x = S.int_vector(1608, n, 0, 7)
+    k = O.num_parts(e.shape[0], P)
+    E = dev(e)
+    part, rep = ctx.partition(E, n, P)
+    assert np.array_equal(part.cpu().numpy(), O.partition(e, n, P))
+    got = _run_scalar(ctx, epg.KERNEL_GATHER_SCATTER, e, n, part.cpu().numpy(), k, x, None)
+    assert np.array_equal(got.astype(np.float64), O.gather_scatter(e, n, x))
+
+
+def test_stencil_spmv_c5_shape_exact(ctx):
+    """C5's shape (2D 5-point Laplacian, bipartite COO in row-major order) at g = 300."""
+    from paper_1605_02043_b200 import epg
+    n, e, w = S.stencil2d_spmv(300)
+    N = n // 2
+    x = np.concatenate([S.int_vector(1609, N, -8, 8), np.zeros(N, np.float32)])
+    P = 1024
+    k = O.num_parts(e.shape[0], P)
+    part, _ = ctx.partition(dev(e), n, P)
+    got = _run_scalar(ctx, epg.KERNEL_SPMV, e, n, part.cpu().numpy(), k, x, w)
+    assert np.array_equal(got.astype(np.float64), O.spmv(e, n, w, x))
