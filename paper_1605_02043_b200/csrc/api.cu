@@ -596,7 +596,16 @@ epg_status run_pipelined(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t s
 // occupancy kernel limits: execution partitions of <= 1024 edges and <= 768 staged rows
 // (704 rows keep a cfd CTA at ~55 KB of shared memory: four CTAs per SM)
 constexpr int kOccThreads = 256, kOccEPT = 4;
-constexpr int kExecMaxEdges = kOccThreads * kOccEPT;
+// edge cap of an execution partition: 1024 (default) or 512 via EPG_EXEC_MAX_EDGES
+int exec_max_edges() {
+    static int v = [] {
+        const char *e = std::getenv("EPG_EXEC_MAX_EDGES");
+        int x = e ? std::atoi(e) : 1024;
+        return x <= 512 ? 512 : 1024;
+    }();
+    return v;
+}
+#define kExecMaxEdges exec_max_edges()
 // staged-row cap of an execution partition: 704 (default) keeps 4 CTAs/SM; up to 1024
 // (3 CTAs/SM, fewer split partitions) via EPG_EXEC_MAX_ROWS, read once
 int exec_max_rows() {
@@ -626,9 +635,9 @@ cudaError_t launch_pdl(K kern, unsigned grid, unsigned block, size_t smem, cudaS
     return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
-template <class Fn, int W, int VPT>
+template <class Fn, int W, int VPT, int EPT = kOccEPT>
 epg_status launch_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, OccArgs a, size_t smem) {
-    auto kern = k_edge_occ<Fn, kOccThreads, kOccEPT, VPT, W>;
+    auto kern = k_edge_occ<Fn, kOccThreads, EPT, VPT, W>;
     CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     float *bufs[2] = {static_cast<float *>(state->state_in), static_cast<float *>(state->state_out)};
     const int64_t fin_work = pl->S + (pl->n - pl->touched);
@@ -677,7 +686,7 @@ epg_status run_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, 
     const int recs_bytes = up16i(4 * Fn::REC * pl->Lcap + 64);
     a.rows_land = up16i(recs_bytes - (4 * Fn::ROW * pl->Lcap + 16) - 16);
     a.off_phi = a.off_recs + recs_bytes;
-    const size_t smem = (size_t)a.off_phi + up16i(4 * Fn::PHIREC * (pl->Scap + 1));
+    const size_t smem = (size_t)a.off_phi + up16i(4 * Fn::PHIREC * (kPhiSentinel + 1));
     if (smem + 1024 > (size_t)dev_max) return EPG_OK;
     *fits = true;
     a.desc = pl->desc3;
@@ -688,6 +697,13 @@ epg_status run_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, 
     a.halo_buf = pl->halo_buf;
     a.first = 0;
     const bool v4 = pl->Lcap > 3 * kOccThreads;
+    if (pl->Scap <= 2 * kOccThreads && pl->Lcap <= 2 * kOccThreads) {   // small execution partitions
+        switch (pl->inc_width) {
+            case 4: return launch_occ<Fn, 4, 2, 2>(ctx, pl, state, steps, a, smem);
+            case 8: return launch_occ<Fn, 8, 2, 2>(ctx, pl, state, steps, a, smem);
+            default: return launch_occ<Fn, 0, 2, 2>(ctx, pl, state, steps, a, smem);
+        }
+    }
     switch (pl->inc_width) {
         case 4: return v4 ? launch_occ<Fn, 4, 4>(ctx, pl, state, steps, a, smem)
                           : launch_occ<Fn, 4, 3>(ctx, pl, state, steps, a, smem);
@@ -708,7 +724,7 @@ epg_status run_edges_range(epg_ctx *ctx, epg_plan *pl, epg_state *state, int64_t
     const int recs_bytes = up16i(4 * Fn::REC * pl->Lcap + 64);
     a.rows_land = up16i(recs_bytes - (4 * Fn::ROW * pl->Lcap + 16) - 16);
     a.off_phi = a.off_recs + recs_bytes;
-    const size_t smem = (size_t)a.off_phi + up16i(4 * Fn::PHIREC * (pl->Scap + 1));
+    const size_t smem = (size_t)a.off_phi + up16i(4 * Fn::PHIREC * (kPhiSentinel + 1));
     a.desc = pl->desc3;
     a.blob = pl->blob3;
     a.slots = pl->slots;

@@ -30,6 +30,8 @@ namespace epg {
 // blob of the occupancy kernel: [halo ids nH x i32] pad16 [incidence] (W as in the
 // pipelined blob: W x L u16 padded lists, or W = 0: 2s u16 entries + L u16 offsets)
 __host__ __device__ __forceinline__ int blob3_inc_offset(int nH) { return (4 * nH + 15) & ~15; }
+// padded incidence entries point at this Phi record, kept zero (>= every EPT x BLOCK)
+constexpr int kPhiSentinel = 1024;
 __host__ __device__ __forceinline__ int blob3_bytes_for(int nH, int s, int L, int W) {
     const int inc = W > 0 ? 2 * W * L : 4 * s + 2 * L;
     return (blob3_inc_offset(nH) + inc + 15) & ~15;
@@ -54,6 +56,7 @@ __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
     __shared__ __align__(8) uint64_t bar;
     constexpr int ROW = Fn::ROW, PW = Fn::PAYW;
     const int tid = threadIdx.x;
+    EPG_TP(0, 0);
     const PartDesc d = a.desc[a.first + blockIdx.x];
     const int L = d.nO + d.nH;
     unsigned char *sblob = occ_smem;
@@ -79,7 +82,7 @@ __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
         const int i = tid + r * BLOCK;
         sl[r] = 0;
 #pragma unroll
-        for (int c = 0; c < PW; c++) pw[r][c] = 1.0f;
+        for (int c = 0; c < PW; c++) pw[r][c] = i < d.s ? 1.0f : 0.0f;
         if (i < d.s) {
             sl[r] = __ldg(a.slots + d.e0 + i);
             if (a.payload) {
@@ -97,20 +100,24 @@ __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
     ptx::pdl_wait();                               // state_in is final from here on
     if (tid == 0) region_bulk(rows_base, g_rows, rows_bytes, &bar);
     __syncthreads();                               // barrier initialisation visible
+    EPG_TP(0, 1);
     ptx::mbar_wait(&bar, 0);
+    EPG_TP(0, 2);
     // ragged ends of the owned range + halo rows
     if (tid < 32) region_ragged(rows_base, g_rows, rows_bytes, tid);
     {
         const int32_t *hid = reinterpret_cast<const int32_t *>(sblob);
         float *hr = rows + ROW * d.nO;
-        for (int w = tid; w < ROW * d.nH; w += BLOCK) {
-            const int j = w / ROW, c = w - j * ROW;
-            ptx::cp_async4(hr + w, a.state_in + (int64_t)ROW * hid[j] + c);
+        for (int j = tid; j < d.nH; j += BLOCK) {      // one halo row per thread
+            const float *src = a.state_in + (int64_t)ROW * hid[j];
+#pragma unroll
+            for (int c = 0; c < ROW; c++) ptx::cp_async4(hr + ROW * j + c, src + c);
         }
     }
     ptx::cp_async_commit();
     ptx::cp_async_wait<0>();
     __syncthreads();
+    EPG_TP(0, 3);
     // rows -> registers -> derived records (in place: the rows sit in the upper part)
     float rv[VPT][ROW];
 #pragma unroll
@@ -135,9 +142,10 @@ __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
         if (i < d.s) Fn::edge_rec_pw(recs, (int)(sl[r] & 0xffffu), (int)(sl[r] >> 16), pw[r], i, phis);
     }
     if constexpr (W > 0) {
-        if (tid == 0) Fn::zero_phi(phis, d.s);
+        if (tid == 0) Fn::zero_phi(phis, kPhiSentinel);
     }
     __syncthreads();
+    EPG_TP(0, 4);
     // reduce per local vertex into registers
     const uint16_t *inc = reinterpret_cast<const uint16_t *>(sblob + blob3_inc_offset(d.nH));
     float out[VPT][ROW];
@@ -231,7 +239,9 @@ __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
         ragged_store(gb, b_bytes, outB_base);
     }
     ptx::pdl_launch_dependents();                  // the finalise may start launching
+    EPG_TP(0, 5);
     if (tid == 0) ptx::bulk_wait_read0();          // shared memory must outlive the stores' reads
+    EPG_TP(0, 6);
 }
 
 // Boundary finalise (a6): U'_v = (U + dt F_owner)_v + dt * sum of v's halo partials, in
@@ -483,7 +493,7 @@ __global__ void k_build_blob3(const int32_t *__restrict__ peb, const int32_t *__
         for (int j = threadIdx.x; j < L; j += blockDim.x) {
             const int q0 = inc_off[lbase + j], q1 = j + 1 < L ? inc_off[lbase + j + 1] : 2 * s;
             for (int r = 0; r < W; r++)
-                ic[W * j + r] = q0 + r < q1 ? inc[2 * (int64_t)e0 + q0 + r] : (uint16_t)(s << 1);
+                ic[W * j + r] = q0 + r < q1 ? inc[2 * (int64_t)e0 + q0 + r] : (uint16_t)(kPhiSentinel << 1);
         }
     } else {
         uint16_t *io = ic + 2 * s;
