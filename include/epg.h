@@ -151,7 +151,7 @@ int64_t epg_num_parts(int64_t m, int32_t part_size);
  * order P:380; EPG-1 replaces METIS P:384/P:418, reading Z3). Partition sizes are
  * s_i = floor(m/k) + [i < m mod k] (Eq. (1) "L_i = m/k", exact +-1, Z2).
  * shards = G > 1 runs the hierarchical variant (shard-level EPG-1, then per shard).
- *   edges [m][2] HOST; part_of_edge [m] HOST out.
+ *   edges [m][2] HOST; part_of_edge [m] HOST out; 0 < m < 2^31.
  * Returns EPG_ERR_INPUT / EPG_ERR_INFEASIBLE as above; writes the message into
  * errbuf (errbuf_len bytes, may be NULL). */
 epg_status epg_partition_host(const int32_t *edges, int64_t m, int32_t n_vertices, int32_t part_size,

@@ -2,9 +2,10 @@
 //
 // The paper runs the optimisation "using a separate thread on the CPU while kernel is
 // executed on the GPU": EP partitioning is sequential graph growing and
-// belongs on the host. This is the library's own implementation (binary heap with lazy
-// deletion, counting-sort chains); it shares no code with oracle/ and must agree with
-// it bit for bit because EPG-1's order is fully fixed by its stamps (O5).
+// belongs on the host. This is the library's own implementation (fixed-width T, packed
+// per-task state, one lazy-deletion min-heap per gain value, counting-sort chains); it
+// shares no code with oracle/ and must agree with it bit for bit because EPG-1's order is
+// fully fixed by its stamps (O5).
 //
 //  T (Def. 3, contracted; weight "very large" P:377; chain "in index order"
 //  P:380): every vertex's endpoint slots in ascending (task, side) order form a chain;
@@ -19,6 +20,10 @@
 #include "epg_internal.h"
 
 #include <algorithm>
+#ifdef EPG_PART_TIMING
+#include <chrono>
+#include <cstdio>
+#endif
 #include <cstring>
 #include <queue>
 #include <string>
@@ -30,10 +35,14 @@ namespace {
 
 constexpr int64_t kInf = INT64_MAX;
 
+// T with at most 4 chain links per task (2 endpoint slots x predecessor / successor in the
+// vertex chains): fixed 4-slot rows, ascending, unused slots -1. A weight-w edge of T
+// (w links to the same task) is kept as w repeated unit entries: visiting them one by one
+// leaves the same gains, stamps and current heap entries as adding w at once (the
+// intermediate entry goes stale under lazy deletion), so the gain never exceeds 4.
 struct TaskGraph {
-    std::vector<int64_t> ptr;   // [ntask + 1]
-    std::vector<int32_t> adj;   // neighbours, ascending per task
-    std::vector<int32_t> w;
+    int64_t ntask = 0;
+    std::vector<int32_t> nb;   // [4 * ntask]
 };
 
 // Contracted clone-and-connect graph from the edge list.
@@ -43,91 +52,109 @@ TaskGraph build_task_graph(const int32_t *edges, int64_t m, int32_t n) {
     for (int64_t j = 0; j < 2 * m; j++) vbeg[edges[j] + 1]++;
     for (int32_t v = 0; v < n; v++) vbeg[v + 1] += vbeg[v];
     std::vector<int64_t> fill(vbeg.begin(), vbeg.end() - 1);
-    std::vector<int64_t> chain(2 * m);
-    for (int64_t j = 0; j < 2 * m; j++) chain[fill[edges[j]]++] = j;
-    // each task has at most 4 chain neighbours (2 slots x predecessor/successor)
-    std::vector<int32_t> nb(4 * m), cnt(m, 0);
+    std::vector<uint32_t> chain(2 * m);   // m < 2^31 (checked by host_partition)
+    for (int64_t j = 0; j < 2 * m; j++) chain[fill[edges[j]]++] = static_cast<uint32_t>(j);
+    std::vector<int64_t>().swap(fill);
+    TaskGraph T;
+    T.ntask = m;
+    T.nb.assign(4 * m, -1);
+    std::vector<uint8_t> cnt(m, 0);
     for (int32_t v = 0; v < n; v++) {
         for (int64_t q = vbeg[v]; q + 1 < vbeg[v + 1]; q++) {
             int64_t t0 = chain[q] >> 1, t1 = chain[q + 1] >> 1;
             if (t0 == t1) continue;
-            nb[4 * t0 + cnt[t0]++] = static_cast<int32_t>(t1);
-            nb[4 * t1 + cnt[t1]++] = static_cast<int32_t>(t0);
+            T.nb[4 * t0 + cnt[t0]++] = static_cast<int32_t>(t1);
+            T.nb[4 * t1 + cnt[t1]++] = static_cast<int32_t>(t0);
         }
     }
-    TaskGraph T;
-    T.ptr.assign(m + 1, 0);
-    T.adj.reserve(4 * m);
-    T.w.reserve(4 * m);
-    for (int64_t t = 0; t < m; t++) {
-        int32_t *b = &nb[4 * t];
-        std::sort(b, b + cnt[t]);
-        for (int c = 0; c < cnt[t]; c++) {
-            if (c > 0 && b[c] == b[c - 1]) { T.w.back()++; continue; }
-            T.adj.push_back(b[c]);
-            T.w.push_back(1);
-        }
-        T.ptr[t + 1] = static_cast<int64_t>(T.adj.size());
-    }
+    // per task: sort its <= 4 links ascending (slots past cnt stay -1)
+    for (int64_t t = 0; t < m; t++) std::sort(&T.nb[4 * t], &T.nb[4 * t] + cnt[t]);
     return T;
 }
 
-struct HeapEntry {
-    int64_t gain, stamp;
-    int32_t task;
+// Per-task growing state in one 16-byte record (one cache line per neighbour visit).
+struct TaskState {
+    int32_t part;   // -1 unassigned
+    int32_t lst;    // local stamp (kNoStamp = none since the last reset)
+    int32_t gst;    // global stamp (kNoStamp = none)
+    int32_t gain;   // weight into the current partition, 0..4
 };
-struct HeapLess {  // max-heap on gain, then min stamp
-    bool operator()(const HeapEntry &a, const HeapEntry &b) const {
-        if (a.gain != b.gain) return a.gain < b.gain;
-        return a.stamp > b.stamp;
+constexpr int32_t kNoStamp = INT32_MAX;
+
+// Frontier: one min-heap on the local stamp per gain value (0..4); an entry is current
+// iff the task is unassigned and its gain still equals the bucket (lazy deletion). The
+// pick -- largest gain, then smallest local stamp -- is EPG-1's (O5).
+struct Frontier {
+    std::vector<uint64_t> h[5];   // (stamp << 32) | task, min-heaps
+    void clear() { for (auto &v : h) v.clear(); }
+    void push(int gain, int32_t stamp, int32_t task) {
+        auto &v = h[gain];
+        v.push_back((static_cast<uint64_t>(static_cast<uint32_t>(stamp)) << 32) | static_cast<uint32_t>(task));
+        std::push_heap(v.begin(), v.end(), std::greater<uint64_t>());
+    }
+    // pop the best current entry; -1 when empty
+    int32_t pop(const std::vector<TaskState> &st) {
+        for (int g = 4; g >= 0; g--) {
+            auto &v = h[g];
+            while (!v.empty()) {
+                const uint64_t top = v.front();
+                std::pop_heap(v.begin(), v.end(), std::greater<uint64_t>());
+                v.pop_back();
+                const int32_t t = static_cast<int32_t>(top & 0xffffffffu);
+                if (st[t].part == -1 && st[t].gain == g) return t;
+            }
+        }
+        return -1;
     }
 };
 
 void grow(const TaskGraph &T, const int64_t *sizes, int64_t nparts, int32_t *part) {
-    const int64_t ntask = static_cast<int64_t>(T.ptr.size()) - 1;
-    std::vector<int64_t> gst(ntask, kInf), lst(ntask, kInf), gain(ntask, 0);
+    const int64_t ntask = T.ntask;
+    std::vector<TaskState> st(ntask, TaskState{-1, kNoStamp, kNoStamp, 0});
     std::vector<int32_t> by_gst;
     by_gst.reserve(ntask);
     std::vector<int32_t> dirty;
-    std::priority_queue<HeapEntry, std::vector<HeapEntry>, HeapLess> heap;
-    std::fill(part, part + ntask, -1);
+    Frontier fr;
     size_t gnext = 0;
-    int64_t lowest = 0, gclock = 0;
+    int64_t lowest = 0;
+    int32_t gclock = 0;
     auto next_unassigned = [&]() {
-        while (lowest < ntask && part[lowest] != -1) lowest++;
+        while (lowest < ntask && st[lowest].part != -1) lowest++;
         return lowest;
     };
     for (int64_t i = 0; i < nparts; i++) {
-        while (gnext < by_gst.size() && part[by_gst[gnext]] != -1) gnext++;
-        int64_t seed = gnext < by_gst.size() ? by_gst[gnext] : next_unassigned();
-        for (int32_t t : dirty) { lst[t] = kInf; gain[t] = 0; }
+        while (gnext < by_gst.size() && st[by_gst[gnext]].part != -1) gnext++;
+        const int64_t seed = gnext < by_gst.size() ? by_gst[gnext] : next_unassigned();
+        for (int32_t t : dirty) { st[t].lst = kNoStamp; st[t].gain = 0; }
         dirty.clear();
-        heap = decltype(heap)();
+        fr.clear();
         if (sizes[i] == 0) continue;
-        int64_t clock = 0;
-        lst[seed] = clock++;
+        int32_t clock = 0;
+        st[seed].lst = clock++;
         dirty.push_back(static_cast<int32_t>(seed));
-        heap.push({0, lst[seed], static_cast<int32_t>(seed)});
+        fr.push(0, st[seed].lst, static_cast<int32_t>(seed));
         for (int64_t r = 0; r < sizes[i]; r++) {
-            int32_t t = -1;
-            while (!heap.empty()) {
-                HeapEntry top = heap.top();
-                heap.pop();
-                if (part[top.task] == -1 && gain[top.task] == top.gain) { t = top.task; break; }
-            }
+            int32_t t = fr.pop(st);
             if (t < 0) {  // frontier exhausted: restart on the remainder
                 t = static_cast<int32_t>(next_unassigned());
-                lst[t] = clock++;
+                st[t].lst = clock++;
                 dirty.push_back(t);
             }
+            st[t].part = static_cast<int32_t>(i);
             part[t] = static_cast<int32_t>(i);
-            for (int64_t q = T.ptr[t]; q < T.ptr[t + 1]; q++) {
-                int32_t u = T.adj[q];
-                if (part[u] != -1) continue;
-                if (lst[u] == kInf) { lst[u] = clock++; dirty.push_back(u); }
-                gain[u] += T.w[q];
-                if (gst[u] == kInf) { gst[u] = gclock++; by_gst.push_back(u); }
-                heap.push({gain[u], lst[u], u});
+            const int32_t *nb = &T.nb[4 * static_cast<int64_t>(t)];
+            for (int c = 0; c < 4 && nb[c] >= 0; c++) __builtin_prefetch(&st[nb[c]]);
+            for (int c = 0; c < 4 && nb[c] >= 0; c++) {
+                TaskState &u = st[nb[c]];
+                if (u.part != -1) continue;
+                if (u.lst == kNoStamp) {
+                    u.lst = clock++;
+                    dirty.push_back(nb[c]);
+                    __builtin_prefetch(&T.nb[4 * static_cast<int64_t>(nb[c])]);
+                }
+                u.gain += 1;
+                if (u.gst == kNoStamp) { u.gst = gclock++; by_gst.push_back(nb[c]); }
+                fr.push(u.gain, u.lst, nb[c]);
             }
         }
     }
@@ -139,6 +166,10 @@ epg_status host_partition(const int32_t *edges, int64_t m, int32_t n, int32_t pa
                           int32_t *part, std::string *err) {
     if (m <= 0 || n <= 0 || edges == nullptr || part == nullptr) {
         *err = "partition: need m > 0, n > 0 and non-NULL arrays";
+        return EPG_ERR_INPUT;
+    }
+    if (m >= (int64_t(1) << 31)) {   // task ids and stamps are int32
+        *err = "partition: m must be below 2^31";
         return EPG_ERR_INPUT;
     }
     for (int64_t e = 0; e < m; e++) {
@@ -159,9 +190,20 @@ epg_status host_partition(const int32_t *edges, int64_t m, int32_t n, int32_t pa
     }
     std::vector<int64_t> s(k);
     for (int64_t i = 0; i < k; i++) s[i] = m / k + (i < m % k ? 1 : 0);
+#ifdef EPG_PART_TIMING
+    auto c0 = std::chrono::steady_clock::now();
+#endif
     TaskGraph T = build_task_graph(edges, m, n);
+#ifdef EPG_PART_TIMING
+    auto c1 = std::chrono::steady_clock::now();
+#endif
     if (shards == 1) {
         grow(T, s.data(), k, part);
+#ifdef EPG_PART_TIMING
+        auto c2 = std::chrono::steady_clock::now();
+        fprintf(stderr, "T build %.3f s, grow %.3f s\n", std::chrono::duration<double>(c1 - c0).count(),
+                std::chrono::duration<double>(c2 - c1).count());
+#endif
         return EPG_OK;
     }
     // hierarchical: shard-level growing, then growing inside each shard
@@ -178,15 +220,17 @@ epg_status host_partition(const int32_t *edges, int64_t m, int32_t n, int32_t pa
     for (int g = 0; g < shards; g++) {
         const auto &mem = members[g];
         TaskGraph Tg;
-        Tg.ptr.assign(mem.size() + 1, 0);
+        Tg.ntask = static_cast<int64_t>(mem.size());
+        Tg.nb.assign(4 * mem.size(), -1);
         for (size_t j = 0; j < mem.size(); j++) {
-            int32_t t = mem[j];
-            for (int64_t q = T.ptr[t]; q < T.ptr[t + 1]; q++) {
-                if (shard[T.adj[q]] != g) continue;
-                Tg.adj.push_back(local[T.adj[q]]);
-                Tg.w.push_back(T.w[q]);
+            const int64_t t = mem[j];
+            int o = 0;   // ascending ids map to ascending local ids: order preserved
+            for (int c = 0; c < 4 && T.nb[4 * t + c] >= 0; c++) {
+                const int32_t u = T.nb[4 * t + c];
+                if (shard[u] != g) continue;
+                Tg.nb[4 * j + o] = local[u];
+                o++;
             }
-            Tg.ptr[j + 1] = static_cast<int64_t>(Tg.adj.size());
         }
         const int64_t p0 = g * k / shards, p1 = (g + 1) * k / shards;
         std::vector<int32_t> sub(mem.size());

@@ -88,3 +88,11 @@ def test_host_partition_errors():
     with pytest.raises(epg.EpgError) as ex:
         epg.partition_host(np.zeros((0, 2), np.int32), 2, 2)
     assert ex.value.status == epg.ERR_INPUT
+
+
+def test_host_partition_rmat_bitexact():
+    """Hub vertices and parallel edges (R-MAT, Z15): many weight>1 edges of T."""
+    from paper_1605_02043_b200 import epg
+    n, e = S.rmat(10)
+    for P, G in ((64, 1), (256, 1), (128, 4)):
+        assert np.array_equal(epg.partition_host(e, n, P, G), O.partition(e, n, P, G))
