@@ -593,6 +593,7 @@ def run_ours(args, rank, local_rank, world):
         "partition": {"load_count": rep.load_count, "touched": rep.touched, "cut_cost": rep.cut_cost,
                       "replication": rep.replication, "redundant_fraction": rep.redundant_fraction,
                       "max_size": rep.max_size, "min_size": rep.min_size, "shared_vertices": plan.shared,
+                      "hubs": plan.hubs, "hub_min_halo_entries": plan.hub_min, "k_exec": plan.k_exec,
                       "host_partition_s": t_part, "remap_s": t_remap, "mesh_gen_s": t_gen},
         "comparators": comparators,
         "bytes_per_edge_ncu": variants,

@@ -267,6 +267,22 @@ epg_status epg_accumulate_rows(epg_ctx *ctx, const float *src, const int32_t *id
  * differ in how partitions are staged and scheduled. */
 epg_status epg_set_variant(epg_ctx *ctx, int32_t variant);
 
+/* Hub split (power-law graphs, the hub discussion of P:642-683):
+ * plans created by later epg_remap calls on ctx treat every shared vertex with at least
+ * `min_halo_entries` halo entries as a hub. Variant 3 then sums each execution
+ * partition's partial of a hub in shared memory, as for any vertex. It adds that partial
+ * with one red.global.add into a per-hub accumulator, and a hub finalise applies the
+ * accumulator. The finalise then no longer gathers the hub's scattered halo partials.
+ * The sum order over partitions is then not fixed, so results are deterministic only up
+ * to fp32 rounding for hubs (exact for integer-valued data). 0 turns it off. The default
+ * (-1 = unset) is 7, overridable by the EPG_HUB_MIN environment variable. Meshes with
+ * degree <= 4 (cfd) never have hubs at the default. -1 restores the default; values
+ * below -1 return EPG_ERR_INPUT. */
+epg_status epg_set_hub_split(epg_ctx *ctx, int32_t min_halo_entries);
+/* Hub count of a plan (-1 for NULL); *min_halo_entries (may be NULL) receives the
+ * threshold it was built with (0 = off). */
+int64_t epg_plan_hubs(const epg_plan *plan, int32_t *min_halo_entries);
+
 /* -- measurement -------------------------------------------------------------- */
 /* Kernel timing for bench.py: while enabled, epg_run / epg_run_naive record a CUDA event
  * pair on the ctx stream around every kernel they launch. epg_profile_read synchronises

@@ -25,6 +25,7 @@ struct epg_ctx {
     // profiling: event pairs around launches, per kernel class (0 edge, 1 finalise/update)
     bool profiling = false;
     int variant = 0;  // 0 auto, 1 one CTA per partition, 2 pipelined TMA, 3 occupancy TMA
+    int hub_min = -1; // hub split: shared vertices with >= hub_min halo entries (0 off, -1 default)
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_used;
     cudaEvent_t take_event() {
@@ -83,6 +84,13 @@ struct epg_plan {
     int64_t n_heavy = 0;
     int32_t *medium = nullptr;  // shared vertices with (kHeavyHalo, kBlockHalo] halo entries
     int64_t n_medium = 0;
+    // hub split (occupancy kernel only): hubs = shared vertices with >= hub_min halo entries
+    int32_t hub_min = 0;
+    int64_t n_hub = 0;
+    int32_t *hub_sid = nullptr;   // [n_hub] shared index of hub i
+    float *hub_acc = nullptr;     // [n_hub][5] partial sums, zero between steps
+    int finalise_skip = 8;        // k_finalise3 leaves vertices with more halo entries
+    int hub_words = 1;            // blob3 words per halo row (2 with hub indices)
     // the EP map the plan executes (k, C of the paper's partitions; the plan itself may
     // split oversized partitions into contiguous execution ranges)
     int64_t k_ep = 0, C_ep = 0;
@@ -107,6 +115,13 @@ using namespace epg;
 constexpr int kThreads = 256;
 constexpr int kHeavyHalo = 8;      // halo entries above which a shared vertex leaves the thread path
 constexpr int kBlockHalo = 1024;   // ... and above which a whole CTA (not a warp) finalises it
+constexpr int kHubMinDefault = 7;  // hub split default: >= 7 halo entries (the rest fit k_finalise_rec)
+
+int hub_min_for(const epg_ctx *ctx) {
+    if (ctx->hub_min >= 0) return ctx->hub_min;
+    const char *e = std::getenv("EPG_HUB_MIN");
+    return e ? std::max(0, std::atoi(e)) : kHubMinDefault;
+}
 
 inline unsigned grid_for(int64_t work, int threads = kThreads) {
     return (unsigned)std::max<int64_t>(1, (work + threads - 1) / threads);
@@ -389,11 +404,70 @@ epg_status build_pipeline_blob(epg_ctx *ctx, epg_plan *pl) {
                                                       pl->slots, pl->inc, pl->inc_off, off.as<int32_t>(),
                                                       hoff.as<int32_t>(), W, pl->blob, pl->hid_blob, pl->desc);
     CHECK_LAUNCH();
-    {   // occupancy-kernel blobs
+    {   // occupancy-kernel blobs; hub split and finalise tiers first (the hubs shape the blob)
+        Tmp hub_of_h(ctx);
+        int hw = 1;
+        if (pl->S > 0) {
+            pl->hub_min = hub_min_for(ctx);
+            Tmp hm(ctx);
+            CU(hm.alloc(2 * sizeof(int32_t)));
+            CU(cudaMemsetAsync(hm.p, 0, 2 * sizeof(int32_t), ctx->stream));
+            if ((st = plan_alloc_t(pl, ctx, &pl->fin_recs, 2 * pl->S))) return st;
+            k_finalise_records<<<grid_for(pl->S), kThreads, 0, ctx->stream>>>(
+                pl->shared_ids, pl->hv_off, pl->hv_list, (int32_t)pl->S, pl->hub_min, pl->fin_recs, hm.as<int32_t>());
+            int32_t hmax = 0, nhub = 0;
+            if ((st = read_i32(ctx, hm.as<int32_t>(), &hmax)) || (st = read_i32(ctx, hm.as<int32_t>() + 1, &nhub)))
+                return st;
+            if (hmax > 6) pl->fin_recs = nullptr;   // (the allocation is released with the plan)
+            pl->finalise_skip = nhub > 0 ? std::min(kHeavyHalo, pl->hub_min - 1) : kHeavyHalo;
+            if (hmax > kHeavyHalo || nhub > 0) {    // list medium / heavy vertices and hubs on the host
+                std::vector<int32_t> off(pl->S + 1), hv, md, hubs, hub_of_s;
+                CU(cudaMemcpy(off.data(), pl->hv_off, sizeof(int32_t) * (pl->S + 1), cudaMemcpyDeviceToHost));
+                if (nhub > 0) hub_of_s.assign(pl->S, -1);
+                for (int64_t t = 0; t < pl->S; t++) {
+                    const int c = off[t + 1] - off[t];
+                    if (nhub > 0 && c >= pl->hub_min) {
+                        hub_of_s[t] = (int32_t)hubs.size();
+                        hubs.push_back((int32_t)t);
+                    } else if (c > kBlockHalo) hv.push_back((int32_t)t);
+                    else if (c > kHeavyHalo) md.push_back((int32_t)t);
+                }
+                pl->n_heavy = (int64_t)hv.size();
+                pl->n_medium = (int64_t)md.size();
+                pl->n_hub = (int64_t)hubs.size();
+                if ((st = plan_alloc_t(pl, ctx, &pl->heavy, pl->n_heavy)) ||
+                    (st = plan_alloc_t(pl, ctx, &pl->medium, pl->n_medium)) ||
+                    (st = plan_alloc_t(pl, ctx, &pl->hub_sid, pl->n_hub)) ||
+                    (st = plan_alloc_t(pl, ctx, &pl->hub_acc, 5 * pl->n_hub)))
+                    return st;
+                if (pl->n_heavy)
+                    CU(cudaMemcpy(pl->heavy, hv.data(), sizeof(int32_t) * pl->n_heavy, cudaMemcpyHostToDevice));
+                if (pl->n_medium)
+                    CU(cudaMemcpy(pl->medium, md.data(), sizeof(int32_t) * pl->n_medium, cudaMemcpyHostToDevice));
+                if (pl->n_hub) {
+                    CU(cudaMemcpy(pl->hub_sid, hubs.data(), sizeof(int32_t) * pl->n_hub, cudaMemcpyHostToDevice));
+                    CU(cudaMemset(pl->hub_acc, 0, sizeof(float) * 5 * pl->n_hub));
+                    Tmp hos(ctx);
+                    CU(hos.alloc(sizeof(int32_t) * pl->S));
+                    CU(cudaMemcpyAsync(hos.p, hub_of_s.data(), sizeof(int32_t) * pl->S, cudaMemcpyHostToDevice,
+                                       ctx->stream));
+                    CU(hub_of_h.alloc(sizeof(int32_t) * std::max<int64_t>(1, pl->C)));
+                    CU(cudaMemsetAsync(hub_of_h.p, 0xff, sizeof(int32_t) * std::max<int64_t>(1, pl->C), ctx->stream));
+                    k_hub_mark<<<grid_for(pl->S), kThreads, 0, ctx->stream>>>(hos.as<int32_t>(), (int32_t)pl->S,
+                                                                             pl->hv_off, pl->hv_list,
+                                                                             hub_of_h.as<int32_t>());
+                    CHECK_LAUNCH();
+                    CU(cudaStreamSynchronize(ctx->stream));   // hub_of_s is a host vector
+                    hw = 2;
+                }
+            }
+        }
+        pl->hub_words = hw;
         Tmp u3(ctx), o3(ctx);
         CU(u3.alloc(sizeof(int32_t) * (k + 1)));
         CU(o3.alloc(sizeof(int32_t) * (k + 1)));
-        k_blob3_sizes<<<grid_for(k + 1), kThreads, 0, ctx->stream>>>(pl->peb, pl->pvb, pl->hb, k, W, u3.as<int32_t>());
+        k_blob3_sizes<<<grid_for(k + 1), kThreads, 0, ctx->stream>>>(pl->peb, pl->pvb, pl->hb, k, W, hw,
+                                                                    u3.as<int32_t>());
         if ((st = exclusive_scan(ctx, u3.as<int32_t>(), o3.as<int32_t>(), k + 1))) return st;
         int32_t t3 = 0;
         if ((st = read_i32(ctx, o3.as<int32_t>() + k, &t3))) return st;
@@ -401,37 +475,11 @@ epg_status build_pipeline_blob(epg_ctx *ctx, epg_plan *pl) {
             (st = plan_alloc_t(pl, ctx, &pl->desc3, k)))
             return st;
         k_build_blob3<<<(unsigned)k, 256, 0, ctx->stream>>>(pl->peb, pl->pvb, pl->hb, pl->halo_ids, pl->inc,
-                                                           pl->inc_off, o3.as<int32_t>(), W, pl->blob3, pl->desc3);
-        if (pl->S > 0) {
-            Tmp hm(ctx);
-            CU(hm.alloc(sizeof(int32_t)));
-            CU(cudaMemsetAsync(hm.p, 0, sizeof(int32_t), ctx->stream));
-            if ((st = plan_alloc_t(pl, ctx, &pl->fin_recs, 2 * pl->S))) return st;
-            k_finalise_records<<<grid_for(pl->S), kThreads, 0, ctx->stream>>>(
-                pl->shared_ids, pl->hv_off, pl->hv_list, (int32_t)pl->S, pl->fin_recs, hm.as<int32_t>());
-            int32_t hmax = 0;
-            if ((st = read_i32(ctx, hm.as<int32_t>(), &hmax))) return st;
-            if (hmax > 6) pl->fin_recs = nullptr;   // (the allocation is released with the plan)
-            if (hmax > kHeavyHalo) {                // hubs: list them for the block-per-vertex finalise
-                std::vector<int32_t> off(pl->S + 1), hv, md;
-                CU(cudaMemcpy(off.data(), pl->hv_off, sizeof(int32_t) * (pl->S + 1), cudaMemcpyDeviceToHost));
-                for (int64_t t = 0; t < pl->S; t++) {
-                    const int c = off[t + 1] - off[t];
-                    if (c > kBlockHalo) hv.push_back((int32_t)t);
-                    else if (c > kHeavyHalo) md.push_back((int32_t)t);
-                }
-                pl->n_heavy = (int64_t)hv.size();
-                pl->n_medium = (int64_t)md.size();
-                if ((st = plan_alloc_t(pl, ctx, &pl->heavy, pl->n_heavy)) ||
-                    (st = plan_alloc_t(pl, ctx, &pl->medium, pl->n_medium)))
-                    return st;
-                if (pl->n_heavy)
-                    CU(cudaMemcpy(pl->heavy, hv.data(), sizeof(int32_t) * pl->n_heavy, cudaMemcpyHostToDevice));
-                if (pl->n_medium)
-                    CU(cudaMemcpy(pl->medium, md.data(), sizeof(int32_t) * pl->n_medium, cudaMemcpyHostToDevice));
-            }
-        }
+                                                           pl->inc_off, o3.as<int32_t>(), W,
+                                                           hw == 2 ? hub_of_h.as<int32_t>() : nullptr, pl->blob3,
+                                                           pl->desc3);
         CHECK_LAUNCH();
+        CU(cudaStreamSynchronize(ctx->stream));
     }
     std::vector<int32_t> peb(k + 1), pvb(k + 1), hb(k + 1);
     CU(cudaMemcpyAsync(peb.data(), pl->peb, sizeof(int32_t) * (k + 1), cudaMemcpyDeviceToHost, ctx->stream));
@@ -449,7 +497,7 @@ epg_status build_pipeline_blob(epg_ctx *ctx, epg_plan *pl) {
         pl->part_rows[p] = nO + nH;
         pl->part_edges[p] = s;
         bmax = std::max(bmax, blob_bytes_for(nH, s, nO + nH, W));
-        pl->blob3_max = std::max(pl->blob3_max, blob3_bytes_for(nH, s, nO + nH, W));
+        pl->blob3_max = std::max(pl->blob3_max, blob3_bytes_for(nH, s, nO + nH, W, pl->hub_words));
         // measured on B200 (cfd, P = 1024): ~1.4 ns per edge, ~1.6 per staged row, ~1 per halo row
         pl->part_cost[p] = 1.4 * s + 1.6 * (nO + nH) + 1.0 * nH;
     }
@@ -657,7 +705,7 @@ epg_status launch_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t step
                 CU(launch_pdl(k_finalise3<Fn>, grid_for(fin_work), kThreads, 0, ctx->stream,
                               (const int32_t *)pl->shared_ids, (const int32_t *)pl->hv_off,
                               (const int32_t *)pl->hv_list, (const float *)pl->halo_buf, (const float *)a.state_in,
-                              a.state_out, a.vconst, (int32_t)pl->S, pl->touched, pl->n, (int32_t)kHeavyHalo));
+                              a.state_out, a.vconst, (int32_t)pl->S, pl->touched, pl->n, (int32_t)pl->finalise_skip));
             if (pl->n_medium > 0)
                 CU(launch_pdl(k_finalise_warp<Fn>, (unsigned)((pl->n_medium + 7) / 8), 256u, 0, ctx->stream,
                               (const int32_t *)pl->medium, pl->n_medium, (const int32_t *)pl->shared_ids,
@@ -668,6 +716,10 @@ epg_status launch_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t step
                               (const int32_t *)pl->heavy, (const int32_t *)pl->shared_ids,
                               (const int32_t *)pl->hv_off, (const int32_t *)pl->hv_list,
                               (const float *)pl->halo_buf, a.state_out, a.vconst));
+            if (pl->n_hub > 0)
+                CU(launch_pdl(k_finalise_hub<Fn>, grid_for(pl->n_hub), kThreads, 0, ctx->stream,
+                              (const int32_t *)pl->hub_sid, pl->n_hub, (const int32_t *)pl->shared_ids, pl->hub_acc,
+                              a.state_out, a.vconst));
             ctx->prof_end(1, t1);
         }
     }
@@ -696,6 +748,8 @@ epg_status run_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, 
     a.vconst = static_cast<const float *>(state->vertex_const);
     a.halo_buf = pl->halo_buf;
     a.first = 0;
+    a.hw = pl->hub_words;
+    a.hub_acc = pl->n_hub > 0 ? pl->hub_acc : nullptr;
     const bool v4 = pl->Lcap > 3 * kOccThreads;
     if (pl->Scap <= 2 * kOccThreads && pl->Lcap <= 2 * kOccThreads) {   // small execution partitions
         switch (pl->inc_width) {
@@ -734,6 +788,8 @@ epg_status run_edges_range(epg_ctx *ctx, epg_plan *pl, epg_state *state, int64_t
     a.vconst = static_cast<const float *>(state->vertex_const);
     a.halo_buf = pl->halo_buf;
     a.first = first;
+    a.hw = pl->hub_words;
+    a.hub_acc = nullptr;   // shard ranges sum every halo partial through hv_list
     if (count <= 0) return EPG_OK;
     auto go = [&](auto kern) -> epg_status {
         CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1394,6 +1450,20 @@ epg_status epg_set_variant(epg_ctx *ctx, int32_t variant) {
         return ctx->fail(EPG_ERR_INPUT, "set_variant: 0 auto, 1 per-partition, 2 pipelined, 3 occupancy");
     ctx->variant = variant;
     return EPG_OK;
+}
+
+epg_status epg_set_hub_split(epg_ctx *ctx, int32_t min_halo_entries) {
+    if (!ctx) return EPG_ERR_STATE;
+    if (min_halo_entries < -1)
+        return ctx->fail(EPG_ERR_INPUT, "set_hub_split: min_halo_entries must be >= 0 (0 = off) or -1 (default)");
+    ctx->hub_min = min_halo_entries;
+    return EPG_OK;
+}
+
+int64_t epg_plan_hubs(const epg_plan *plan, int32_t *min_halo_entries) {
+    if (!plan) return -1;
+    if (min_halo_entries) *min_halo_entries = plan->hub_min;
+    return plan->n_hub;
 }
 
 epg_status epg_set_profiling(epg_ctx *ctx, int32_t enable) {

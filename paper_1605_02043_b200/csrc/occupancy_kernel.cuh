@@ -27,14 +27,15 @@
 
 namespace epg {
 
-// blob of the occupancy kernel: [halo ids nH x i32] pad16 [incidence] (W as in the
-// pipelined blob: W x L u16 padded lists, or W = 0: 2s u16 entries + L u16 offsets)
-__host__ __device__ __forceinline__ int blob3_inc_offset(int nH) { return (4 * nH + 15) & ~15; }
+// blob of the occupancy kernel: [halo ids nH x i32] ([hub index nH x i32] when the plan has
+// hubs: hw = 2 words per halo row) pad16 [incidence] (W as in the pipelined blob: W x L u16
+// padded lists, or W = 0: 2s u16 entries + L u16 offsets)
+__host__ __device__ __forceinline__ int blob3_inc_offset(int nH, int hw = 1) { return (4 * hw * nH + 15) & ~15; }
 // padded incidence entries point at this Phi record, kept zero (>= every EPT x BLOCK)
 constexpr int kPhiSentinel = 1024;
-__host__ __device__ __forceinline__ int blob3_bytes_for(int nH, int s, int L, int W) {
+__host__ __device__ __forceinline__ int blob3_bytes_for(int nH, int s, int L, int W, int hw = 1) {
     const int inc = W > 0 ? 2 * W * L : 4 * s + 2 * L;
-    return (blob3_inc_offset(nH) + inc + 15) & ~15;
+    return (blob3_inc_offset(nH, hw) + inc + 15) & ~15;
 }
 
 struct OccArgs {
@@ -48,6 +49,8 @@ struct OccArgs {
     float *halo_buf;           // [C][ROW] in halo (partition) order
     int off_recs, rows_land, off_phi;
     int64_t first;             // this launch runs execution partitions first .. first + grid
+    int hw;                    // blob words per halo row (2: hub indices follow the halo ids)
+    float *hub_acc;            // [hubs][ROW] or NULL: hub partials are added here as well
 };
 
 template <class Fn, int BLOCK, int EPT, int VPT, int W>
@@ -147,7 +150,7 @@ __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
     __syncthreads();
     EPG_TP(0, 4);
     // reduce per local vertex into registers
-    const uint16_t *inc = reinterpret_cast<const uint16_t *>(sblob + blob3_inc_offset(d.nH));
+    const uint16_t *inc = reinterpret_cast<const uint16_t *>(sblob + blob3_inc_offset(d.nH, a.hw));
     float out[VPT][ROW];
 #pragma unroll
     for (int r = 0; r < VPT; r++) {
@@ -185,6 +188,13 @@ __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
         } else {
 #pragma unroll
             for (int c = 0; c < ROW; c++) out[r][c] = acc[c];
+            if (a.hub_acc) {   // hub split: this partition's partial of a hub, pre-summed above
+                const int hx = reinterpret_cast<const int32_t *>(sblob)[d.nH + (j - d.nO)];
+                if (hx >= 0) {
+#pragma unroll
+                    for (int c = 0; c < ROW; c++) atomicAdd(a.hub_acc + (int64_t)ROW * hx + c, acc[c]);
+                }
+            }
         }
     }
     __syncthreads();                               // records and Phi no longer read
@@ -444,6 +454,7 @@ __global__ void k_finalise_rec(const int4 *__restrict__ recs, const float *__res
         const int4 r0 = recs[2 * t], r1 = recs[2 * t + 1];
         const int64_t v = r0.x;
         const int c = r0.y;
+        if (c < 0) return;                         // a hub: k_finalise_hub's vertex
         const int h[6] = {r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
         float acc[Fn::ROW];
 #pragma unroll
@@ -463,12 +474,21 @@ __global__ void k_finalise_rec(const int4 *__restrict__ recs, const float *__res
     if (v < n) Fn::untouched(state_in + Fn::ROW * v, state_out + Fn::ROW * v);
 }
 
-// records for k_finalise_rec; *hmax receives the largest halo count
+// records for k_finalise_rec; *hmax receives the largest halo count of a non-hub vertex
+// (hubs: count >= hub_min > 0, recorded with count -1)
 __global__ void k_finalise_records(const int32_t *__restrict__ shared_ids, const int32_t *__restrict__ hv_off,
-                                   const int32_t *__restrict__ hv_list, int32_t S, int4 *recs, int32_t *hmax) {
+                                   const int32_t *__restrict__ hv_list, int32_t S, int32_t hub_min, int4 *recs,
+                                   int32_t *hmax) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= S) return;
-    const int q0 = hv_off[t], c = hv_off[t + 1] - q0;
+    const int q0 = hv_off[t];
+    int c = hv_off[t + 1] - q0;
+    if (hub_min > 0 && c >= hub_min) {
+        recs[2 * t] = make_int4(shared_ids[t], -1, 0, 0);
+        recs[2 * t + 1] = make_int4(0, 0, 0, 0);
+        atomicAdd(hmax + 1, 1);
+        return;
+    }
     int h[6];
     for (int i = 0; i < 6; i++) h[i] = i < c ? hv_list[q0 + i] : 0;
     recs[2 * t] = make_int4(shared_ids[t], c, h[0], h[1]);
@@ -476,18 +496,54 @@ __global__ void k_finalise_records(const int32_t *__restrict__ shared_ids, const
     atomicMax(hmax, c);
 }
 
+// Hub finalise (hub split): U'_v += dt * hub_acc[i] for hub i of
+// shared vertex hub_sid[i]; hub_acc is cleared for the next step. The hub's partials were
+// added by the edge kernel with one red.global.add per (execution partition, hub) after
+// the partition summed its edges in shared memory, so the sum order is not fixed.
+template <class Fn>
+__global__ void k_finalise_hub(const int32_t *__restrict__ hub_sid, int64_t nhub, const int32_t *__restrict__ shared_ids,
+                               float *__restrict__ hub_acc, float *__restrict__ state_out,
+                               const float *__restrict__ vconst) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    ptx::pdl_wait();
+    ptx::pdl_launch_dependents();
+    if (i >= nhub) return;
+    const int64_t v = shared_ids[hub_sid[i]];
+    float sum[Fn::ROW];
+#pragma unroll
+    for (int c = 0; c < Fn::ROW; c++) {
+        sum[c] = hub_acc[Fn::ROW * i + c];
+        hub_acc[Fn::ROW * i + c] = 0.0f;
+    }
+    Fn::finalise_add(state_out + Fn::ROW * v, sum, Fn::kUsesConst ? vconst[v] : 0.0f);
+}
+
+// hub_of_h[h] = hub index of halo entry h's vertex (entries of non-hubs keep -1)
+__global__ void k_hub_mark(const int32_t *__restrict__ hub_of_s, int32_t S, const int32_t *__restrict__ hv_off,
+                           const int32_t *__restrict__ hv_list, int32_t *__restrict__ hub_of_h) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= S) return;
+    const int32_t hx = hub_of_s[t];
+    if (hx < 0) return;
+    for (int q = hv_off[t]; q < hv_off[t + 1]; q++) hub_of_h[hv_list[q]] = hx;
+}
+
 // blob3 of partition p
 __global__ void k_build_blob3(const int32_t *__restrict__ peb, const int32_t *__restrict__ pvb,
                               const int32_t *__restrict__ hb, const int32_t *__restrict__ halo_ids,
                               const uint16_t *__restrict__ inc, const uint16_t *__restrict__ inc_off,
-                              const int32_t *__restrict__ blob16, int W, unsigned char *blob, PartDesc *desc) {
+                              const int32_t *__restrict__ blob16, int W, const int32_t *__restrict__ hub_of_h,
+                              unsigned char *blob, PartDesc *desc) {
     const int p = blockIdx.x;
     const int o0 = pvb[p], nO = pvb[p + 1] - o0, h0 = hb[p], nH = hb[p + 1] - h0, e0 = peb[p], s = peb[p + 1] - e0;
     const int L = nO + nH;
     unsigned char *b = blob + 16 * (int64_t)blob16[p];
     int32_t *hid = reinterpret_cast<int32_t *>(b);
-    uint16_t *ic = reinterpret_cast<uint16_t *>(b + blob3_inc_offset(nH));
+    const int hw = hub_of_h ? 2 : 1;
+    uint16_t *ic = reinterpret_cast<uint16_t *>(b + blob3_inc_offset(nH, hw));
     for (int j = threadIdx.x; j < nH; j += blockDim.x) hid[j] = halo_ids[h0 + j];
+    if (hub_of_h)
+        for (int j = threadIdx.x; j < nH; j += blockDim.x) hid[nH + j] = hub_of_h[h0 + j];
     const int64_t lbase = (int64_t)o0 + h0;
     if (W > 0) {
         for (int j = threadIdx.x; j < L; j += blockDim.x) {
@@ -500,16 +556,17 @@ __global__ void k_build_blob3(const int32_t *__restrict__ peb, const int32_t *__
         for (int q = threadIdx.x; q < 2 * s; q += blockDim.x) ic[q] = inc[2 * (int64_t)e0 + q];
         for (int j = threadIdx.x; j < L; j += blockDim.x) io[j] = inc_off[lbase + j];
     }
-    if (threadIdx.x == 0) desc[p] = PartDesc{o0, nO, e0, s, h0, nH, blob16[p], blob3_bytes_for(nH, s, L, W), 0, 0, 0, 0};
+    if (threadIdx.x == 0)
+        desc[p] = PartDesc{o0, nO, e0, s, h0, nH, blob16[p], blob3_bytes_for(nH, s, L, W, hw), 0, 0, 0, 0};
 }
 
 __global__ void k_blob3_sizes(const int32_t *__restrict__ peb, const int32_t *__restrict__ pvb,
-                              const int32_t *__restrict__ hb, int64_t k, int W, int32_t *units16) {
+                              const int32_t *__restrict__ hb, int64_t k, int W, int hw, int32_t *units16) {
     int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p > k) return;
     if (p == k) { units16[p] = 0; return; }
     const int nO = pvb[p + 1] - pvb[p], nH = hb[p + 1] - hb[p], s = peb[p + 1] - peb[p];
-    units16[p] = blob3_bytes_for(nH, s, nO + nH, W) / 16;
+    units16[p] = blob3_bytes_for(nH, s, nO + nH, W, hw) / 16;
 }
 
 // execution partitions: partition p of the EP map is cut into c_p contiguous edge ranges

@@ -29,7 +29,7 @@ SYMBOLS = ["epg_create", "epg_destroy", "epg_last_error", "epg_num_parts", "epg_
            "epg_default_partition", "epg_load_count", "epg_remap", "epg_plan_destroy", "epg_plan_info",
            "epg_permute_rows", "epg_run", "epg_run_naive", "epg_set_variant", "epg_set_profiling",
            "epg_profile_read", "epg_shard_ranges", "epg_shard_halos_host", "epg_run_edges", "epg_run_finalise",
-           "epg_shard_reduce", "epg_accumulate_rows", "epg_remapped_edges"]
+           "epg_shard_reduce", "epg_accumulate_rows", "epg_remapped_edges", "epg_set_hub_split", "epg_plan_hubs"]
 
 
 class _Report(C.Structure):
@@ -68,6 +68,8 @@ def _load():
         "epg_run": (st, [P, P, C.c_int, C.POINTER(_State), i32]),
         "epg_run_naive": (st, [P, C.c_int, P, i64, i32, C.POINTER(_State), i32]),
         "epg_set_variant": (st, [P, i32]),
+        "epg_set_hub_split": (st, [P, i32]),
+        "epg_plan_hubs": (i64, [P, P]),
         "epg_shard_ranges": (st, [P, i32, i32, P]),
         "epg_shard_halos_host": (st, [P, P, P, i64, i32, P, P, i64, P]),
         "epg_run_edges": (st, [P, P, C.c_int, C.POINTER(_State), i64, i64]),
@@ -181,6 +183,9 @@ class Plan:
         lib.epg_plan_info(handle, info.ctypes.data)
         (self.m, self.n, self.k, self.touched, self.cut_cost, self.shared,
          self.k_exec, self.cut_cost_exec) = (int(x) for x in info)
+        hm = C.c_int32(0)
+        self.hubs = int(lib.epg_plan_hubs(handle, C.byref(hm)))
+        self.hub_min = int(hm.value)
 
     def close(self):
         if self.handle:
@@ -315,6 +320,10 @@ class Context:
     def set_variant(self, variant: int):
         """0 auto, 1 one CTA per partition, 2 pipelined TMA kernel, 3 occupancy TMA kernel."""
         self._check(lib.epg_set_variant(self.handle, variant))
+
+    def set_hub_split(self, min_halo_entries: int):
+        """Hub split for plans remapped after this call (0 off; default 7, see include/epg.h)."""
+        self._check(lib.epg_set_hub_split(self.handle, min_halo_entries))
 
     def set_profiling(self, enable: bool):
         self._check(lib.epg_set_profiling(self.handle, 1 if enable else 0))
