@@ -59,12 +59,14 @@ class Workload:
             self.kernel, self.functor = 1, "cfd_flux"
             self.state, self.payload, self.vconst = S.cfd_state(M.n), M.normals, S.cfd_dt(M.volume)
             self.per_edge, self.per_vertex = 20, 44     # 8 B ids + 12 B normal; 20 B read, 4 B dt, 20 B write
+            self.exec_rows = 704                        # ~55 KB smem per cfd CTA: 4 per SM
         elif config == "c4":
             self.n, self.edges = S.rmat(24)
             self.m = self.edges.shape[0]
             self.kernel, self.functor = 2, "gather_scatter"
             self.state, self.payload, self.vconst = S.int_vector(1608, self.n, 0, 7), None, None
             self.per_edge, self.per_vertex = 8, 8       # 8 B ids; 4 B x read, 4 B y write
+            self.exec_rows = 1024                       # one-float rows (profiles/r01_c4_exec_sweep.txt)
         elif config == "c5":
             self.n, self.edges, w = S.stencil2d_spmv(3536)
             self.m = self.edges.shape[0]
@@ -73,6 +75,7 @@ class Workload:
             self.state = np.concatenate([S.int_vector(1609, N, -8, 8), np.zeros(N, np.float32)])
             self.payload, self.vconst = w, None
             self.per_edge, self.per_vertex = 12, 4      # 8 B ids + 4 B value; 4 B x or y per vertex
+            self.exec_rows = 1024
         else:
             raise ValueError(config)
         self.gen_s = time.perf_counter() - t0
@@ -412,6 +415,7 @@ def run_ours(args, rank, local_rank, world):
     M = Workload(args.config)
     t_gen = M.gen_s
     KER = M.kernel
+    ctx.set_exec_limits(M.exec_rows, 1024)
     E = torch.from_numpy(M.edges).to(dev)
     k = epg.num_parts(M.m, P)
     torch.cuda.synchronize()
@@ -594,6 +598,7 @@ def run_ours(args, rank, local_rank, world):
                       "replication": rep.replication, "redundant_fraction": rep.redundant_fraction,
                       "max_size": rep.max_size, "min_size": rep.min_size, "shared_vertices": plan.shared,
                       "hubs": plan.hubs, "hub_min_halo_entries": plan.hub_min, "k_exec": plan.k_exec,
+                      "exec_max_rows": M.exec_rows,
                       "host_partition_s": t_part, "remap_s": t_remap, "mesh_gen_s": t_gen},
         "comparators": comparators,
         "bytes_per_edge_ncu": variants,

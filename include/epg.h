@@ -157,6 +157,22 @@ int64_t epg_num_parts(int64_t m, int32_t part_size);
 epg_status epg_partition_host(const int32_t *edges, int64_t m, int32_t n_vertices, int32_t part_size,
                               int32_t shards, int32_t *part_of_edge, char *errbuf, int64_t errbuf_len);
 
+/* PowerGraph's edge partitioners, the quality baselines of SURVEY §8(f)
+ * rank 4, with the same k = ceil(m / part_size) clusters (host only, no device needed).
+ * epg_partition_random_host: "randomly assigns edges into partitions" with exact
+ *   balance (reading Z18): the edges ordered by (SplitMix64(seed, e), e) are
+ *   dealt round-robin, so cluster c gets floor(m/k) + [c < m mod k] edges.
+ * epg_partition_greedy_host: one pass in task order; each edge goes to the cluster that
+ *   "already possess[es] the endpoints": the highest [u in V_c] + [v in V_c]
+ *   among clusters holding fewer than ceil(m/k) edges, ties by fewer edges, then lower
+ *   id (with no holder open: "the partition with the fewest edges"; reading
+ *   Z19). Time grows with the number of clusters holding each endpoint (slow on hubs).
+ *   part_of_edge [m] HOST out. Status and errbuf as for epg_partition_host. */
+epg_status epg_partition_random_host(int64_t m, int32_t part_size, uint64_t seed, int32_t *part_of_edge,
+                                     char *errbuf, int64_t errbuf_len);
+epg_status epg_partition_greedy_host(const int32_t *edges, int64_t m, int32_t n_vertices, int32_t part_size,
+                                     int32_t *part_of_edge, char *errbuf, int64_t errbuf_len);
+
 /* epg_partition_host, then the GPU cost function on the result (epg_load_count).
  *   edges [m][2] host or device; part_of_edge [m] host or device out; out report. */
 epg_status epg_partition(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n_vertices, int32_t part_size,
@@ -266,6 +282,16 @@ epg_status epg_accumulate_rows(epg_ctx *ctx, const float *src, const int32_t *id
  * EPG_ERR_INFEASIBLE if the plan does not fit them. All compute the same result; they
  * differ in how partitions are staged and scheduled. */
 epg_status epg_set_variant(epg_ctx *ctx, int32_t variant);
+
+/* Execution-split caps for plans created by later epg_remap calls on ctx: an EP
+ * partition with more than max_rows staged rows (|V_p|) or max_edges edges is executed
+ * as contiguous ranges of its reorganised edges (the public layout is unchanged; see
+ * epg_plan_info's k_exec). max_rows in [64, 2048] (above 1024 only one-float functors,
+ * GATHER_SCATTER and SPMV, run the occupancy kernel), max_edges in [32, 1024]; -1 keeps
+ * the default: EPG_EXEC_MAX_ROWS / EPG_EXEC_MAX_EDGES from the environment, else 704
+ * rows (a cfd CTA at ~55 KB of shared memory, four per SM) and 1024 edges.
+ * EPG_ERR_INPUT outside these ranges. */
+epg_status epg_set_exec_limits(epg_ctx *ctx, int32_t max_rows, int32_t max_edges);
 
 /* Hub split (power-law graphs, the hub discussion of P:642-683):
  * plans created by later epg_remap calls on ctx treat every shared vertex with at least

@@ -53,6 +53,8 @@ def lib():
             "orc_cfd_step": (None, [P, i64, i32, P, P, P, P, P]),
             "orc_gather_scatter": (None, [P, i64, i32, P, P, P]),
             "orc_spmv": (None, [P, i64, i32, P, P, P]),
+            "orc_partition_random": (C.c_int, [i64, i32, C.c_uint64, P]),
+            "orc_partition_greedy": (C.c_int, [P, i64, i32, i32, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -237,3 +239,22 @@ def spmv(edges, n: int, w, x) -> np.ndarray:
     y = np.zeros(n, np.float64)
     lib().orc_spmv(_p(e), m, n, _p(np.ascontiguousarray(w, np.float32)), _p(np.ascontiguousarray(x, np.float32)), _p(y))
     return y
+
+
+def partition_random(m: int, P: int, seed: int = 1605) -> np.ndarray:
+    """PowerGraph random edge placement, exactly balanced (reading Z18)."""
+    part = np.empty(m, np.int32)
+    st = lib().orc_partition_random(m, P, seed & 0xFFFFFFFFFFFFFFFF, _p(part))
+    if st:
+        raise OracleError(st, "partition_random")
+    return part
+
+
+def partition_greedy(edges, n: int, P: int) -> np.ndarray:
+    """PowerGraph greedy edge placement (reading Z19)."""
+    e, m = _edges(edges)
+    part = np.empty(m, np.int32)
+    st = lib().orc_partition_greedy(_p(e), m, n, P, _p(part))
+    if st:
+        raise OracleError(st, "partition_greedy")
+    return part

@@ -508,3 +508,82 @@ void orc_spmv(const int32_t *edges, int64_t m, int32_t n, const float *w, const 
         y[i] += (double)w[e] * (double)x[j];
     }
 }
+
+/* ------------------------------------------------------------------------- */
+/* Baselines: PowerGraph's two edge partitioners, the quality     */
+/* comparators of SURVEY §8(f) rank 4. Both use k = ceil(m/P) clusters (O1).  */
+/* ------------------------------------------------------------------------- */
+
+/* Counter-based SplitMix64 (the generator synth/ draws inputs with; each side  */
+/* implements it, ③): output number c of stream `seed`.                        */
+static uint64_t orc_splitmix64(uint64_t seed, uint64_t c) {
+    uint64_t x = seed + (c + 1) * 0x9E3779B97F4A7C15ull;
+    uint64_t z = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+typedef struct { uint64_t key; int64_t e; } orc_keyed;
+static int cmp_keyed(const void *x, const void *y) {
+    const orc_keyed *a = (const orc_keyed *)x, *b = (const orc_keyed *)y;
+    if (a->key != b->key) return a->key < b->key ? -1 : 1;
+    return (a->e > b->e) - (a->e < b->e);
+}
+
+/* "The random based method randomly assigns edges into partitions", made  */
+/* exactly balanced (reading Z18): the edges, ordered by (SplitMix64(seed, e), e),  */
+/* are dealt round-robin -- the i-th of them goes to cluster i mod k, so cluster c   */
+/* receives floor(m/k) + [c < m mod k] edges, the sizes s_c of O1.                   */
+int orc_partition_random(int64_t m, int32_t P, uint64_t seed, int32_t *part) {
+    if (m <= 0) return ORC_ERR_INPUT;
+    if (P < 1 || P > ORC_MAX_PART) return ORC_ERR_INFEASIBLE;
+    const int64_t k = orc_num_parts(m, P);
+    orc_keyed *a = (orc_keyed *)malloc(sizeof(orc_keyed) * m);
+    for (int64_t e = 0; e < m; e++) { a[e].key = orc_splitmix64(seed, (uint64_t)e); a[e].e = e; }
+    qsort(a, m, sizeof(orc_keyed), cmp_keyed);
+    for (int64_t i = 0; i < m; i++) part[a[i].e] = (int32_t)(i % k);
+    free(a);
+    return ORC_OK;
+}
+
+/* "The greedy based method prioritizes choosing partitions that already possess   */
+/* the endpoints of the to-be-assigned edge. If no such partition is found, then the */
+/* partition with the fewest edges is selected to ensure balance".       */
+/* Reading Z19: one pass over the edges in task order; clusters     */
+/* holding cap = ceil(m/k) edges are full; score(c) = [u in V_c] + [v in V_c]; the   */
+/* edge goes to the non-full cluster with the highest score, ties by fewer edges,    */
+/* then the lower id (with every score 0 this is the cluster with the fewest edges). */
+/* Presence is a plain k x n bit matrix (ORC_ERR_INFEASIBLE above 2^33 bits).        */
+int orc_partition_greedy(const int32_t *edges, int64_t m, int32_t n, int32_t P, int32_t *part) {
+    if (m <= 0 || n <= 0) return ORC_ERR_INPUT;
+    if (orc_first_bad_edge(edges, m, n) >= 0) return ORC_ERR_INPUT;
+    if (P < 1 || P > ORC_MAX_PART) return ORC_ERR_INFEASIBLE;
+    const int64_t k = orc_num_parts(m, P);
+    const int64_t cap = (m + k - 1) / k;
+    if ((double)k * (double)n > 8589934592.0) return ORC_ERR_INFEASIBLE;
+    const int64_t words = ((int64_t)n + 63) / 64;
+    uint64_t *has = (uint64_t *)calloc((size_t)(k * words), sizeof(uint64_t));
+    int64_t *size = (int64_t *)calloc((size_t)k, sizeof(int64_t));
+    if (!has || !size) { free(has); free(size); return ORC_ERR_INFEASIBLE; }
+#define ORC_HAS(c, v) ((has[(c) * words + ((v) >> 6)] >> ((v) & 63)) & 1ull)
+    for (int64_t e = 0; e < m; e++) {
+        const int32_t u = edges[2 * e], v = edges[2 * e + 1];
+        int64_t best = -1, best_score = -1;
+        for (int64_t c = 0; c < k; c++) {
+            if (size[c] >= cap) continue;
+            const int64_t score = (int64_t)ORC_HAS(c, u) + (int64_t)ORC_HAS(c, v);
+            if (best < 0 || score > best_score || (score == best_score && size[c] < size[best])) {
+                best = c;
+                best_score = score;
+            }
+        }
+        part[e] = (int32_t)best;
+        size[best]++;
+        has[best * words + (u >> 6)] |= 1ull << (u & 63);
+        has[best * words + (v >> 6)] |= 1ull << (v & 63);
+    }
+#undef ORC_HAS
+    free(has);
+    free(size);
+    return ORC_OK;
+}

@@ -8,8 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libepg.so")
-SOURCES = ["api.cu", "partition.cpp"]
-DEPS = SOURCES + ["epg_internal.h", "functors.cuh", "layout_kernels.cuh", "run_kernels.cuh", "pipelined_kernel.cuh", "ptx.cuh"]
+SOURCES = ["api.cu", "partition.cpp", "baselines.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -24,7 +23,7 @@ def stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, d) for d in DEPS] + [os.path.join(HERE, "..", "include", "epg.h")]
+    deps = [os.path.join(CSRC, d) for d in os.listdir(CSRC)] + [os.path.join(HERE, "..", "include", "epg.h")]
     return any(os.path.getmtime(d) > t for d in deps)
 
 

@@ -26,6 +26,7 @@ struct epg_ctx {
     bool profiling = false;
     int variant = 0;  // 0 auto, 1 one CTA per partition, 2 pipelined TMA, 3 occupancy TMA
     int hub_min = -1; // hub split: shared vertices with >= hub_min halo entries (0 off, -1 default)
+    int exec_rows = -1, exec_edges = -1;   // execution-split caps for later remaps (-1 default)
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_used;
     cudaEvent_t take_event() {
@@ -641,30 +642,26 @@ epg_status run_pipelined(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t s
     }
 }
 
-// occupancy kernel limits: execution partitions of <= 1024 edges and <= 768 staged rows
-// (704 rows keep a cfd CTA at ~55 KB of shared memory: four CTAs per SM)
+// occupancy kernel limits: execution partitions of <= 1024 edges (EPT x BLOCK, the Phi
+// sentinel) and <= 1024 staged rows (VPT 4), 2048 for one-float rows (VPT 8)
 constexpr int kOccThreads = 256, kOccEPT = 4;
-// edge cap of an execution partition: 1024 (default) or 512 via EPG_EXEC_MAX_EDGES
-int exec_max_edges() {
-    static int v = [] {
-        const char *e = std::getenv("EPG_EXEC_MAX_EDGES");
-        int x = e ? std::atoi(e) : 1024;
-        return x <= 512 ? 512 : 1024;
-    }();
-    return v;
+constexpr int kOccMaxEdges = 1024, kOccMaxRows = 1024, kOccMaxRowsScalar = 2048;
+template <class Fn> constexpr int occ_max_rows() { return Fn::ROW == 1 ? kOccMaxRowsScalar : kOccMaxRows; }
+// execution-split caps of a remap: epg_set_exec_limits, else EPG_EXEC_MAX_EDGES /
+// EPG_EXEC_MAX_ROWS, else 1024 edges and 704 rows (704 rows keep a cfd CTA at ~55 KB of
+// shared memory: four CTAs per SM)
+int exec_max_edges(const epg_ctx *ctx) {
+    if (ctx->exec_edges > 0) return ctx->exec_edges;
+    const char *e = std::getenv("EPG_EXEC_MAX_EDGES");
+    const int x = e ? std::atoi(e) : kOccMaxEdges;
+    return std::min(kOccMaxEdges, std::max(32, x));
 }
-#define kExecMaxEdges exec_max_edges()
-// staged-row cap of an execution partition: 704 (default) keeps 4 CTAs/SM; up to 1024
-// (3 CTAs/SM, fewer split partitions) via EPG_EXEC_MAX_ROWS, read once
-int exec_max_rows() {
-    static int v = [] {
-        const char *e = std::getenv("EPG_EXEC_MAX_ROWS");
-        int x = e ? std::atoi(e) : 704;
-        return std::min(1024, std::max(64, x));
-    }();
-    return v;
+int exec_max_rows(const epg_ctx *ctx) {
+    if (ctx->exec_rows > 0) return ctx->exec_rows;
+    const char *e = std::getenv("EPG_EXEC_MAX_ROWS");
+    const int x = e ? std::atoi(e) : 704;
+    return std::min(kOccMaxRowsScalar, std::max(64, x));
 }
-#define kExecMaxRows exec_max_rows()
 
 // launch with programmatic stream serialization (the kernel calls griddepcontrol.wait
 // before touching what the previous kernel in the stream writes)
@@ -730,7 +727,7 @@ epg_status launch_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t step
 template <class Fn>
 epg_status run_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, bool *fits) {
     *fits = false;
-    if (pl->Scap > kExecMaxEdges || pl->Lcap > kExecMaxRows) return EPG_OK;
+    if (pl->Scap > kOccMaxEdges || pl->Lcap > occ_max_rows<Fn>()) return EPG_OK;
     int dev_max = 0;
     CU(cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
     OccArgs a{};
@@ -758,6 +755,15 @@ epg_status run_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, 
             default: return launch_occ<Fn, 0, 2, 2>(ctx, pl, state, steps, a, smem);
         }
     }
+    if constexpr (Fn::ROW == 1) {   // more than 1024 staged rows: 8 rows per thread
+        if (pl->Lcap > 4 * kOccThreads) {
+            switch (pl->inc_width) {
+                case 4: return launch_occ<Fn, 4, 8>(ctx, pl, state, steps, a, smem);
+                case 8: return launch_occ<Fn, 8, 8>(ctx, pl, state, steps, a, smem);
+                default: return launch_occ<Fn, 0, 8>(ctx, pl, state, steps, a, smem);
+            }
+        }
+    }
     switch (pl->inc_width) {
         case 4: return v4 ? launch_occ<Fn, 4, 4>(ctx, pl, state, steps, a, smem)
                           : launch_occ<Fn, 4, 3>(ctx, pl, state, steps, a, smem);
@@ -771,7 +777,7 @@ epg_status run_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, 
 // edge kernel over execution partitions [first, first + count) only (no finalise)
 template <class Fn>
 epg_status run_edges_range(epg_ctx *ctx, epg_plan *pl, epg_state *state, int64_t first, int64_t count) {
-    if (pl->Scap > kExecMaxEdges || pl->Lcap > kExecMaxRows)
+    if (pl->Scap > kOccMaxEdges || pl->Lcap > occ_max_rows<Fn>())
         return ctx->fail(EPG_ERR_INFEASIBLE, "run_edges: plan exceeds the occupancy kernel limits");
     OccArgs a{};
     a.off_recs = up16i(pl->blob3_max);
@@ -799,6 +805,15 @@ epg_status run_edges_range(epg_ctx *ctx, epg_plan *pl, epg_state *state, int64_t
         return EPG_OK;
     };
     const bool v4 = pl->Lcap > 3 * kOccThreads;
+    if constexpr (Fn::ROW == 1) {
+        if (pl->Lcap > 4 * kOccThreads) {
+            switch (pl->inc_width) {
+                case 4: return go(k_edge_occ<Fn, kOccThreads, kOccEPT, 8, 4>);
+                case 8: return go(k_edge_occ<Fn, kOccThreads, kOccEPT, 8, 8>);
+                default: return go(k_edge_occ<Fn, kOccThreads, kOccEPT, 8, 0>);
+            }
+        }
+    }
     switch (pl->inc_width) {
         case 4: return v4 ? go(k_edge_occ<Fn, kOccThreads, kOccEPT, 4, 4>) : go(k_edge_occ<Fn, kOccThreads, kOccEPT, 3, 4>);
         case 8: return v4 ? go(k_edge_occ<Fn, kOccThreads, kOccEPT, 4, 8>) : go(k_edge_occ<Fn, kOccThreads, kOccEPT, 3, 8>);
@@ -1179,6 +1194,7 @@ epg_status epg_remap(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, c
     epg_plan *ep = nullptr;
     epg_status st = remap_impl(ctx, edges, m, n, part, k, L, &ep);
     if (st) return st;
+    const int kExecMaxEdges = exec_max_edges(ctx), kExecMaxRows = exec_max_rows(ctx);
     std::vector<int32_t> cuts(k, 1);
     bool split = false;
     for (int64_t p = 0; p < k; p++) {
@@ -1449,6 +1465,16 @@ epg_status epg_set_variant(epg_ctx *ctx, int32_t variant) {
     if (variant < 0 || variant > 3)
         return ctx->fail(EPG_ERR_INPUT, "set_variant: 0 auto, 1 per-partition, 2 pipelined, 3 occupancy");
     ctx->variant = variant;
+    return EPG_OK;
+}
+
+epg_status epg_set_exec_limits(epg_ctx *ctx, int32_t max_rows, int32_t max_edges) {
+    if (!ctx) return EPG_ERR_STATE;
+    if (!(max_rows == -1 || (max_rows >= 64 && max_rows <= kOccMaxRowsScalar)) ||
+        !(max_edges == -1 || (max_edges >= 32 && max_edges <= kOccMaxEdges)))
+        return ctx->fail(EPG_ERR_INPUT, "set_exec_limits: max_rows in [64, 2048], max_edges in [32, 1024], or -1");
+    ctx->exec_rows = max_rows;
+    ctx->exec_edges = max_edges;
     return EPG_OK;
 }
 

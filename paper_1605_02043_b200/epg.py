@@ -29,7 +29,8 @@ SYMBOLS = ["epg_create", "epg_destroy", "epg_last_error", "epg_num_parts", "epg_
            "epg_default_partition", "epg_load_count", "epg_remap", "epg_plan_destroy", "epg_plan_info",
            "epg_permute_rows", "epg_run", "epg_run_naive", "epg_set_variant", "epg_set_profiling",
            "epg_profile_read", "epg_shard_ranges", "epg_shard_halos_host", "epg_run_edges", "epg_run_finalise",
-           "epg_shard_reduce", "epg_accumulate_rows", "epg_remapped_edges", "epg_set_hub_split", "epg_plan_hubs"]
+           "epg_shard_reduce", "epg_accumulate_rows", "epg_remapped_edges", "epg_set_hub_split", "epg_plan_hubs",
+           "epg_set_exec_limits", "epg_partition_random_host", "epg_partition_greedy_host"]
 
 
 class _Report(C.Structure):
@@ -69,6 +70,9 @@ def _load():
         "epg_run_naive": (st, [P, C.c_int, P, i64, i32, C.POINTER(_State), i32]),
         "epg_set_variant": (st, [P, i32]),
         "epg_set_hub_split": (st, [P, i32]),
+        "epg_set_exec_limits": (st, [P, i32, i32]),
+        "epg_partition_random_host": (st, [i64, i32, C.c_uint64, P, C.c_char_p, i64]),
+        "epg_partition_greedy_host": (st, [P, i64, i32, i32, P, C.c_char_p, i64]),
         "epg_plan_hubs": (i64, [P, P]),
         "epg_shard_ranges": (st, [P, i32, i32, P]),
         "epg_shard_halos_host": (st, [P, P, P, i64, i32, P, P, i64, P]),
@@ -159,6 +163,28 @@ def partition_host(edges, n: int, part_size: int, shards: int = 1) -> np.ndarray
     part = np.zeros(max(m, 1), np.int32)
     buf = C.create_string_buffer(512)
     s = lib.epg_partition_host(e.ctypes.data if m else None, m, n, part_size, shards, part.ctypes.data, buf, 512)
+    if s != OK:
+        raise EpgError(s, buf.value.decode())
+    return part[:m]
+
+
+def partition_random_host(m: int, part_size: int, seed: int = 1605) -> np.ndarray:
+    """PowerGraph random baseline (epg_partition_random_host)."""
+    part = np.zeros(max(m, 1), np.int32)
+    buf = C.create_string_buffer(512)
+    s = lib.epg_partition_random_host(m, part_size, seed & 0xFFFFFFFFFFFFFFFF, part.ctypes.data, buf, 512)
+    if s != OK:
+        raise EpgError(s, buf.value.decode())
+    return part[:m]
+
+
+def partition_greedy_host(edges, n: int, part_size: int) -> np.ndarray:
+    """PowerGraph greedy baseline (epg_partition_greedy_host)."""
+    e = np.ascontiguousarray(edges.cpu().numpy() if isinstance(edges, torch.Tensor) else edges, dtype=np.int32)
+    m = e.shape[0]
+    part = np.zeros(max(m, 1), np.int32)
+    buf = C.create_string_buffer(512)
+    s = lib.epg_partition_greedy_host(e.ctypes.data if m else None, m, n, part_size, part.ctypes.data, buf, 512)
     if s != OK:
         raise EpgError(s, buf.value.decode())
     return part[:m]
@@ -320,6 +346,10 @@ class Context:
     def set_variant(self, variant: int):
         """0 auto, 1 one CTA per partition, 2 pipelined TMA kernel, 3 occupancy TMA kernel."""
         self._check(lib.epg_set_variant(self.handle, variant))
+
+    def set_exec_limits(self, max_rows: int = -1, max_edges: int = -1):
+        """Execution-split caps for plans remapped after this call (-1 = default)."""
+        self._check(lib.epg_set_exec_limits(self.handle, max_rows, max_edges))
 
     def set_hub_split(self, min_halo_entries: int):
         """Hub split for plans remapped after this call (0 off; default 7, see include/epg.h)."""

@@ -96,3 +96,40 @@ def test_host_partition_rmat_bitexact():
     n, e = S.rmat(10)
     for P, G in ((64, 1), (256, 1), (128, 4)):
         assert np.array_equal(epg.partition_host(e, n, P, G), O.partition(e, n, P, G))
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_baselines_bitexact(seed):
+    """PowerGraph random / greedy baselines: library == oracle, bit for bit."""
+    from paper_1605_02043_b200 import epg
+    rng = np.random.default_rng(1200 + seed)
+    m = int(rng.integers(1, 4000))
+    nv = int(rng.integers(1, 800))
+    n, e = S.random_multigraph(seed, m, nv)
+    P = int(rng.integers(1, 200))
+    assert np.array_equal(epg.partition_random_host(m, P, seed * 7919), O.partition_random(m, P, seed * 7919))
+    assert np.array_equal(epg.partition_greedy_host(e, n, P), O.partition_greedy(e, n, P))
+
+
+def test_baselines_bitexact_mesh_and_rmat(mesh_c1):
+    from paper_1605_02043_b200 import epg
+    M = mesh_c1
+    for P in (256, 1024):
+        assert np.array_equal(epg.partition_greedy_host(M.edges, M.n, P), O.partition_greedy(M.edges, M.n, P))
+        assert np.array_equal(epg.partition_random_host(M.m, P, 1605), O.partition_random(M.m, P, 1605))
+    n, e = S.rmat(11)
+    assert np.array_equal(epg.partition_greedy_host(e, n, 128), O.partition_greedy(e, n, 128))
+
+
+def test_baselines_errors():
+    from paper_1605_02043_b200 import epg
+    with pytest.raises(epg.EpgError) as ex:
+        epg.partition_greedy_host(np.array([[0, 1], [1, 7]], np.int32), 3, 2)
+    assert ex.value.status == epg.ERR_INPUT and "edge 1" in ex.value.message
+    for bad in (0, 4097):
+        with pytest.raises(epg.EpgError) as ex:
+            epg.partition_random_host(10, bad)
+        assert ex.value.status == epg.ERR_INFEASIBLE
+    with pytest.raises(epg.EpgError) as ex:
+        epg.partition_random_host(0, 4)
+    assert ex.value.status == epg.ERR_INPUT

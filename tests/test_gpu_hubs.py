@@ -173,3 +173,57 @@ def test_set_hub_split_rejects_below_minus_one():
     with pytest.raises(epg.EpgError) as ex:
         c.set_hub_split(-2)
     assert ex.value.status == epg.ERR_INPUT
+
+
+@pytest.mark.parametrize("rows,edges", [(2048, 1024), (1536, 1024), (1024, 512), (128, 256), (64, 32)])
+def test_exec_limits_rmat_exact(rmat14, rows, edges):
+    """Execution-split caps (epg_set_exec_limits): wide caps run one-float rows with 8 rows
+    per thread, narrow caps cut EP partitions into many ranges; all bit-exact."""
+    from paper_1605_02043_b200 import epg
+    n, e, P, part = rmat14
+    x = S.int_vector(1613, n, 0, 7)
+    ctx = _ctx(-1)
+    ctx.set_exec_limits(rows, edges)
+    got, plan = _scalar(ctx, epg.KERNEL_GATHER_SCATTER, e, n, part, O.num_parts(len(e), P), x)
+    assert np.array_equal(got.astype(np.float64), O.gather_scatter(e, n, x))
+    assert plan.k_exec >= plan.k
+    if rows <= 128:
+        assert plan.k_exec > 2 * plan.k
+
+
+def test_exec_limits_wide_rows_cfd_falls_back(small_mesh):
+    """cfd rows above 1024 do not fit the occupancy kernel: variant 3 refuses, variant 0
+    runs another kernel, and the result still matches the oracle."""
+    from paper_1605_02043_b200 import epg
+    M = small_mesh
+    P = 4096
+    part = O.partition(M.edges, M.n, P)
+    k = O.num_parts(M.m, P)
+    U = S.cfd_state(M.n)
+    dt = S.cfd_dt(M.volume).astype(np.float32)
+    ref, _ = O.cfd_step(M.edges, M.n, M.normals, U, dt)
+    for variant in (3, 0):
+        ctx = _ctx(-1, variant)
+        ctx.set_exec_limits(2048, 1024)
+        L, plan = ctx.remap(dev(M.edges), M.n, dev(part), k)
+        Un = ctx.permute_rows(dev(U), L.vertex_perm, epg.PERM_SCATTER)
+        nrm = ctx.permute_rows(dev(M.normals), L.edge_perm, epg.PERM_GATHER)
+        dtn = ctx.permute_rows(dev(dt), L.vertex_perm, epg.PERM_SCATTER)
+        out = torch.empty_like(Un)
+        try:
+            ctx.run(plan, epg.KERNEL_CFD_FLUX, Un, out, nrm, dtn)
+        except epg.EpgError as ex:                # an execution partition has > 1024 rows
+            assert variant == 3 and ex.status == epg.ERR_INFEASIBLE
+            continue
+        got = ctx.permute_rows(out, L.vertex_perm, epg.PERM_GATHER).cpu().numpy()
+        assert normwise_err(got, ref).max() <= TOL
+
+
+def test_set_exec_limits_rejects_out_of_range():
+    from paper_1605_02043_b200 import epg
+    c = epg.Context(0)
+    for r, e in ((63, 1024), (4096, 1024), (704, 31), (704, 2048), (-2, 1024)):
+        with pytest.raises(epg.EpgError) as ex:
+            c.set_exec_limits(r, e)
+        assert ex.value.status == epg.ERR_INPUT
+    c.set_exec_limits(-1, -1)
