@@ -228,7 +228,8 @@ epg_status epg_remapped_edges(epg_ctx *ctx, const int32_t *edges, int64_t m, con
  * shared memory, evaluates the functor per edge from shared memory, reduces each
  * vertex's incident contributions in shared memory and writes interior vertices'
  * results directly; vertices shared by several partitions (p_v > 1) are completed
- * by a boundary-finalise pass. Deterministic: the summation order is fixed. */
+ * by a boundary-finalise pass. Deterministic: the summation order is fixed, except for
+ * hub vertices under the hub split (epg_set_hub_split; never on cfd meshes). */
 epg_status epg_run(epg_ctx *ctx, const epg_plan *plan, epg_kernel kernel, epg_state *state, int32_t steps);
 
 /* The default (unscheduled) comparator: the same functor with one thread per task
@@ -308,6 +309,61 @@ epg_status epg_set_hub_split(epg_ctx *ctx, int32_t min_halo_entries);
 /* Hub count of a plan (-1 for NULL); *min_halo_entries (may be NULL) receives the
  * threshold it was built with (0 = off). */
 int64_t epg_plan_hubs(const epg_plan *plan, int32_t *min_halo_entries);
+
+/* -- adaptive overhead control --------------------- */
+/* The paper's runtime policy around the transformed kernel, as a native executor:
+ *   - "data sharing optimization using a separate thread on the CPU while kernel is
+ *     executed on the GPU": create starts host EPG-1 (flat, part_size) on a
+ *     std::thread; until it finishes, steps run the original kernel (epg_run_naive:
+ *     original task order, global-memory operands), each timed with CUDA events;
+ *   - "check if the asynchronous optimization is completed before calling the kernel
+ *     and apply the optimization if so": before every step, a finished partition
+ *     is remapped (epg_load_count + epg_remap on the ctx stream) and the state moved to
+ *     the plan's layout. (If it finishes before any original step was timed, one original
+ *     step runs first so there is a runtime to compare with.);
+ *   - "record the transformed kernel runtime the first time it runs, and compare it with
+ *     the original kernel runtime. If the first run ... is slower, then we fall back to the
+ *     original kernel in the next iteration": the first EP step is timed and
+ *     kept iff ep_first_ms <= fallback_ratio * (median timed original step); otherwise
+ *     the state moves back and every later step runs the original kernel (1.0 = the
+ *     paper's rule);
+ *   - "If the optimization thread does not complete when the program finishes, we
+ *     terminate it": epg_adaptive_destroy cancels (polled once per partition)
+ *     and joins the thread.
+ * Every step advances one time step of the functor (state_out = F(state_in), the two
+ * state buffers alternating), whichever kernel runs it.
+ *   create: edges_host [m][2] HOST (copied); edge_payload (original task order),
+ *     vertex_const and state ([n][row] original vertex order) host or device, copied --
+ *     the executor owns its buffers. Payload / constants as for epg_run (cfd needs both,
+ *     SPMV the payload, GATHER_SCATTER optional weights). EPG_ERR_INPUT / INFEASIBLE as
+ *     for epg_partition_host; EPG_ERR_CUDA on allocation failures.
+ *   read_state: the current state in original vertex order into state_out (DEVICE,
+ *     [n][row]; asynchronous on the ctx stream).
+ *   wait: blocks until the partition thread has finished (the next step applies it).
+ *   info: phase (epg_adaptive_phase), step counts and the timings the policy used. */
+typedef struct epg_adaptive epg_adaptive;
+typedef enum {
+    EPG_ADAPTIVE_ORIGINAL = 0,     /* partition running; original kernel */
+    EPG_ADAPTIVE_EP = 1,           /* EP plan applied and kept */
+    EPG_ADAPTIVE_FELL_BACK = 2,    /* first EP step was slower; original kernel from then on */
+    EPG_ADAPTIVE_NO_PARTITION = 3  /* the partition failed; original kernel */
+} epg_adaptive_phase;
+typedef struct {
+    int32_t phase, partition_done;
+    int64_t steps_original, steps_ep;
+    double partition_seconds;      /* wall time of the host partition thread (0 while running) */
+    double original_ms;            /* median of the timed original steps */
+    double ep_first_ms;            /* the first EP step */
+} epg_adaptive_report;
+epg_status epg_adaptive_create(epg_ctx *ctx, epg_kernel kernel, const int32_t *edges_host, int64_t m,
+                               int32_t n_vertices, int32_t part_size, const void *edge_payload,
+                               const void *vertex_const, const void *state, double fallback_ratio,
+                               epg_adaptive **out);
+epg_status epg_adaptive_step(epg_adaptive *ad, int32_t steps);
+epg_status epg_adaptive_wait(epg_adaptive *ad);
+epg_status epg_adaptive_read_state(epg_adaptive *ad, void *state_out);
+epg_status epg_adaptive_info(const epg_adaptive *ad, epg_adaptive_report *out);
+void epg_adaptive_destroy(epg_adaptive *ad);
 
 /* -- measurement -------------------------------------------------------------- */
 /* Kernel timing for bench.py: while enabled, epg_run / epg_run_naive record a CUDA event

@@ -200,9 +200,12 @@ def shard_halos(edges, n: int, part, k: int, G: int, vertex_perm, part_vertex_be
     e, m = _edges(edges)
     begin = np.zeros(G * G + 1, np.int32)
     ids = np.zeros(2 * m, np.int32)
-    st = lib().orc_shard_halos(_p(e), m, n, _p(np.ascontiguousarray(part, np.int32)), k, G,
-                               _p(np.ascontiguousarray(vertex_perm, np.int32)),
-                               _p(np.ascontiguousarray(part_vertex_begin, np.int32)), _p(begin), _p(ids), 2 * m)
+    # converted inputs are bound to names: a temporary would be freed before the C call
+    part = np.ascontiguousarray(part, np.int32)
+    vertex_perm = np.ascontiguousarray(vertex_perm, np.int32)
+    part_vertex_begin = np.ascontiguousarray(part_vertex_begin, np.int32)
+    st = lib().orc_shard_halos(_p(e), m, n, _p(part), k, G, _p(vertex_perm), _p(part_vertex_begin), _p(begin),
+                               _p(ids), 2 * m)
     if st:
         raise OracleError(st, "orc_shard_halos")
     return begin, ids[: int(begin[-1])].copy()
@@ -211,8 +214,9 @@ def shard_halos(edges, n: int, part, k: int, G: int, vertex_perm, part_vertex_be
 def cfd_flux(edges, n: int, normals, U) -> np.ndarray:
     e, m = _edges(edges)
     F = np.zeros((n, 5), np.float64)
-    lib().orc_cfd_flux(_p(e), m, n, _p(np.ascontiguousarray(normals, np.float32)),
-                       _p(np.ascontiguousarray(U, np.float32)), _p(F))
+    normals = np.ascontiguousarray(normals, np.float32)
+    U = np.ascontiguousarray(U, np.float32)
+    lib().orc_cfd_flux(_p(e), m, n, _p(normals), _p(U), _p(F))
     return F
 
 
@@ -220,9 +224,10 @@ def cfd_step(edges, n: int, normals, U, dt):
     e, m = _edges(edges)
     Uout = np.zeros((n, 5), np.float64)
     F = np.zeros((n, 5), np.float64)
-    lib().orc_cfd_step(_p(e), m, n, _p(np.ascontiguousarray(normals, np.float32)),
-                       _p(np.ascontiguousarray(U, np.float32)), _p(np.ascontiguousarray(dt, np.float32)),
-                       _p(Uout), _p(F))
+    normals = np.ascontiguousarray(normals, np.float32)
+    U = np.ascontiguousarray(U, np.float32)
+    dt = np.ascontiguousarray(dt, np.float32)
+    lib().orc_cfd_step(_p(e), m, n, _p(normals), _p(U), _p(dt), _p(Uout), _p(F))
     return Uout, F
 
 
@@ -230,14 +235,17 @@ def gather_scatter(edges, n: int, x, w=None) -> np.ndarray:
     e, m = _edges(edges)
     y = np.zeros(n, np.float64)
     wa = None if w is None else np.ascontiguousarray(w, np.float32)
-    lib().orc_gather_scatter(_p(e), m, n, _p(wa), _p(np.ascontiguousarray(x, np.float32)), _p(y))
+    x = np.ascontiguousarray(x, np.float32)
+    lib().orc_gather_scatter(_p(e), m, n, _p(wa), _p(x), _p(y))
     return y
 
 
 def spmv(edges, n: int, w, x) -> np.ndarray:
     e, m = _edges(edges)
     y = np.zeros(n, np.float64)
-    lib().orc_spmv(_p(e), m, n, _p(np.ascontiguousarray(w, np.float32)), _p(np.ascontiguousarray(x, np.float32)), _p(y))
+    w = np.ascontiguousarray(w, np.float32)
+    x = np.ascontiguousarray(x, np.float32)
+    lib().orc_spmv(_p(e), m, n, _p(w), _p(x), _p(y))
     return y
 
 

@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libepg.so")
-SOURCES = ["api.cu", "partition.cpp", "baselines.cpp"]
+SOURCES = ["api.cu", "partition.cpp", "baselines.cpp", "adaptive.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

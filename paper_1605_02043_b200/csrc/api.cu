@@ -1179,6 +1179,12 @@ epg_status remap_impl(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, 
 }
 }  // namespace
 
+namespace epg {
+void *ctx_stream(epg_ctx *ctx) { return ctx->stream; }
+int ctx_device(epg_ctx *ctx) { return ctx->device; }
+epg_status ctx_fail(epg_ctx *ctx, epg_status s, const std::string &msg) { return ctx->fail(s, msg); }
+}  // namespace epg
+
 extern "C" {
 
 // Task reorganisation + cpack layout of the EP map (the public layout), then the

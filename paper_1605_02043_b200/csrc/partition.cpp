@@ -20,10 +20,7 @@
 #include "epg_internal.h"
 
 #include <algorithm>
-#ifdef EPG_PART_TIMING
-#include <chrono>
-#include <cstdio>
-#endif
+#include <atomic>
 #include <cstring>
 #include <queue>
 #include <string>
@@ -108,7 +105,8 @@ struct Frontier {
     }
 };
 
-void grow(const TaskGraph &T, const int64_t *sizes, int64_t nparts, int32_t *part) {
+// returns false if *cancel became non-zero (checked once per partition)
+bool grow(const TaskGraph &T, const int64_t *sizes, int64_t nparts, int32_t *part, const std::atomic<int> *cancel) {
     const int64_t ntask = T.ntask;
     std::vector<TaskState> st(ntask, TaskState{-1, kNoStamp, kNoStamp, 0});
     std::vector<int32_t> by_gst;
@@ -123,6 +121,7 @@ void grow(const TaskGraph &T, const int64_t *sizes, int64_t nparts, int32_t *par
         return lowest;
     };
     for (int64_t i = 0; i < nparts; i++) {
+        if (cancel && cancel->load(std::memory_order_relaxed)) return false;
         while (gnext < by_gst.size() && st[by_gst[gnext]].part != -1) gnext++;
         const int64_t seed = gnext < by_gst.size() ? by_gst[gnext] : next_unassigned();
         for (int32_t t : dirty) { st[t].lst = kNoStamp; st[t].gain = 0; }
@@ -158,12 +157,13 @@ void grow(const TaskGraph &T, const int64_t *sizes, int64_t nparts, int32_t *par
             }
         }
     }
+    return true;
 }
 
 }  // namespace
 
 epg_status host_partition(const int32_t *edges, int64_t m, int32_t n, int32_t part_size, int32_t shards,
-                          int32_t *part, std::string *err) {
+                          int32_t *part, std::string *err, const std::atomic<int> *cancel) {
     if (m <= 0 || n <= 0 || edges == nullptr || part == nullptr) {
         *err = "partition: need m > 0, n > 0 and non-NULL arrays";
         return EPG_ERR_INPUT;
@@ -190,28 +190,18 @@ epg_status host_partition(const int32_t *edges, int64_t m, int32_t n, int32_t pa
     }
     std::vector<int64_t> s(k);
     for (int64_t i = 0; i < k; i++) s[i] = m / k + (i < m % k ? 1 : 0);
-#ifdef EPG_PART_TIMING
-    auto c0 = std::chrono::steady_clock::now();
-#endif
+    auto cancelled = [&]() {
+        *err = "partition: cancelled";
+        return EPG_ERR_STATE;
+    };
     TaskGraph T = build_task_graph(edges, m, n);
-#ifdef EPG_PART_TIMING
-    auto c1 = std::chrono::steady_clock::now();
-#endif
-    if (shards == 1) {
-        grow(T, s.data(), k, part);
-#ifdef EPG_PART_TIMING
-        auto c2 = std::chrono::steady_clock::now();
-        fprintf(stderr, "T build %.3f s, grow %.3f s\n", std::chrono::duration<double>(c1 - c0).count(),
-                std::chrono::duration<double>(c2 - c1).count());
-#endif
-        return EPG_OK;
-    }
+    if (shards == 1) return grow(T, s.data(), k, part, cancel) ? EPG_OK : cancelled();
     // hierarchical: shard-level growing, then growing inside each shard
     std::vector<int64_t> ssize(shards, 0);
     for (int g = 0; g < shards; g++)
         for (int64_t i = g * k / shards; i < (g + 1) * k / shards; i++) ssize[g] += s[i];
     std::vector<int32_t> shard(m);
-    grow(T, ssize.data(), shards, shard.data());
+    if (!grow(T, ssize.data(), shards, shard.data(), cancel)) return cancelled();
     std::vector<std::vector<int32_t>> members(shards);
     for (int64_t t = 0; t < m; t++) members[shard[t]].push_back(static_cast<int32_t>(t));
     std::vector<int32_t> local(m);
@@ -234,7 +224,7 @@ epg_status host_partition(const int32_t *edges, int64_t m, int32_t n, int32_t pa
         }
         const int64_t p0 = g * k / shards, p1 = (g + 1) * k / shards;
         std::vector<int32_t> sub(mem.size());
-        grow(Tg, s.data() + p0, p1 - p0, sub.data());
+        if (!grow(Tg, s.data() + p0, p1 - p0, sub.data(), cancel)) return cancelled();
         for (size_t j = 0; j < mem.size(); j++) part[mem[j]] = static_cast<int32_t>(sub[j] + p0);
     }
     return EPG_OK;

@@ -30,7 +30,9 @@ SYMBOLS = ["epg_create", "epg_destroy", "epg_last_error", "epg_num_parts", "epg_
            "epg_permute_rows", "epg_run", "epg_run_naive", "epg_set_variant", "epg_set_profiling",
            "epg_profile_read", "epg_shard_ranges", "epg_shard_halos_host", "epg_run_edges", "epg_run_finalise",
            "epg_shard_reduce", "epg_accumulate_rows", "epg_remapped_edges", "epg_set_hub_split", "epg_plan_hubs",
-           "epg_set_exec_limits", "epg_partition_random_host", "epg_partition_greedy_host"]
+           "epg_set_exec_limits", "epg_partition_random_host", "epg_partition_greedy_host",
+           "epg_adaptive_create", "epg_adaptive_step", "epg_adaptive_wait", "epg_adaptive_read_state",
+           "epg_adaptive_info", "epg_adaptive_destroy"]
 
 
 class _Report(C.Structure):
@@ -41,6 +43,12 @@ class _Layout(C.Structure):
     _fields_ = [("edge_perm", C.c_void_p), ("part_edge_begin", C.c_void_p), ("vertex_perm", C.c_void_p),
                 ("part_vertex_begin", C.c_void_p), ("halo_begin", C.c_void_p), ("halo_ids", C.c_void_p),
                 ("halo_cap", C.c_int64), ("slots", C.c_void_p)]
+
+
+class _AdaptiveReport(C.Structure):
+    _fields_ = [("phase", C.c_int32), ("partition_done", C.c_int32), ("steps_original", C.c_int64),
+                ("steps_ep", C.c_int64), ("partition_seconds", C.c_double), ("original_ms", C.c_double),
+                ("ep_first_ms", C.c_double)]
 
 
 class _State(C.Structure):
@@ -73,6 +81,12 @@ def _load():
         "epg_set_exec_limits": (st, [P, i32, i32]),
         "epg_partition_random_host": (st, [i64, i32, C.c_uint64, P, C.c_char_p, i64]),
         "epg_partition_greedy_host": (st, [P, i64, i32, i32, P, C.c_char_p, i64]),
+        "epg_adaptive_create": (st, [P, C.c_int, P, i64, i32, i32, P, P, P, C.c_double, C.POINTER(P)]),
+        "epg_adaptive_step": (st, [P, i32]),
+        "epg_adaptive_wait": (st, [P]),
+        "epg_adaptive_read_state": (st, [P, P]),
+        "epg_adaptive_info": (st, [P, C.POINTER(_AdaptiveReport)]),
+        "epg_adaptive_destroy": (None, [P]),
         "epg_plan_hubs": (i64, [P, P]),
         "epg_shard_ranges": (st, [P, i32, i32, P]),
         "epg_shard_halos_host": (st, [P, P, P, i64, i32, P, P, i64, P]),
@@ -188,6 +202,57 @@ def partition_greedy_host(edges, n: int, part_size: int) -> np.ndarray:
     if s != OK:
         raise EpgError(s, buf.value.decode())
     return part[:m]
+
+
+ADAPTIVE_ORIGINAL, ADAPTIVE_EP, ADAPTIVE_FELL_BACK, ADAPTIVE_NO_PARTITION = 0, 1, 2, 3
+
+
+class Adaptive:
+    """epg_adaptive: the paper's adaptive overhead control -- original kernel
+    while host EPG-1 runs on a thread, EP plan applied when ready, kept iff its first
+    step is not slower (include/epg.h)."""
+
+    def __init__(self, ctx: "Context", kernel: int, edges, n: int, part_size: int, state: torch.Tensor,
+                 payload: torch.Tensor | None = None, vconst: torch.Tensor | None = None,
+                 fallback_ratio: float = 1.0):
+        self.ctx = ctx
+        self._edges = np.ascontiguousarray(edges.cpu().numpy() if isinstance(edges, torch.Tensor) else edges,
+                                           dtype=np.int32)
+        self.n = n
+        self.shape, self.dtype, self.device = state.shape, state.dtype, state.device
+        h = C.c_void_p()
+        ctx._check(lib.epg_adaptive_create(ctx.handle, kernel, self._edges.ctypes.data, self._edges.shape[0], n,
+                                           part_size, _ptr(payload), _ptr(vconst), _ptr(state), fallback_ratio,
+                                           C.byref(h)))
+        self.handle = h
+
+    def step(self, steps: int = 1):
+        self.ctx._check(lib.epg_adaptive_step(self.handle, steps))
+
+    def wait(self):
+        self.ctx._check(lib.epg_adaptive_wait(self.handle))
+
+    def read_state(self, out: torch.Tensor | None = None) -> torch.Tensor:
+        if out is None:
+            out = torch.empty(self.shape, dtype=self.dtype, device=self.device)
+        self.ctx._check(lib.epg_adaptive_read_state(self.handle, _ptr(out)))
+        return out
+
+    def info(self) -> dict:
+        r = _AdaptiveReport()
+        lib.epg_adaptive_info(self.handle, C.byref(r))
+        return {f: getattr(r, f) for f, _ in _AdaptiveReport._fields_}
+
+    def close(self):
+        if self.handle:
+            lib.epg_adaptive_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 @dataclass

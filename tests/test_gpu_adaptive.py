@@ -1,0 +1,129 @@
+"""Adaptive overhead control through epg_adaptive_*:
+original kernel while host EPG-1 runs on a thread, EP plan applied before the next step
+once it is ready, kept iff its first step is not slower, partition thread cancelled on
+destroy. Every step is the same functor time step, so results match the oracle whichever
+kernel ran them (bit-exact for integer-valued gather-scatter)."""
+import time
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import synth as S
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+def normwise_err(got, ref):
+    got = np.asarray(got, np.float64).reshape(ref.shape[0], -1)
+    ref = np.asarray(ref, np.float64).reshape(ref.shape[0], -1)
+    return (np.abs(got - ref).max(axis=0) / np.maximum(np.abs(ref).max(axis=0), 1e-300))
+
+
+def _gs_graph():
+    n, e = S.random_multigraph(31, 6000, 3000)
+    x = S.int_vector(32, n, 0, 1)
+    return n, e, x
+
+
+def _gs_ref(e, n, x, steps):
+    y = x.astype(np.float64)
+    for _ in range(steps):
+        y = O.gather_scatter(e, n, y.astype(np.float32))
+    assert np.abs(y).max() < 2 ** 24
+    return y
+
+
+@pytest.mark.parametrize("ratio,phase", [(1e9, 1), (0.0, 2)])
+def test_adaptive_switch_and_fallback_exact(ratio, phase):
+    from paper_1605_02043_b200 import epg
+    n, e, x = _gs_graph()
+    ctx = epg.Context(0)
+    ad = epg.Adaptive(ctx, epg.KERNEL_GATHER_SCATTER, e, n, 256, torch.from_numpy(x).cuda(), fallback_ratio=ratio)
+    ad.step(1)                                    # original kernel, timed
+    assert ad.info()["steps_original"] == 1
+    ad.wait()
+    assert ad.info()["partition_done"] == 1
+    ad.step(3)                                    # applies EP on the first of these
+    info = ad.info()
+    assert info["phase"] == phase
+    assert info["steps_original"] + info["steps_ep"] == 4
+    assert info["steps_ep"] == (3 if phase == 1 else 1)
+    assert info["original_ms"] > 0 and info["ep_first_ms"] > 0 and info["partition_seconds"] > 0
+    got = ad.read_state().cpu().numpy()
+    assert np.array_equal(got.astype(np.float64), _gs_ref(e, n, x, 4))
+    ad.close()
+
+
+def test_adaptive_partition_finished_before_first_step():
+    """If the partition is ready before any original step was timed, one original step
+    runs first (there must be an original runtime to compare with), then EP."""
+    from paper_1605_02043_b200 import epg
+    n, e, x = _gs_graph()
+    ctx = epg.Context(0)
+    ad = epg.Adaptive(ctx, epg.KERNEL_GATHER_SCATTER, e, n, 512, torch.from_numpy(x).cuda(), fallback_ratio=1e9)
+    ad.wait()
+    ad.step(3)
+    info = ad.info()
+    assert (info["phase"], info["steps_original"], info["steps_ep"]) == (1, 1, 2)
+    assert np.array_equal(ad.read_state().cpu().numpy().astype(np.float64), _gs_ref(e, n, x, 3))
+
+
+def test_adaptive_cfd_one_step_at_a_time(small_mesh):
+    """O8: each step within tolerance of the oracle applied to the previous fp32 state,
+    the first by the original kernel, the second by the EP plan."""
+    from paper_1605_02043_b200 import epg
+    M = small_mesh
+    U = S.cfd_state(M.n)
+    dt = S.cfd_dt(M.volume).astype(np.float32)
+    ctx = epg.Context(0)
+    ad = epg.Adaptive(ctx, epg.KERNEL_CFD_FLUX, M.edges, M.n, 512, torch.from_numpy(U).cuda(),
+                      torch.from_numpy(M.normals).cuda(), torch.from_numpy(dt).cuda(), fallback_ratio=1e9)
+    ad.step(1)
+    s1 = ad.read_state().cpu().numpy()
+    ref1, _ = O.cfd_step(M.edges, M.n, M.normals, U, dt)
+    assert normwise_err(s1, ref1).max() <= TOL
+    ad.wait()
+    ad.step(1)
+    assert ad.info()["phase"] == 1
+    s2 = ad.read_state().cpu().numpy()
+    ref2, _ = O.cfd_step(M.edges, M.n, M.normals, s1, dt)
+    assert normwise_err(s2, ref2).max() <= TOL
+    ad.step(2)                                    # EP steps keep matching
+    s4 = ad.read_state().cpu().numpy()
+    ad2 = epg.Adaptive(ctx, epg.KERNEL_CFD_FLUX, M.edges, M.n, 512, torch.from_numpy(s2).cuda(),
+                       torch.from_numpy(M.normals).cuda(), torch.from_numpy(dt).cuda(), fallback_ratio=0.0)
+    ad2.step(2)                                   # original kernel only (partition pending or fallen back)
+    assert normwise_err(s4, ad2.read_state().cpu().numpy().astype(np.float64)).max() <= TOL
+
+
+def test_adaptive_destroy_cancels_partition():
+    """an unfinished optimisation thread is terminated at the end."""
+    from paper_1605_02043_b200 import epg
+    n, e = S.rmat(18)
+    x = torch.from_numpy(S.int_vector(5, n, 0, 1)).cuda()
+    ctx = epg.Context(0)
+    ad = epg.Adaptive(ctx, epg.KERNEL_GATHER_SCATTER, e, n, 1024, x)
+    ad.step(1)
+    t0 = time.perf_counter()
+    ad.close()
+    assert time.perf_counter() - t0 < 10.0
+
+
+def test_adaptive_input_errors():
+    from paper_1605_02043_b200 import epg
+    ctx = epg.Context(0)
+    e = np.array([[0, 1], [1, 2]], np.int32)
+    x = torch.zeros(3, device="cuda")
+    with pytest.raises(epg.EpgError) as ex:       # cfd needs normals and dt
+        epg.Adaptive(ctx, epg.KERNEL_CFD_FLUX, e, 3, 4, torch.zeros((3, 5), device="cuda"))
+    assert ex.value.status == epg.ERR_INPUT
+    with pytest.raises(epg.EpgError) as ex:
+        epg.Adaptive(ctx, epg.KERNEL_GATHER_SCATTER, np.array([[0, 5]], np.int32), 3, 4, x)
+    assert ex.value.status == epg.ERR_INPUT and "edge 0" in ex.value.message
+    with pytest.raises(epg.EpgError) as ex:
+        epg.Adaptive(ctx, epg.KERNEL_GATHER_SCATTER, e, 3, 5000, x)
+    assert ex.value.status == epg.ERR_INFEASIBLE

@@ -103,3 +103,19 @@ def test_spmv_stencil():
     A = sp.coo_matrix((vals, (rows, cols)), shape=(N, N)).tocsr()
     assert np.array_equal(y[N:], A @ x[:N].astype(np.float64))
     assert np.all(y[:N] == 0)
+
+
+def test_wrappers_keep_converted_inputs_alive():
+    """Regression: inputs converted to float32 by the ctypes wrappers must outlive the C
+    call (a temporary's buffer was freed before it, and reads returned garbage once the
+    allocator reused it). float64 inputs must give the float32 results exactly."""
+    import synth as S
+    n, e = S.random_multigraph(3, 4000, 700)
+    x64 = S.int_vector(4, n, 0, 7).astype(np.float64)
+    ref = O.gather_scatter(e, n, x64.astype(np.float32))
+    for i in range(30):
+        junk = [np.full(n + 7 * i, 1e30, np.float32) for _ in range(4)]   # churn the allocator
+        assert np.array_equal(O.gather_scatter(e, n, x64), ref)
+        assert np.array_equal(O.spmv(e, n, np.ones(len(e)), x64), O.spmv(e, n, np.ones(len(e), np.float32),
+                                                                          x64.astype(np.float32)))
+        del junk
