@@ -106,6 +106,8 @@ def parse():
     ap.add_argument("--part-size", type=int, default=1024)
     ap.add_argument("--flush-mib", type=int, default=512)
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="bounded oracle sample for cpu_baseline")
+    ap.add_argument("--variant", type=int, default=0,
+                    help="staged-kernel variant (epg_set_variant): 0 auto, 3 occupancy + finalise, 4 persistent fused")
     ap.add_argument("--no-comparators", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-sharded", action="store_true",
@@ -416,6 +418,7 @@ def run_ours(args, rank, local_rank, world):
     t_gen = M.gen_s
     KER = M.kernel
     ctx.set_exec_limits(M.exec_rows, 1024)
+    ctx.set_variant(args.variant)
     E = torch.from_numpy(M.edges).to(dev)
     k = epg.num_parts(M.m, P)
     torch.cuda.synchronize()

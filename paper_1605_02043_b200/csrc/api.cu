@@ -1527,7 +1527,12 @@ epg_status epg_profile_read(epg_ctx *ctx, float *ms2, int64_t *launches2) {
 // development only (not in epg.h): copy the kernel trace buffer to the host
 epg_status epg_debug_trace(unsigned long long *host, int64_t count) {
     cudaMemcpyFromSymbol(host, epg::g_trace, sizeof(unsigned long long) * count);
-    cudaMemset(host ? nullptr : nullptr, 0, 0);
+    return EPG_OK;
+}
+epg_status epg_debug_trace_clear() {
+    void *p = nullptr;
+    cudaGetSymbolAddress(&p, epg::g_trace);
+    cudaMemset(p, 0, sizeof(epg::g_trace));
     return EPG_OK;
 }
 #endif

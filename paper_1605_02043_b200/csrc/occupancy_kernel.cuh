@@ -101,22 +101,25 @@ __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
         dtv[r] = (Fn::kUsesConst && j < d.nO) ? __ldg(a.vconst + d.o0 + j) : 0.0f;
     }
     ptx::pdl_wait();                               // state_in is final from here on
+    // every CTA of this grid has started: the finalise may launch and load its (static)
+    // records on SMs with room while the edge partitions run
+    ptx::pdl_launch_dependents();
     if (tid == 0) region_bulk(rows_base, g_rows, rows_bytes, &bar);
-    __syncthreads();                               // barrier initialisation visible
-    EPG_TP(0, 1);
-    ptx::mbar_wait(&bar, 0);
-    EPG_TP(0, 2);
-    // ragged ends of the owned range + halo rows
-    if (tid < 32) region_ragged(rows_base, g_rows, rows_bytes, tid);
-    {
-        const int32_t *hid = reinterpret_cast<const int32_t *>(sblob);
+    {   // halo rows H_p, gathered now so they fly with the bulk copies: the halo ids open the
+        // blob, so each thread reads its ids from global memory instead of waiting for the copy
+        const int32_t *hid = reinterpret_cast<const int32_t *>(a.blob + 16 * (int64_t)d.blob16);
         float *hr = rows + ROW * d.nO;
         for (int j = tid; j < d.nH; j += BLOCK) {      // one halo row per thread
-            const float *src = a.state_in + (int64_t)ROW * hid[j];
+            const float *src = a.state_in + (int64_t)ROW * __ldg(hid + j);
 #pragma unroll
             for (int c = 0; c < ROW; c++) ptx::cp_async4(hr + ROW * j + c, src + c);
         }
     }
+    __syncthreads();                               // barrier initialisation visible
+    EPG_TP(0, 1);
+    ptx::mbar_wait(&bar, 0);
+    EPG_TP(0, 2);
+    if (tid < 32) region_ragged(rows_base, g_rows, rows_bytes, tid);   // ragged ends of the owned range
     ptx::cp_async_commit();
     ptx::cp_async_wait<0>();
     __syncthreads();
@@ -248,7 +251,6 @@ __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
         ragged_store(ga, a_bytes, outA_base);
         ragged_store(gb, b_bytes, outB_base);
     }
-    ptx::pdl_launch_dependents();                  // the finalise may start launching
     EPG_TP(0, 5);
     if (tid == 0) ptx::bulk_wait_read0();          // shared memory must outlive the stores' reads
     EPG_TP(0, 6);
@@ -448,10 +450,18 @@ __global__ void k_finalise_rec(const int4 *__restrict__ recs, const float *__res
                                const float *__restrict__ state_in, float *__restrict__ state_out,
                                const float *__restrict__ vconst, int32_t S, int64_t touched, int64_t n) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    // the records and dt are plan / constant data: loaded before the wait, i.e. while the
+    // edge kernel still runs (it triggers this launch as soon as all of its CTAs started)
+    int4 r0 = make_int4(0, -1, 0, 0), r1 = make_int4(0, 0, 0, 0);
+    float dt = 0.0f;
+    if (t < S) {
+        r0 = recs[2 * t];
+        r1 = recs[2 * t + 1];
+        if (Fn::kUsesConst && r0.y >= 0) dt = vconst[r0.x];
+    }
     ptx::pdl_wait();
     ptx::pdl_launch_dependents();
     if (t < S) {
-        const int4 r0 = recs[2 * t], r1 = recs[2 * t + 1];
         const int64_t v = r0.x;
         const int c = r0.y;
         if (c < 0) return;                         // a hub: k_finalise_hub's vertex
@@ -466,7 +476,6 @@ __global__ void k_finalise_rec(const int4 *__restrict__ recs, const float *__res
                 for (int k = 0; k < Fn::ROW; k++) acc[k] += halo_buf[Fn::ROW * (int64_t)h[i] + k];
             }
         }
-        const float dt = Fn::kUsesConst ? vconst[v] : 0.0f;
         Fn::finalise_add(state_out + Fn::ROW * v, acc, dt);
         return;
     }
