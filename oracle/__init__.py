@@ -47,6 +47,8 @@ def lib():
             "orc_build_T": (C.c_int, [P, i64, i32, P, P, P, i64, P]),
             "orc_epg1": (C.c_int, [i64, P, P, P, P, i64, P]),
             "orc_partition": (C.c_int, [P, i64, i32, i32, i32, P]),
+            "orc_partition_method": (C.c_int, [P, i64, i32, i32, i32, i32, P]),
+            "orc_epg2": (C.c_int, [i64, P, i32, P, i64, P]),
             "orc_remap": (C.c_int, [P, i64, i32, P, i64, P, P, P, P, P, P, i64, P]),
             "orc_shard_halos": (C.c_int, [P, i64, i32, P, i64, i32, P, P, P, P, i64]),
             "orc_cfd_flux": (None, [P, i64, i32, P, P, P]),
@@ -162,10 +164,23 @@ def epg1(t_ptr, t_adj, t_w, sizes) -> np.ndarray:
     return part
 
 
-def partition(edges, n: int, P: int, shards: int = 1) -> np.ndarray:
+def epg2(edges, n: int, sizes) -> np.ndarray:
+    """EPG-2 (O5') with explicit cluster sizes."""
+    e, m = _edges(edges)
+    sizes = np.ascontiguousarray(sizes, dtype=np.int64)
+    part = np.zeros(max(m, 1), dtype=np.int32)
+    st = lib().orc_epg2(m, _p(e), n, _p(sizes), sizes.size, _p(part))
+    if st:
+        raise OracleError(st, "orc_epg2")
+    return part[:m]
+
+
+def partition(edges, n: int, P: int, shards: int = 1, method: int = 1) -> np.ndarray:
+    """method 1: EPG-1 on the contracted clone-and-connect graph T (O5); method 2: EPG-2,
+    growing on the EP objective of Eq. (1) directly (O5', reading Z20)."""
     e, m = _edges(edges)
     part = np.zeros(max(m, 1), dtype=np.int32)
-    st = lib().orc_partition(_p(e), m, n, P, shards, _p(part))
+    st = lib().orc_partition_method(_p(e), m, n, P, shards, method, _p(part))
     if st:
         raise OracleError(st, "orc_partition")
     return part[:m]

@@ -237,13 +237,132 @@ int orc_epg1(int64_t ntask, const int64_t *t_ptr, const int32_t *t_adj, const in
     return ORC_OK;
 }
 
+/* ------------------------------------------------------------------------- */
+/* O5'. EPG-2: balanced growing on the EP objective itself (SURVEY 8(f) rank */
+/* 2; reading Z20). Eq. (1) charges a partition one load per distinct vertex */
+/* it touches, so the task that adds the fewest new vertices is  */
+/* the one with the most distinct endpoints already in V_i. Same schedule as */
+/* EPG-1 (O5) with the gain redefined:                                       */
+/*  1. seed = unassigned task with the smallest global stamp gst if any has  */
+/*     one, else the smallest-id unassigned task;                            */
+/*  2. reset local state: V_i = {}, g = 0, lst = INF for all tasks, c = 0;   */
+/*     lst[seed] = c++;                                                      */
+/*  3. repeat s_i times:                                                     */
+/*     - if no unassigned task has finite lst, the smallest-id unassigned    */
+/*       task gets lst = c++;                                                */
+/*     - pick the unassigned task with finite lst maximising g (its distinct */
+/*       endpoints already in V_i), ties by the smallest lst; part[t] = i;   */
+/*     - for each distinct endpoint u of t (u_t, then v_t) not yet in V_i:   */
+/*       add u to V_i; for each unassigned task t' incident to u, ascending */
+/*       id, each once: if lst[t'] = INF then lst[t'] = c++; g[t'] += 1;     */
+/*       if gst[t'] = INF then gst[t'] = G++ (G never reset).                */
+/* The pick is a plain linear scan over the tasks stamped in this partition. */
+/* ------------------------------------------------------------------------- */
+int orc_epg2(int64_t ntask, const int32_t *edges, int32_t n, const int64_t *sizes, int64_t nparts,
+             int32_t *part) {
+    int64_t total = 0;
+    for (int64_t i = 0; i < nparts; i++) total += sizes[i];
+    if (total != ntask) return ORC_ERR_INPUT;
+    /* incidence: vertex -> its tasks, ascending, each task once (a self-loop once) */
+    int64_t *ip = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
+    for (int64_t t = 0; t < ntask; t++) {
+        ip[edges[2 * t] + 1]++;
+        if (edges[2 * t + 1] != edges[2 * t]) ip[edges[2 * t + 1] + 1]++;
+    }
+    for (int32_t v = 0; v < n; v++) ip[v + 1] += ip[v];
+    int64_t *fill = (int64_t *)malloc(sizeof(int64_t) * ((size_t)n + 1));
+    memcpy(fill, ip, sizeof(int64_t) * ((size_t)n + 1));
+    int64_t *inc = (int64_t *)malloc(sizeof(int64_t) * (ip[n] > 0 ? ip[n] : 1));
+    for (int64_t t = 0; t < ntask; t++) {     /* t ascending: lists come out ascending */
+        inc[fill[edges[2 * t]]++] = t;
+        if (edges[2 * t + 1] != edges[2 * t]) inc[fill[edges[2 * t + 1]]++] = t;
+    }
+    free(fill);
+    int64_t *gst = (int64_t *)malloc(sizeof(int64_t) * ntask);
+    int64_t *lst = (int64_t *)malloc(sizeof(int64_t) * ntask);
+    int64_t *g = (int64_t *)malloc(sizeof(int64_t) * ntask);
+    int64_t *gst_order = (int64_t *)malloc(sizeof(int64_t) * (ntask + 1));
+    int64_t *stamped = (int64_t *)malloc(sizeof(int64_t) * (ntask + 1));
+    char *in_v = (char *)calloc((size_t)n, 1);
+    int32_t *vin = (int32_t *)malloc(sizeof(int32_t) * ((size_t)n + 1));   /* vertices of V_i */
+    for (int64_t t = 0; t < ntask; t++) { part[t] = -1; gst[t] = INF64; lst[t] = INF64; g[t] = 0; }
+    int64_t G = 0, n_gst = 0, gptr = 0, idptr = 0, nst = 0, nvin = 0;
+
+    for (int64_t i = 0; i < nparts; i++) {
+        /* 1. seed */
+        while (gptr < n_gst && part[gst_order[gptr]] != -1) gptr++;
+        int64_t seed;
+        if (gptr < n_gst) seed = gst_order[gptr];
+        else {
+            while (idptr < ntask && part[idptr] != -1) idptr++;
+            seed = idptr;
+        }
+        /* 2. reset local state */
+        for (int64_t j = 0; j < nst; j++) { lst[stamped[j]] = INF64; g[stamped[j]] = 0; }
+        nst = 0;
+        for (int64_t j = 0; j < nvin; j++) in_v[vin[j]] = 0;
+        nvin = 0;
+        int64_t c = 0;
+        if (sizes[i] == 0) continue;
+        lst[seed] = c++; stamped[nst++] = seed;
+        /* 3. grow */
+        for (int64_t r = 0; r < sizes[i]; r++) {
+            int64_t best = -1;
+            for (int64_t j = 0; j < nst; j++) {
+                int64_t t = stamped[j];
+                if (part[t] != -1) continue;
+                if (best < 0 || g[t] > g[best] || (g[t] == g[best] && lst[t] < lst[best])) best = t;
+            }
+            if (best < 0) {
+                while (idptr < ntask && part[idptr] != -1) idptr++;
+                best = idptr;
+                lst[best] = c++; stamped[nst++] = best;
+            }
+            part[best] = (int32_t)i;
+            for (int side = 0; side < 2; side++) {
+                int32_t u = edges[2 * best + side];
+                if (side == 1 && u == edges[2 * best]) continue;   /* distinct endpoints */
+                if (in_v[u]) continue;
+                in_v[u] = 1; vin[nvin++] = u;
+                for (int64_t q = ip[u]; q < ip[u + 1]; q++) {
+                    int64_t nb = inc[q];
+                    if (part[nb] != -1) continue;
+                    if (lst[nb] == INF64) { lst[nb] = c++; stamped[nst++] = nb; }
+                    g[nb] += 1;
+                    if (gst[nb] == INF64) { gst[nb] = G++; gst_order[n_gst++] = nb; }
+                }
+            }
+        }
+    }
+    free(ip); free(inc); free(gst); free(lst); free(g); free(gst_order); free(stamped); free(in_v); free(vin);
+    return ORC_OK;
+}
+
 /* Flat (shards = 1) or hierarchical (shards = G > 1) EPG-1 (O5):
  *  shard g receives partitions [floor(gk/G), floor((g+1)k/G)) and target size the
  *  sum of their s_i; EPG-1 on T with those G sizes gives shard[t]; then, for g
  *  ascending, EPG-1 on T restricted to shard g (tasks renumbered by ascending id)
  *  with its slice of s_i, partition ids offset by floor(gk/G).                   */
+/* method 1 = EPG-1 on T (O5), method 2 = EPG-2 on the edge list (O5'). In         */
+/* hierarchical mode EPG-2's shard subproblem is the shard's tasks (renumbered by     */
+/* ascending id) with their original endpoints.                                       */
+static int grow_method(int method, int64_t ntask, const int64_t *tp, const int32_t *ta, const int32_t *tw,
+                       const int32_t *edges, int32_t n, const int64_t *sizes, int64_t nparts, int32_t *part) {
+    if (method == 2) return orc_epg2(ntask, edges, n, sizes, nparts, part);
+    return orc_epg1(ntask, tp, ta, tw, sizes, nparts, part);
+}
+
+int orc_partition_method(const int32_t *edges, int64_t m, int32_t n, int32_t P, int32_t shards, int32_t method,
+                         int32_t *part);
+
 int orc_partition(const int32_t *edges, int64_t m, int32_t n, int32_t P, int32_t shards, int32_t *part) {
+    return orc_partition_method(edges, m, n, P, shards, 1, part);
+}
+
+int orc_partition_method(const int32_t *edges, int64_t m, int32_t n, int32_t P, int32_t shards, int32_t method,
+                         int32_t *part) {
     if (m <= 0 || n <= 0) return ORC_ERR_INPUT;
+    if (method != 1 && method != 2) return ORC_ERR_INPUT;
     if (orc_first_bad_edge(edges, m, n) >= 0) return ORC_ERR_INPUT;
     if (P < 1 || P > ORC_MAX_PART) return ORC_ERR_INFEASIBLE;
     int64_t k = orc_num_parts(m, P);
@@ -259,14 +378,15 @@ int orc_partition(const int32_t *edges, int64_t m, int32_t n, int32_t P, int32_t
     orc_part_sizes(m, k, s);
 
     if (shards == 1) {
-        st = orc_epg1(m, t_ptr, t_adj, t_w, s, k, part);
+        st = grow_method(method, m, t_ptr, t_adj, t_w, edges, n, s, k, part);
     } else {
         int64_t Gs = shards;
         int64_t *ssize = (int64_t *)calloc(Gs, sizeof(int64_t));
         for (int64_t gi = 0; gi < Gs; gi++)
             for (int64_t i = gi * k / Gs; i < (gi + 1) * k / Gs; i++) ssize[gi] += s[i];
         int32_t *shard = (int32_t *)malloc(sizeof(int32_t) * m);
-        st = orc_epg1(m, t_ptr, t_adj, t_w, ssize, Gs, shard);
+        int32_t *sedges = (int32_t *)malloc(sizeof(int32_t) * 2 * m);    /* shard's edge list */
+        st = grow_method(method, m, t_ptr, t_adj, t_w, edges, n, ssize, Gs, shard);
         int64_t *loc = (int64_t *)malloc(sizeof(int64_t) * m);   /* task -> id inside its shard */
         int64_t *glob = (int64_t *)malloc(sizeof(int64_t) * m);  /* local id -> task           */
         int64_t *sp = (int64_t *)malloc(sizeof(int64_t) * (m + 1));
@@ -285,11 +405,12 @@ int orc_partition(const int32_t *edges, int64_t m, int32_t n, int32_t P, int32_t
                     if (shard[t_adj[q]] == gi) { sa[q2] = (int32_t)loc[t_adj[q]]; sw[q2] = t_w[q]; q2++; }
                 sp[j + 1] = q2;
             }
+            for (int64_t j = 0; j < mg; j++) { sedges[2 * j] = edges[2 * glob[j]]; sedges[2 * j + 1] = edges[2 * glob[j] + 1]; }
             int64_t p0 = gi * k / Gs, p1 = (gi + 1) * k / Gs;
-            st = orc_epg1(mg, sp, sa, sw, s + p0, p1 - p0, sub);
+            st = grow_method(method, mg, sp, sa, sw, sedges, n, s + p0, p1 - p0, sub);
             for (int64_t j = 0; j < mg; j++) part[glob[j]] = (int32_t)(sub[j] + p0);
         }
-        free(ssize); free(shard); free(loc); free(glob); free(sp); free(sa); free(sw); free(sub);
+        free(ssize); free(shard); free(sedges); free(loc); free(glob); free(sp); free(sa); free(sw); free(sub);
     }
     free(t_ptr); free(t_adj); free(t_w); free(s);
     return st;
