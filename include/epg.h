@@ -157,6 +157,19 @@ int64_t epg_num_parts(int64_t m, int32_t part_size);
 epg_status epg_partition_host(const int32_t *edges, int64_t m, int32_t n_vertices, int32_t part_size,
                               int32_t shards, int32_t *part_of_edge, char *errbuf, int64_t errbuf_len);
 
+/* Partitioner methods. EPG_PARTITION_EPG1 is epg_partition_host above. EPG_PARTITION_EPG2
+ * (reading Z20) keeps EPG-1's seed and stamp schedule but
+ * grows on Eq. (1)'s own objective: the gain of a frontier task is the number
+ * of its distinct endpoints already loaded by the growing partition, so each step adds
+ * the fewest new loads; the frontier grows through vertex incidence lists instead of T.
+ * Same sizes, hierarchy (shards) and determinism as EPG-1. */
+#define EPG_PARTITION_EPG1 1
+#define EPG_PARTITION_EPG2 2
+/* epg_partition_host with a method (EPG_ERR_INPUT for any other value). */
+epg_status epg_partition_host_method(const int32_t *edges, int64_t m, int32_t n_vertices, int32_t part_size,
+                                     int32_t shards, int32_t method, int32_t *part_of_edge, char *errbuf,
+                                     int64_t errbuf_len);
+
 /* PowerGraph's edge partitioners, the quality baselines of SURVEY §8(f)
  * rank 4, with the same k = ceil(m / part_size) clusters (host only, no device needed).
  * epg_partition_random_host: "randomly assigns edges into partitions" with exact
@@ -173,7 +186,11 @@ epg_status epg_partition_random_host(int64_t m, int32_t part_size, uint64_t seed
 epg_status epg_partition_greedy_host(const int32_t *edges, int64_t m, int32_t n_vertices, int32_t part_size,
                                      int32_t *part_of_edge, char *errbuf, int64_t errbuf_len);
 
-/* epg_partition_host, then the GPU cost function on the result (epg_load_count).
+/* Partitioner used by epg_partition and the adaptive executor on ctx (default EPG1);
+ * EPG_ERR_INPUT for an unknown method. */
+epg_status epg_set_partition_method(epg_ctx *ctx, int32_t method);
+
+/* epg_partition_host (with ctx's method), then the GPU cost function on the result (epg_load_count).
  *   edges [m][2] host or device; part_of_edge [m] host or device out; out report. */
 epg_status epg_partition(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n_vertices, int32_t part_size,
                          int32_t shards, int32_t *part_of_edge, epg_report *out);

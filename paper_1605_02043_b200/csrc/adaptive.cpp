@@ -289,10 +289,11 @@ epg_status epg_adaptive_create(epg_ctx *ctx, epg_kernel kernel, const int32_t *e
     if ((e = cudaStreamSynchronize(ad->stream))) return fail("adaptive_create", e);
     // the optimisation thread (host only; never touches the context or the device)
     ad->part_h.assign((size_t)m, 0);
-    ad->worker = std::thread([ad] {
+    const int32_t method = epg::ctx_partition_method(ctx);
+    ad->worker = std::thread([ad, method] {
         const auto t0 = std::chrono::steady_clock::now();
         ad->part_status = epg::host_partition(ad->edges_h.data(), ad->m, ad->n, ad->part_size, 1, ad->part_h.data(),
-                                              &ad->part_err, &ad->cancel);
+                                              &ad->part_err, &ad->cancel, method);
         ad->part_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         ad->done.store(1, std::memory_order_release);
     });

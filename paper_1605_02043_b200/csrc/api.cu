@@ -24,6 +24,7 @@ struct epg_ctx {
     size_t naive_F_bytes = 0;
     // profiling: event pairs around launches, per kernel class (0 edge, 1 finalise/update)
     bool profiling = false;
+    int partition_method = EPG_PARTITION_EPG1;
     int variant = 0;  // 0 auto, 1 one CTA per partition, 2 pipelined TMA, 3 occupancy TMA
     int hub_min = -1; // hub split: shared vertices with >= hub_min halo entries (0 off, -1 default)
     int exec_rows = -1, exec_edges = -1;   // execution-split caps for later remaps (-1 default)
@@ -988,7 +989,8 @@ epg_status epg_partition(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t 
         edges_h = eh.data();
     }
     std::string err;
-    epg_status st = epg::host_partition(edges_h, m, n, part_size, shards, ph.data(), &err);
+    epg_status st = epg::host_partition(edges_h, m, n, part_size, shards, ph.data(), &err, nullptr,
+                                        ctx->partition_method);
     if (st) return ctx->fail(st, err);
     Tmp ed(ctx), pd(ctx);
     const int32_t *edges_d = edges;
@@ -1181,6 +1183,7 @@ epg_status remap_impl(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, 
 
 namespace epg {
 void *ctx_stream(epg_ctx *ctx) { return ctx->stream; }
+int32_t ctx_partition_method(epg_ctx *ctx) { return ctx->partition_method; }
 int ctx_device(epg_ctx *ctx) { return ctx->device; }
 epg_status ctx_fail(epg_ctx *ctx, epg_status s, const std::string &msg) { return ctx->fail(s, msg); }
 }  // namespace epg
@@ -1471,6 +1474,14 @@ epg_status epg_set_variant(epg_ctx *ctx, int32_t variant) {
     if (variant < 0 || variant > 3)
         return ctx->fail(EPG_ERR_INPUT, "set_variant: 0 auto, 1 per-partition, 2 pipelined, 3 occupancy");
     ctx->variant = variant;
+    return EPG_OK;
+}
+
+epg_status epg_set_partition_method(epg_ctx *ctx, int32_t method) {
+    if (!ctx) return EPG_ERR_STATE;
+    if (method != EPG_PARTITION_EPG1 && method != EPG_PARTITION_EPG2)
+        return ctx->fail(EPG_ERR_INPUT, "set_partition_method: 1 (EPG-1) or 2 (EPG-2)");
+    ctx->partition_method = method;
     return EPG_OK;
 }
 

@@ -17,6 +17,11 @@
 //  tasks, always taking the frontier task with the largest gain g (weight into the
 //  partition), ties to the earliest local stamp; restart at the smallest unassigned
 //  id when the frontier empties.
+//
+//  EPG-2 (reading Z20): the same schedule, but the gain
+//  is Eq. (1)'s own objective -- a task's distinct endpoints already loaded by the
+//  partition (one load per distinct vertex), so the pick adds the fewest new
+//  loads. The frontier grows through the vertex incidence lists instead of T.
 #include "epg_internal.h"
 
 #include <algorithm>
@@ -160,10 +165,102 @@ bool grow(const TaskGraph &T, const int64_t *sizes, int64_t nparts, int32_t *par
     return true;
 }
 
+// ---- EPG-2 ----------------------------------------------------------------------
+// Vertex -> incident tasks (ascending, each task once: a self-loop appears once).
+struct Incidence {
+    std::vector<int64_t> beg;   // [n + 1]
+    std::vector<int32_t> task;
+};
+
+Incidence build_incidence(const int32_t *edges, int64_t m, int32_t n) {
+    Incidence I;
+    I.beg.assign(static_cast<size_t>(n) + 1, 0);
+    for (int64_t t = 0; t < m; t++) {
+        I.beg[edges[2 * t] + 1]++;
+        if (edges[2 * t + 1] != edges[2 * t]) I.beg[edges[2 * t + 1] + 1]++;
+    }
+    for (int32_t v = 0; v < n; v++) I.beg[v + 1] += I.beg[v];
+    std::vector<int64_t> at(I.beg.begin(), I.beg.end() - 1);
+    I.task.resize(static_cast<size_t>(I.beg[n]));
+    for (int64_t t = 0; t < m; t++) {   // ascending t: lists come out sorted
+        I.task[at[edges[2 * t]]++] = static_cast<int32_t>(t);
+        if (edges[2 * t + 1] != edges[2 * t]) I.task[at[edges[2 * t + 1]]++] = static_cast<int32_t>(t);
+    }
+    return I;
+}
+
+// EPG-2 growing: frontier heaps per gain 0..2 (distinct endpoints inside), lazy deletion
+// as for EPG-1; a vertex joins V_i the first time one of its tasks is taken (mark[v] = i
+// + 1, so the per-partition reset is free).
+bool grow_direct(const int32_t *edges, int64_t ntask, int32_t n, const int64_t *sizes, int64_t nparts, int32_t *part,
+                 const std::atomic<int> *cancel) {
+    const Incidence I = build_incidence(edges, ntask, n);
+    std::vector<TaskState> st(ntask, TaskState{-1, kNoStamp, kNoStamp, 0});
+    std::vector<int64_t> mark(static_cast<size_t>(n), 0);
+    std::vector<int32_t> by_gst;
+    by_gst.reserve(ntask);
+    std::vector<int32_t> dirty;
+    Frontier fr;
+    size_t gnext = 0;
+    int64_t lowest = 0;
+    int32_t gclock = 0;
+    auto next_unassigned = [&]() {
+        while (lowest < ntask && st[lowest].part != -1) lowest++;
+        return lowest;
+    };
+    for (int64_t i = 0; i < nparts; i++) {
+        if (cancel && cancel->load(std::memory_order_relaxed)) return false;
+        while (gnext < by_gst.size() && st[by_gst[gnext]].part != -1) gnext++;
+        const int64_t seed = gnext < by_gst.size() ? by_gst[gnext] : next_unassigned();
+        for (int32_t t : dirty) { st[t].lst = kNoStamp; st[t].gain = 0; }
+        dirty.clear();
+        fr.clear();
+        if (sizes[i] == 0) continue;
+        int32_t clock = 0;
+        st[seed].lst = clock++;
+        dirty.push_back(static_cast<int32_t>(seed));
+        fr.push(0, st[seed].lst, static_cast<int32_t>(seed));
+        for (int64_t r = 0; r < sizes[i]; r++) {
+            int32_t t = fr.pop(st);
+            if (t < 0) {  // frontier exhausted: restart on the remainder
+                t = static_cast<int32_t>(next_unassigned());
+                st[t].lst = clock++;
+                dirty.push_back(t);
+            }
+            st[t].part = static_cast<int32_t>(i);
+            part[t] = static_cast<int32_t>(i);
+            const int32_t ends[2] = {edges[2 * static_cast<int64_t>(t)], edges[2 * static_cast<int64_t>(t) + 1]};
+            for (int side = 0; side < 2; side++) {
+                const int32_t v = ends[side];
+                if (side == 1 && v == ends[0]) break;   // distinct endpoints only
+                if (mark[v] == i + 1) continue;         // already loaded by this partition
+                mark[v] = i + 1;
+                for (int64_t q = I.beg[v]; q < I.beg[v + 1]; q++) {
+                    const int32_t w = I.task[q];
+                    TaskState &u = st[w];
+                    if (u.part != -1) continue;
+                    if (u.lst == kNoStamp) {
+                        u.lst = clock++;
+                        dirty.push_back(w);
+                    }
+                    u.gain += 1;
+                    if (u.gst == kNoStamp) { u.gst = gclock++; by_gst.push_back(w); }
+                    fr.push(u.gain, u.lst, w);
+                }
+            }
+        }
+    }
+    return true;
+}
+
 }  // namespace
 
 epg_status host_partition(const int32_t *edges, int64_t m, int32_t n, int32_t part_size, int32_t shards,
-                          int32_t *part, std::string *err, const std::atomic<int> *cancel) {
+                          int32_t *part, std::string *err, const std::atomic<int> *cancel, int32_t method) {
+    if (method != EPG_PARTITION_EPG1 && method != EPG_PARTITION_EPG2) {
+        *err = "partition: method must be 1 (EPG-1) or 2 (EPG-2)";
+        return EPG_ERR_INPUT;
+    }
     if (m <= 0 || n <= 0 || edges == nullptr || part == nullptr) {
         *err = "partition: need m > 0, n > 0 and non-NULL arrays";
         return EPG_ERR_INPUT;
@@ -194,6 +291,31 @@ epg_status host_partition(const int32_t *edges, int64_t m, int32_t n, int32_t pa
         *err = "partition: cancelled";
         return EPG_ERR_STATE;
     };
+    if (method == EPG_PARTITION_EPG2) {
+        if (shards == 1) return grow_direct(edges, m, n, s.data(), k, part, cancel) ? EPG_OK : cancelled();
+        // hierarchical: shard-level growing, then growing on each shard's own edge list
+        std::vector<int64_t> ssize(shards, 0);
+        for (int g = 0; g < shards; g++)
+            for (int64_t i = g * k / shards; i < (g + 1) * k / shards; i++) ssize[g] += s[i];
+        std::vector<int32_t> shard(m);
+        if (!grow_direct(edges, m, n, ssize.data(), shards, shard.data(), cancel)) return cancelled();
+        for (int g = 0; g < shards; g++) {
+            std::vector<int32_t> mem, sub_edges;
+            for (int64_t t = 0; t < m; t++)
+                if (shard[t] == g) {
+                    mem.push_back(static_cast<int32_t>(t));
+                    sub_edges.push_back(edges[2 * t]);
+                    sub_edges.push_back(edges[2 * t + 1]);
+                }
+            const int64_t p0 = g * k / shards, p1 = (g + 1) * k / shards;
+            std::vector<int32_t> sub(mem.size());
+            if (!grow_direct(sub_edges.data(), static_cast<int64_t>(mem.size()), n, s.data() + p0, p1 - p0, sub.data(),
+                             cancel))
+                return cancelled();
+            for (size_t j = 0; j < mem.size(); j++) part[mem[j]] = static_cast<int32_t>(sub[j] + p0);
+        }
+        return EPG_OK;
+    }
     TaskGraph T = build_task_graph(edges, m, n);
     if (shards == 1) return grow(T, s.data(), k, part, cancel) ? EPG_OK : cancelled();
     // hierarchical: shard-level growing, then growing inside each shard
@@ -234,8 +356,15 @@ epg_status host_partition(const int32_t *edges, int64_t m, int32_t n, int32_t pa
 
 extern "C" epg_status epg_partition_host(const int32_t *edges, int64_t m, int32_t n_vertices, int32_t part_size,
                                          int32_t shards, int32_t *part_of_edge, char *errbuf, int64_t errbuf_len) {
+    return epg_partition_host_method(edges, m, n_vertices, part_size, shards, EPG_PARTITION_EPG1, part_of_edge, errbuf,
+                                     errbuf_len);
+}
+
+extern "C" epg_status epg_partition_host_method(const int32_t *edges, int64_t m, int32_t n_vertices, int32_t part_size,
+                                                int32_t shards, int32_t method, int32_t *part_of_edge, char *errbuf,
+                                                int64_t errbuf_len) {
     std::string err;
-    epg_status st = epg::host_partition(edges, m, n_vertices, part_size, shards, part_of_edge, &err);
+    epg_status st = epg::host_partition(edges, m, n_vertices, part_size, shards, part_of_edge, &err, nullptr, method);
     if (st != EPG_OK && errbuf && errbuf_len > 0) {
         std::strncpy(errbuf, err.c_str(), static_cast<size_t>(errbuf_len - 1));
         errbuf[errbuf_len - 1] = '\0';

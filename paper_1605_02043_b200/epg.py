@@ -19,6 +19,7 @@ LIB_PATH = os.environ.get("EPG_LIB_PATH", os.path.join(_HERE, "libepg.so"))
 
 OK, ERR_INPUT, ERR_INFEASIBLE, ERR_CUDA, ERR_NCCL, ERR_NOMEM, ERR_STATE = 0, 2, 3, 4, 5, 6, 7
 KERNEL_CFD_FLUX, KERNEL_GATHER_SCATTER, KERNEL_SPMV = 1, 2, 3
+PARTITION_EPG1, PARTITION_EPG2 = 1, 2
 KERNELS = {"cfd": KERNEL_CFD_FLUX, "gather_scatter": KERNEL_GATHER_SCATTER, "spmv": KERNEL_SPMV}
 ROW = {KERNEL_CFD_FLUX: 5, KERNEL_GATHER_SCATTER: 1, KERNEL_SPMV: 1}
 MAX_PART_SIZE = 4096
@@ -32,7 +33,7 @@ SYMBOLS = ["epg_create", "epg_destroy", "epg_last_error", "epg_num_parts", "epg_
            "epg_shard_reduce", "epg_accumulate_rows", "epg_remapped_edges", "epg_set_hub_split", "epg_plan_hubs",
            "epg_set_exec_limits", "epg_partition_random_host", "epg_partition_greedy_host",
            "epg_adaptive_create", "epg_adaptive_step", "epg_adaptive_wait", "epg_adaptive_read_state",
-           "epg_adaptive_info", "epg_adaptive_destroy"]
+           "epg_adaptive_info", "epg_adaptive_destroy", "epg_partition_host_method", "epg_set_partition_method"]
 
 
 class _Report(C.Structure):
@@ -67,6 +68,8 @@ def _load():
         "epg_last_error": (C.c_char_p, [P]),
         "epg_num_parts": (i64, [i64, i32]),
         "epg_partition_host": (st, [P, i64, i32, i32, i32, P, C.c_char_p, i64]),
+        "epg_partition_host_method": (st, [P, i64, i32, i32, i32, i32, P, C.c_char_p, i64]),
+        "epg_set_partition_method": (st, [P, i32]),
         "epg_partition": (st, [P, P, i64, i32, i32, i32, P, C.POINTER(_Report)]),
         "epg_default_partition": (st, [P, i64, i32, P]),
         "epg_load_count": (st, [P, P, i64, i32, P, i64, P, C.POINTER(_Report)]),
@@ -170,13 +173,14 @@ def shard_halos_host(part_vertex_begin, halo_begin, halo_ids, k: int, G: int):
     return begin, ids[: int(cnt[0])]
 
 
-def partition_host(edges, n: int, part_size: int, shards: int = 1) -> np.ndarray:
-    """Host EPG-1 (epg_partition_host); edges int32 [m][2] numpy or CPU tensor."""
+def partition_host(edges, n: int, part_size: int, shards: int = 1, method: int = PARTITION_EPG1) -> np.ndarray:
+    """Host EPG-1 / EPG-2 (epg_partition_host_method); edges int32 [m][2] numpy or CPU tensor."""
     e = np.ascontiguousarray(edges.cpu().numpy() if isinstance(edges, torch.Tensor) else edges, dtype=np.int32)
     m = e.shape[0]
     part = np.zeros(max(m, 1), np.int32)
     buf = C.create_string_buffer(512)
-    s = lib.epg_partition_host(e.ctypes.data if m else None, m, n, part_size, shards, part.ctypes.data, buf, 512)
+    s = lib.epg_partition_host_method(e.ctypes.data if m else None, m, n, part_size, shards, method,
+                                      part.ctypes.data, buf, 512)
     if s != OK:
         raise EpgError(s, buf.value.decode())
     return part[:m]
@@ -411,6 +415,10 @@ class Context:
     def set_variant(self, variant: int):
         """0 auto, 1 one CTA per partition, 2 pipelined TMA kernel, 3 occupancy TMA kernel."""
         self._check(lib.epg_set_variant(self.handle, variant))
+
+    def set_partition_method(self, method: int):
+        """Partitioner of epg_partition / the adaptive executor (PARTITION_EPG1 or _EPG2)."""
+        self._check(lib.epg_set_partition_method(self.handle, method))
 
     def set_exec_limits(self, max_rows: int = -1, max_edges: int = -1):
         """Execution-split caps for plans remapped after this call (-1 = default)."""

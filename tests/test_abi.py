@@ -133,3 +133,49 @@ def test_baselines_errors():
     with pytest.raises(epg.EpgError) as ex:
         epg.partition_random_host(0, 4)
     assert ex.value.status == epg.ERR_INPUT
+
+
+# ---------------------------------------------------------------- EPG-2 (O5', reading Z20)
+def test_host_epg2_fixtures():
+    from paper_1605_02043_b200 import epg
+    g = golden("fig_mot.json")
+    e = np.array(g["topologies"]["star_plus_triangle"], np.int32)
+    assert epg.partition_host(e, 6, 3, method=epg.PARTITION_EPG2).tolist() == g["schedule_b"]
+    g2 = golden("two_triangle.json")
+    e2 = np.array(g2["edges"], np.int32)
+    assert epg.partition_host(e2, 6, 3, method=epg.PARTITION_EPG2).tolist() == g2["optimal_partition"]
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_host_epg2_random_bitexact(seed):
+    """Self-loops, parallel edges, isolated vertices, every shard count."""
+    from paper_1605_02043_b200 import epg
+    rng = np.random.default_rng(1900 + seed)
+    m = int(rng.integers(1, 3000))
+    n = int(rng.integers(1, 1500))
+    n, e = S.random_multigraph(300 + seed, m, n)
+    P = int(rng.integers(1, 300))
+    k = O.num_parts(m, P)
+    for G in (1, 2, 4, 8):
+        if G > k:
+            continue
+        assert np.array_equal(epg.partition_host(e, n, P, G, method=epg.PARTITION_EPG2),
+                              O.partition(e, n, P, G, method=2))
+
+
+@pytest.mark.parametrize("P", [256, 1024])
+def test_host_epg2_mesh_and_rmat_bitexact(mesh_c1, P):
+    from paper_1605_02043_b200 import epg
+    M = mesh_c1
+    assert np.array_equal(epg.partition_host(M.edges, M.n, P, method=epg.PARTITION_EPG2),
+                          O.partition(M.edges, M.n, P, method=2))
+    n, e = S.rmat(10)
+    assert np.array_equal(epg.partition_host(e, n, P // 4, 2, method=epg.PARTITION_EPG2),
+                          O.partition(e, n, P // 4, 2, method=2))
+
+
+def test_host_partition_method_errors():
+    from paper_1605_02043_b200 import epg
+    with pytest.raises(epg.EpgError) as ex:
+        epg.partition_host(np.array([[0, 1]], np.int32), 2, 1, method=3)
+    assert ex.value.status == epg.ERR_INPUT
