@@ -11,10 +11,10 @@ finalise) on resident inputs. Partitioning (a2), the cost kernel (a3) and the re
 application loop -- and are timed separately ("setup").
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config c1|c2|c3] [--part-size P]
+                    [--config c1|c2|c3|c4|c5] [--part-size P] [--partitioner epg1|epg2] [--variant V]
 
 N > 1 (torchrun): weak scaling of the sharded path. The mesh has N times the
-C2 cell count (a Kuhn box truncated to N x 232,536 cells); hierarchical EPG-1 with shards = N
+C2 cell count (a Kuhn box truncated to N x 232,536 cells); hierarchical EPG-2 (or EPG-1) with shards = N
 gives each GPU a contiguous range of partitions; every step pulls the halo rows owned by
 lower shards and pushes per-vertex partial sums back to their owners with grouped NCCL
 send/recv (paper_1605_02043_b200/shard.py), so each GPU keeps a C2-sized share of the work.
@@ -108,11 +108,17 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="bounded oracle sample for cpu_baseline")
     ap.add_argument("--variant", type=int, default=0,
                     help="staged-kernel variant (epg_set_variant): 0 auto, 3 occupancy + finalise, 4 persistent fused")
+    ap.add_argument("--partitioner", choices=["epg1", "epg2"], default="epg2",
+                    help="EP partitioner: epg1 (growing on the clone-and-connect graph T) or epg2 (growing on "
+                         "Eq. (1)'s objective, SURVEY 8(f) rank 2); the other one runs as a comparator")
     ap.add_argument("--no-comparators", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the multi-GPU (sharded, halo-exchange) step even at N = 1")
     return ap.parse_args()
+
+
+PARTITIONERS = {"epg1": 1, "epg2": 2}
 
 
 def dist_env():
@@ -299,7 +305,8 @@ def run_sharded(args, rank, local_rank, world):
     E = torch.from_numpy(M.edges).to(dev)
     k = epg.num_parts(M.m, P)
     t0 = time.perf_counter()
-    part, rep = ctx.partition(E, M.n, P, shards=world)        # hierarchical EPG-1, identical on all ranks
+    ctx.set_partition_method(PARTITIONERS[args.partitioner])
+    part, rep = ctx.partition(E, M.n, P, shards=world)        # hierarchical EPG, identical on all ranks
     t_part = time.perf_counter() - t0
     L, plan = ctx.remap(E, M.n, part, k, halo_cap=rep.cut_cost)
     sh = Shard(ctx, plan, L, epg.KERNEL_CFD_FLUX, world, rank)
@@ -371,7 +378,7 @@ def run_sharded(args, rank, local_rank, world):
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{args.config.upper()}-sized cfd Kuhn mesh per GPU: {M.n:,} cells, {M.m:,} "
                                    f"interior faces in total", "part_size": P, "k": k, "functor": "cfd_flux",
-                       "schedule": f"hierarchical EPG-1, shards = {world}",
+                       "schedule": f"hierarchical {args.partitioner.upper()}, shards = {world}",
                        "step": "halo pull (NCCL) + epg_run_edges + partial push (NCCL) + epg_run_finalise",
                        "l2": f"flushed between timed steps ({args.flush_mib} MiB write)",
                        "parallelism": f"graph shards x{world}, NCCL p2p halo exchange"},
@@ -423,7 +430,8 @@ def run_ours(args, rank, local_rank, world):
     k = epg.num_parts(M.m, P)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    part, rep = ctx.partition(E, M.n, P)                      # host EPG-1 + GPU cost kernel
+    ctx.set_partition_method(PARTITIONERS[args.partitioner])
+    part, rep = ctx.partition(E, M.n, P)                      # host EPG + GPU cost kernel
     t_part = time.perf_counter() - t0
     t0 = time.perf_counter()
     L, plan = ctx.remap(E, M.n, part, k, halo_cap=rep.cut_cost)
@@ -535,7 +543,9 @@ def run_ours(args, rank, local_rank, world):
         # whose hubs make its per-edge candidate scan quadratic)
         runs = [("default_staged", def_step, drep), ("naive_original_order", naive_step, None),
                 ("ep_hardware_cache", hwcache_step, None)]
-        baselines = [("powergraph_random", lambda: epg.partition_random_host(M.m, P, 1605))]
+        other = "epg1" if args.partitioner == "epg2" else "epg2"
+        baselines = [(f"ep_{other}", lambda: epg.partition_host(M.edges, M.n, P, method=PARTITIONERS[other])),
+                     ("powergraph_random", lambda: epg.partition_random_host(M.m, P, 1605))]
         if KER != epg.KERNEL_GATHER_SCATTER:
             baselines.append(("powergraph_greedy", lambda: epg.partition_greedy_host(M.edges, M.n, P)))
         base_keep = []
@@ -613,7 +623,7 @@ def run_ours(args, rank, local_rank, world):
         "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOADS[args.config], "part_size": P, "k": k, "k_exec": plan.k_exec,
                    "functor": M.functor,
-                   "schedule": "EP (host EPG-1) + cpack remap", "step": "epg_run(steps=1): staged edge kernel + boundary finalise",
+                   "schedule": f"EP (host {args.partitioner.upper()}) + cpack remap", "step": "epg_run(steps=1): staged edge kernel + boundary finalise",
                    "l2": f"flushed between timed steps ({args.flush_mib} MiB write)",
                    "parallelism": "replicas" if world > 1 else "single"},
         "roofline": roofline,

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
 #include <queue>
 #include <climits>
 #include <cstdlib>
@@ -104,6 +105,7 @@ struct epg_plan {
     unsigned long long *bar_ctr = nullptr;        // grid barrier counter (monotone)
     unsigned long long bar_gen = 0;               // launches so far
     int32_t *cta_begin = nullptr, *cta_list = nullptr;
+    std::map<const void *, int64_t> resident_ctas;   // per edge-kernel instance: SMs x occupancy
     std::vector<void *> allocs;
     ~epg_plan() {
         for (void *p : allocs) cudaFree(p);
@@ -685,6 +687,16 @@ template <class Fn, int W, int VPT, int EPT = kOccEPT>
 epg_status launch_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, OccArgs a, size_t smem) {
     auto kern = k_edge_occ<Fn, kOccThreads, EPT, VPT, W>;
     CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    {   // early PDL trigger only when the whole grid is resident at once (one wave)
+        auto it = pl->resident_ctas.find(reinterpret_cast<const void *>(kern));
+        if (it == pl->resident_ctas.end()) {
+            int occ = 0, sms = 0;
+            CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kOccThreads, smem));
+            CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+            it = pl->resident_ctas.emplace(reinterpret_cast<const void *>(kern), (int64_t)occ * sms).first;
+        }
+        a.early_pdl = pl->k <= it->second ? 1 : 0;
+    }
     float *bufs[2] = {static_cast<float *>(state->state_in), static_cast<float *>(state->state_out)};
     const int64_t fin_work = pl->S + (pl->n - pl->touched);
     for (int32_t s = 0; s < steps; s++) {

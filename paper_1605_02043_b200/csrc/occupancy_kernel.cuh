@@ -51,6 +51,7 @@ struct OccArgs {
     int64_t first;             // this launch runs execution partitions first .. first + grid
     int hw;                    // blob words per halo row (2: hub indices follow the halo ids)
     float *hub_acc;            // [hubs][ROW] or NULL: hub partials are added here as well
+    int early_pdl;             // 1: trigger dependents at the start (single-wave grids)
 };
 
 template <class Fn, int BLOCK, int EPT, int VPT, int W>
@@ -101,25 +102,41 @@ __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
         dtv[r] = (Fn::kUsesConst && j < d.nO) ? __ldg(a.vconst + d.o0 + j) : 0.0f;
     }
     ptx::pdl_wait();                               // state_in is final from here on
-    // every CTA of this grid has started: the finalise may launch and load its (static)
-    // records on SMs with room while the edge partitions run
-    ptx::pdl_launch_dependents();
+    // single-wave grids: every CTA of this grid is resident, so the finalise may launch now
+    // and load its (static) records on SMs with room while the edge partitions run
+    if (a.early_pdl) ptx::pdl_launch_dependents();
     if (tid == 0) region_bulk(rows_base, g_rows, rows_bytes, &bar);
-    {   // halo rows H_p, gathered now so they fly with the bulk copies: the halo ids open the
-        // blob, so each thread reads its ids from global memory instead of waiting for the copy
-        const int32_t *hid = reinterpret_cast<const int32_t *>(a.blob + 16 * (int64_t)d.blob16);
+    // halo rows H_p. With few halos (nH <= nO, the EP maps) they are gathered now so they fly
+    // with the bulk copies -- the halo ids open the blob, so each thread reads its ids from
+    // global memory instead of waiting for the copy. Halo-heavy partitions (the default
+    // map) gather after the copies instead: their halo rows are mostly other partitions'
+    // owned rows that those CTAs' bulk copies are bringing into L2 at the same time.
+    const bool early_halo = d.nH <= d.nO;
+    auto gather_halo = [&](const int32_t *hid, bool global_ids) {
         float *hr = rows + ROW * d.nO;
-        for (int j = tid; j < d.nH; j += BLOCK) {      // one halo row per thread
-            const float *src = a.state_in + (int64_t)ROW * __ldg(hid + j);
+        int32_t h[VPT];                                 // all ids first: one round trip, not VPT
 #pragma unroll
-            for (int c = 0; c < ROW; c++) ptx::cp_async4(hr + ROW * j + c, src + c);
+        for (int r = 0; r < VPT; r++) {
+            const int j = tid + r * BLOCK;
+            h[r] = j < d.nH ? (global_ids ? __ldg(hid + j) : hid[j]) : 0;
         }
-    }
+#pragma unroll
+        for (int r = 0; r < VPT; r++) {                 // one halo row per thread and r
+            const int j = tid + r * BLOCK;
+            if (j < d.nH) {
+                const float *src = a.state_in + (int64_t)ROW * h[r];
+#pragma unroll
+                for (int c = 0; c < ROW; c++) ptx::cp_async4(hr + ROW * j + c, src + c);
+            }
+        }
+    };
+    if (early_halo) gather_halo(reinterpret_cast<const int32_t *>(a.blob + 16 * (int64_t)d.blob16), true);
     __syncthreads();                               // barrier initialisation visible
     EPG_TP(0, 1);
     ptx::mbar_wait(&bar, 0);
     EPG_TP(0, 2);
     if (tid < 32) region_ragged(rows_base, g_rows, rows_bytes, tid);   // ragged ends of the owned range
+    if (!early_halo) gather_halo(reinterpret_cast<const int32_t *>(sblob), false);
     ptx::cp_async_commit();
     ptx::cp_async_wait<0>();
     __syncthreads();
@@ -251,6 +268,7 @@ __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
         ragged_store(ga, a_bytes, outA_base);
         ragged_store(gb, b_bytes, outB_base);
     }
+    if (!a.early_pdl) ptx::pdl_launch_dependents();   // the finalise may start launching
     EPG_TP(0, 5);
     if (tid == 0) ptx::bulk_wait_read0();          // shared memory must outlive the stores' reads
     EPG_TP(0, 6);
