@@ -2,8 +2,9 @@
 
     ncu --metrics <...> -k regex:'k_edge|k_finalise|k_naive' python tools/ncu_variants.py --config c2
 
-Variants, in launch order: EP staged (k_edge_staged + k_finalise), default-map staged
-(same kernels), naive original order (k_naive_edges + k_naive_update). `--reps R`
+Variants, in launch order: EP staged with the EPG-2 map ("ep"; edge kernel + finalise),
+EP staged with the EPG-1 map ("ep1"), default-map staged (same kernels), naive original
+order (k_naive_edges + k_naive_update). `--reps R`
 repeats the sequence (ncu -s can skip the first). Prints the per-variant kernel order.
 """
 from __future__ import annotations
@@ -25,7 +26,7 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--part-size", type=int, default=1024)
     ap.add_argument("--reps", type=int, default=2)
-    ap.add_argument("--variants", default="ep,default,naive")
+    ap.add_argument("--variants", default="ep,ep1,default,naive")
     a = ap.parse_args()
     M = S.config_mesh(a.config)
     U, dt = S.cfd_state(M.n), S.cfd_dt(M.volume)
@@ -35,8 +36,12 @@ def main():
     Ud = torch.from_numpy(U).cuda()
     runs = []
     for v in a.variants.split(","):
-        if v in ("ep", "default"):
-            part = ctx.partition(E, M.n, a.part_size)[0] if v == "ep" else ctx.default_partition(M.m, a.part_size)
+        if v in ("ep", "ep1", "default"):
+            if v == "default":
+                part = ctx.default_partition(M.m, a.part_size)
+            else:
+                ctx.set_partition_method(epg.PARTITION_EPG2 if v == "ep" else epg.PARTITION_EPG1)
+                part = ctx.partition(E, M.n, a.part_size)[0]
             L, plan = ctx.remap(E, M.n, part, k)
             nrm = ctx.permute_rows(torch.from_numpy(M.normals).cuda(), L.edge_perm, epg.PERM_GATHER)
             dtn = ctx.permute_rows(torch.from_numpy(dt).cuda(), L.vertex_perm, epg.PERM_SCATTER)
