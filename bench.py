@@ -111,6 +111,8 @@ def parse():
     ap.add_argument("--partitioner", choices=["epg1", "epg2"], default="epg2",
                     help="EP partitioner: epg1 (growing on the clone-and-connect graph T) or epg2 (growing on "
                          "Eq. (1)'s objective, SURVEY 8(f) rank 2); the other one runs as a comparator")
+    ap.add_argument("--exec-rows", type=int, default=0,
+                    help="execution-split row cap (epg_set_exec_limits; 0 = the config's default)")
     ap.add_argument("--no-comparators", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-sharded", action="store_true",
@@ -424,6 +426,8 @@ def run_ours(args, rank, local_rank, world):
     M = Workload(args.config)
     t_gen = M.gen_s
     KER = M.kernel
+    if args.exec_rows:
+        M.exec_rows = args.exec_rows
     ctx.set_exec_limits(M.exec_rows, 1024)
     ctx.set_variant(args.variant)
     E = torch.from_numpy(M.edges).to(dev)
