@@ -12,16 +12,17 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("G", [2, 4, 8])
-@pytest.mark.parametrize("P", [1024, 2048])
-def test_virtual_shards_cfd(mesh_c1, G, P):
+@pytest.mark.parametrize("P,method", [(1024, 1), (2048, 1), (1024, 2)])
+def test_virtual_shards_cfd(mesh_c1, G, P, method):
     from paper_1605_02043_b200 import epg
     from paper_1605_02043_b200.shard import Shard, run_virtual, assemble_owned
     M = mesh_c1
     k = O.num_parts(M.m, P)
     ctx = epg.Context(0)
+    ctx.set_partition_method(method)
     E = torch.from_numpy(M.edges).cuda()
     part, _ = ctx.partition(E, M.n, P, shards=G)
-    assert np.array_equal(part.cpu().numpy(), O.partition(M.edges, M.n, P, G))   # hierarchical EPG-1
+    assert np.array_equal(part.cpu().numpy(), O.partition(M.edges, M.n, P, G, method=method))   # hierarchical EPG
     L, plan = ctx.remap(E, M.n, part, k)
     U, dt = S.cfd_state(M.n), S.cfd_dt(M.volume)
     Un = ctx.permute_rows(torch.from_numpy(U).cuda(), L.vertex_perm, epg.PERM_SCATTER)

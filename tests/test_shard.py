@@ -14,13 +14,16 @@ import synth as S
 
 
 @pytest.mark.parametrize("G", [1, 2, 4, 8])
-@pytest.mark.parametrize("sched", ["ep", "default"])
+@pytest.mark.parametrize("sched", ["ep", "ep2", "default"])
 def test_shard_halos_host_matches_oracle(small_mesh, G, sched):
     from paper_1605_02043_b200 import epg
     M = small_mesh
     P = 256
     k = O.num_parts(M.m, P)
-    part = O.partition(M.edges, M.n, P, G) if sched == "ep" else O.default_partition(M.m, P)
+    if sched == "default":
+        part = O.default_partition(M.m, P)
+    else:
+        part = O.partition(M.edges, M.n, P, G, method=2 if sched == "ep2" else 1)
     L = O.remap(M.edges, M.n, part, k)
     begin, ids = epg.shard_halos_host(L.part_vertex_begin, L.halo_begin, L.halo_ids, k, G)
     rb, rids = O.shard_halos(M.edges, M.n, part, k, G, L.vertex_perm, L.part_vertex_begin)
@@ -33,7 +36,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, result_q):
+def _worker(rank, world, port, result_q, method=1):
     import sys
     here = os.path.dirname(os.path.abspath(__file__))
     sys.path.insert(0, os.path.dirname(here))
@@ -49,7 +52,7 @@ def _worker(rank, world, port, result_q):
         M = S2.kuhn_mesh(nbox=7, n_keep=1900)
         P = 128
         k = O2.num_parts(M.m, P)
-        part = O2.partition(M.edges, M.n, P, world)
+        part = O2.partition(M.edges, M.n, P, world, method=method)
         emu = EmuCtx(M.edges, M.n, M.normals, part, k)
         U = S2.cfd_state(M.n).astype(np.float64)
         dt = S2.cfd_dt(M.volume).astype(np.float64)
@@ -75,12 +78,13 @@ def _worker(rank, world, port, result_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_sharded_step_gloo(world):
+@pytest.mark.parametrize("world,method", [(2, 1), (4, 1), (2, 2), (4, 2)])
+def test_sharded_step_gloo(world, method):
+    """method 1: hierarchical EPG-1 shards; method 2: hierarchical EPG-2 (the bench's)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, method)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
