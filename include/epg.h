@@ -162,7 +162,9 @@ epg_status epg_partition_host(const int32_t *edges, int64_t m, int32_t n_vertice
  * grows on Eq. (1)'s own objective: the gain of a frontier task is the number
  * of its distinct endpoints already loaded by the growing partition, so each step adds
  * the fewest new loads; the frontier grows through vertex incidence lists instead of T.
- * Same sizes, hierarchy (shards) and determinism as EPG-1. */
+ * A vertex with more than 4 x part_size incident tasks (a hub, cut into many clusters
+ * whatever happens) attracts no tasks. Same sizes, hierarchy (shards) and
+ * determinism as EPG-1. */
 #define EPG_PARTITION_EPG1 1
 #define EPG_PARTITION_EPG2 2
 /* epg_partition_host with a method (EPG_ERR_INPUT for any other value). */

@@ -48,7 +48,7 @@ def lib():
             "orc_epg1": (C.c_int, [i64, P, P, P, P, i64, P]),
             "orc_partition": (C.c_int, [P, i64, i32, i32, i32, P]),
             "orc_partition_method": (C.c_int, [P, i64, i32, i32, i32, i32, P]),
-            "orc_epg2": (C.c_int, [i64, P, i32, P, i64, P]),
+            "orc_epg2": (C.c_int, [i64, P, i32, P, i64, i64, P]),
             "orc_remap": (C.c_int, [P, i64, i32, P, i64, P, P, P, P, P, P, i64, P]),
             "orc_shard_halos": (C.c_int, [P, i64, i32, P, i64, i32, P, P, P, P, i64]),
             "orc_cfd_flux": (None, [P, i64, i32, P, P, P]),
@@ -164,12 +164,13 @@ def epg1(t_ptr, t_adj, t_w, sizes) -> np.ndarray:
     return part
 
 
-def epg2(edges, n: int, sizes) -> np.ndarray:
-    """EPG-2 (O5') with explicit cluster sizes."""
+def epg2(edges, n: int, sizes, hub: int) -> np.ndarray:
+    """EPG-2 (O5') with explicit cluster sizes; vertices with more than `hub` tasks
+    attract none (the partitioner passes hub = 4P)."""
     e, m = _edges(edges)
     sizes = np.ascontiguousarray(sizes, dtype=np.int64)
     part = np.zeros(max(m, 1), dtype=np.int32)
-    st = lib().orc_epg2(m, _p(e), n, _p(sizes), sizes.size, _p(part))
+    st = lib().orc_epg2(m, _p(e), n, _p(sizes), sizes.size, hub, _p(part))
     if st:
         raise OracleError(st, "orc_epg2")
     return part[:m]

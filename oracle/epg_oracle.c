@@ -253,12 +253,18 @@ int orc_epg1(int64_t ntask, const int64_t *t_ptr, const int32_t *t_adj, const in
 /*     - pick the unassigned task with finite lst maximising g (its distinct */
 /*       endpoints already in V_i), ties by the smallest lst; part[t] = i;   */
 /*     - for each distinct endpoint u of t (u_t, then v_t) not yet in V_i:   */
-/*       add u to V_i; for each unassigned task t' incident to u, ascending */
-/*       id, each once: if lst[t'] = INF then lst[t'] = c++; g[t'] += 1;     */
+/*       add u to V_i; unless u is a hub (more than `hub` incident tasks),   */
+/*       for each unassigned task t' incident to u, ascending id, each once: */
+/*       if lst[t'] = INF then lst[t'] = c++; g[t'] += 1;                    */
 /*       if gst[t'] = INF then gst[t'] = G++ (G never reset).                */
+/* Hubs (reading Z20, after the hub discussion P:642-683): a vertex with more */
+/* tasks than four partitions hold (hub = 4P) is cut into many clusters      */
+/* whatever the growing does, so it attracts no tasks -- which also keeps    */
+/* power-law graphs from rescanning a hub's list in every partition that     */
+/* reaches it. No vertex of a mesh (degree <= 4) is a hub.                   */
 /* The pick is a plain linear scan over the tasks stamped in this partition. */
 /* ------------------------------------------------------------------------- */
-int orc_epg2(int64_t ntask, const int32_t *edges, int32_t n, const int64_t *sizes, int64_t nparts,
+int orc_epg2(int64_t ntask, const int32_t *edges, int32_t n, const int64_t *sizes, int64_t nparts, int64_t hub,
              int32_t *part) {
     int64_t total = 0;
     for (int64_t i = 0; i < nparts; i++) total += sizes[i];
@@ -324,6 +330,7 @@ int orc_epg2(int64_t ntask, const int32_t *edges, int32_t n, const int64_t *size
                 if (side == 1 && u == edges[2 * best]) continue;   /* distinct endpoints */
                 if (in_v[u]) continue;
                 in_v[u] = 1; vin[nvin++] = u;
+                if (ip[u + 1] - ip[u] > hub) continue;                 /* hub: attracts nothing */
                 for (int64_t q = ip[u]; q < ip[u + 1]; q++) {
                     int64_t nb = inc[q];
                     if (part[nb] != -1) continue;
@@ -347,8 +354,9 @@ int orc_epg2(int64_t ntask, const int32_t *edges, int32_t n, const int64_t *size
 /* hierarchical mode EPG-2's shard subproblem is the shard's tasks (renumbered by     */
 /* ascending id) with their original endpoints.                                       */
 static int grow_method(int method, int64_t ntask, const int64_t *tp, const int32_t *ta, const int32_t *tw,
-                       const int32_t *edges, int32_t n, const int64_t *sizes, int64_t nparts, int32_t *part) {
-    if (method == 2) return orc_epg2(ntask, edges, n, sizes, nparts, part);
+                       const int32_t *edges, int32_t n, const int64_t *sizes, int64_t nparts, int32_t P,
+                       int32_t *part) {
+    if (method == 2) return orc_epg2(ntask, edges, n, sizes, nparts, 4 * (int64_t)P, part);
     return orc_epg1(ntask, tp, ta, tw, sizes, nparts, part);
 }
 
@@ -378,7 +386,7 @@ int orc_partition_method(const int32_t *edges, int64_t m, int32_t n, int32_t P, 
     orc_part_sizes(m, k, s);
 
     if (shards == 1) {
-        st = grow_method(method, m, t_ptr, t_adj, t_w, edges, n, s, k, part);
+        st = grow_method(method, m, t_ptr, t_adj, t_w, edges, n, s, k, P, part);
     } else {
         int64_t Gs = shards;
         int64_t *ssize = (int64_t *)calloc(Gs, sizeof(int64_t));
@@ -386,7 +394,7 @@ int orc_partition_method(const int32_t *edges, int64_t m, int32_t n, int32_t P, 
             for (int64_t i = gi * k / Gs; i < (gi + 1) * k / Gs; i++) ssize[gi] += s[i];
         int32_t *shard = (int32_t *)malloc(sizeof(int32_t) * m);
         int32_t *sedges = (int32_t *)malloc(sizeof(int32_t) * 2 * m);    /* shard's edge list */
-        st = grow_method(method, m, t_ptr, t_adj, t_w, edges, n, ssize, Gs, shard);
+        st = grow_method(method, m, t_ptr, t_adj, t_w, edges, n, ssize, Gs, P, shard);
         int64_t *loc = (int64_t *)malloc(sizeof(int64_t) * m);   /* task -> id inside its shard */
         int64_t *glob = (int64_t *)malloc(sizeof(int64_t) * m);  /* local id -> task           */
         int64_t *sp = (int64_t *)malloc(sizeof(int64_t) * (m + 1));
@@ -407,7 +415,7 @@ int orc_partition_method(const int32_t *edges, int64_t m, int32_t n, int32_t P, 
             }
             for (int64_t j = 0; j < mg; j++) { sedges[2 * j] = edges[2 * glob[j]]; sedges[2 * j + 1] = edges[2 * glob[j] + 1]; }
             int64_t p0 = gi * k / Gs, p1 = (gi + 1) * k / Gs;
-            st = grow_method(method, mg, sp, sa, sw, sedges, n, s + p0, p1 - p0, sub);
+            st = grow_method(method, mg, sp, sa, sw, sedges, n, s + p0, p1 - p0, P, sub);
             for (int64_t j = 0; j < mg; j++) part[glob[j]] = (int32_t)(sub[j] + p0);
         }
         free(ssize); free(shard); free(sedges); free(loc); free(glob); free(sp); free(sa); free(sw); free(sub);

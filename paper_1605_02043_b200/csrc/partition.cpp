@@ -21,7 +21,8 @@
 //  EPG-2 (reading Z20): the same schedule, but the gain
 //  is Eq. (1)'s own objective -- a task's distinct endpoints already loaded by the
 //  partition (one load per distinct vertex), so the pick adds the fewest new
-//  loads. The frontier grows through the vertex incidence lists instead of T.
+//  loads. The frontier grows through the vertex incidence lists instead of T; vertices
+//  with more than 4 x part_size tasks (hubs) attract none.
 #include "epg_internal.h"
 
 #include <algorithm>
@@ -192,8 +193,10 @@ Incidence build_incidence(const int32_t *edges, int64_t m, int32_t n) {
 // EPG-2 growing: frontier heaps per gain 0..2 (distinct endpoints inside), lazy deletion
 // as for EPG-1; a vertex joins V_i the first time one of its tasks is taken (mark[v] = i
 // + 1, so the per-partition reset is free).
-bool grow_direct(const int32_t *edges, int64_t ntask, int32_t n, const int64_t *sizes, int64_t nparts, int32_t *part,
-                 const std::atomic<int> *cancel) {
+// A vertex with more than `hub` incident tasks (4 x part_size: it is cut into many clusters
+// whatever happens) attracts no tasks -- the hub discussion of P:642-683, reading Z20.
+bool grow_direct(const int32_t *edges, int64_t ntask, int32_t n, const int64_t *sizes, int64_t nparts, int64_t hub,
+                 int32_t *part, const std::atomic<int> *cancel) {
     const Incidence I = build_incidence(edges, ntask, n);
     std::vector<TaskState> st(ntask, TaskState{-1, kNoStamp, kNoStamp, 0});
     std::vector<int64_t> mark(static_cast<size_t>(n), 0);
@@ -235,6 +238,7 @@ bool grow_direct(const int32_t *edges, int64_t ntask, int32_t n, const int64_t *
                 if (side == 1 && v == ends[0]) break;   // distinct endpoints only
                 if (mark[v] == i + 1) continue;         // already loaded by this partition
                 mark[v] = i + 1;
+                if (I.beg[v + 1] - I.beg[v] > hub) continue;
                 for (int64_t q = I.beg[v]; q < I.beg[v + 1]; q++) {
                     const int32_t w = I.task[q];
                     TaskState &u = st[w];
@@ -292,13 +296,14 @@ epg_status host_partition(const int32_t *edges, int64_t m, int32_t n, int32_t pa
         return EPG_ERR_STATE;
     };
     if (method == EPG_PARTITION_EPG2) {
-        if (shards == 1) return grow_direct(edges, m, n, s.data(), k, part, cancel) ? EPG_OK : cancelled();
+        const int64_t hub = 4 * static_cast<int64_t>(part_size);
+        if (shards == 1) return grow_direct(edges, m, n, s.data(), k, hub, part, cancel) ? EPG_OK : cancelled();
         // hierarchical: shard-level growing, then growing on each shard's own edge list
         std::vector<int64_t> ssize(shards, 0);
         for (int g = 0; g < shards; g++)
             for (int64_t i = g * k / shards; i < (g + 1) * k / shards; i++) ssize[g] += s[i];
         std::vector<int32_t> shard(m);
-        if (!grow_direct(edges, m, n, ssize.data(), shards, shard.data(), cancel)) return cancelled();
+        if (!grow_direct(edges, m, n, ssize.data(), shards, hub, shard.data(), cancel)) return cancelled();
         for (int g = 0; g < shards; g++) {
             std::vector<int32_t> mem, sub_edges;
             for (int64_t t = 0; t < m; t++)
@@ -309,8 +314,8 @@ epg_status host_partition(const int32_t *edges, int64_t m, int32_t n, int32_t pa
                 }
             const int64_t p0 = g * k / shards, p1 = (g + 1) * k / shards;
             std::vector<int32_t> sub(mem.size());
-            if (!grow_direct(sub_edges.data(), static_cast<int64_t>(mem.size()), n, s.data() + p0, p1 - p0, sub.data(),
-                             cancel))
+            if (!grow_direct(sub_edges.data(), static_cast<int64_t>(mem.size()), n, s.data() + p0, p1 - p0, hub,
+                             sub.data(), cancel))
                 return cancelled();
             for (size_t j = 0; j < mem.size(); j++) part[mem[j]] = static_cast<int32_t>(sub[j] + p0);
         }

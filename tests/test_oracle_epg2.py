@@ -1,7 +1,8 @@
 """Pins for EPG-2 (O5', reading Z20 in DESIGN.md): balanced growing on the EP objective
 of Eq. (1) directly -- the task with the most distinct endpoints
 already in the growing cluster adds the fewest new loads -- with EPG-1's seed / stamp
-schedule (O5). SURVEY §8(f) rank 2 (partition quality beyond the T proxy).
+schedule (O5); a vertex with more than 4P tasks (a hub, cut into many clusters whatever
+happens) attracts none. SURVEY §8(f) rank 2 (partition quality beyond the T proxy).
 
 What fixes it, independently of oracle/:
   * hand traces on the paper's worked example (fig:mot) and SPEC's two-triangle
@@ -20,7 +21,7 @@ from bruteforce import loads_and_cut, optimum
 from conftest import golden
 
 
-def epg2_python(edges, n, sizes):
+def epg2_python(edges, n, sizes, hub):
     """O5' transcribed literally (pure Python, small inputs only)."""
     m = len(edges)
     INF = float("inf")
@@ -54,6 +55,8 @@ def epg2_python(edges, n, sizes):
                 if w in inV:
                     continue
                 inV.add(w)
+                if len(inc[w]) > hub:          # a hub attracts no tasks
+                    continue
                 for t2 in inc[w]:
                     if part[t2] != -1:
                         continue
@@ -104,7 +107,7 @@ def test_epg2_invariants_and_transcription(seed):
     part = O.partition(e, n, P, method=2)
     assert np.bincount(part, minlength=k).tolist() == O.part_sizes(m, k).tolist()   # exact +-1 (Z2)
     assert np.array_equal(part, O.partition(e, n, P, method=2))                      # deterministic
-    assert part.tolist() == epg2_python(e.tolist(), n, O.part_sizes(m, k).tolist())
+    assert part.tolist() == epg2_python(e.tolist(), n, O.part_sizes(m, k).tolist(), 4 * P)
 
 
 def test_epg2_vs_bruteforce():
@@ -132,6 +135,25 @@ def test_epg2_vs_bruteforce():
     assert hits / total >= 0.60
 
 
+def test_epg2_hub_rule():
+    """A star with 14 leaves at P = 3 (hub threshold 4P = 12): the centre attracts nothing,
+    so every cluster restarts at the smallest unassigned id -- contiguous chunks of the task
+    order, C = k - 1 = 4 (the optimum: the centre is in every cluster). With 12 leaves the
+    centre is not a hub, and growing follows its incidence list -- the same chunks here."""
+    for leaves in (14, 12):
+        e = np.array([[0, i + 1] for i in range(leaves)], np.int32)
+        k = O.num_parts(leaves, 3)
+        part = O.partition(e, leaves + 1, 3, method=2)
+        assert part.tolist() == [i // 3 for i in range(leaves)]
+        assert part.tolist() == epg2_python(e.tolist(), leaves + 1, O.part_sizes(leaves, k).tolist(), 12)
+        assert O.cost(e, leaves + 1, part, k).cut_cost == k - 1
+    # a hub with a pendant path: the path still grows through its own vertices
+    e2 = np.array([[0, i + 1] for i in range(13)] + [[13, 14], [14, 15], [15, 16]], np.int32)
+    p2 = O.partition(e2, 17, 4, method=2)
+    assert p2.tolist() == epg2_python(e2.tolist(), 17, O.part_sizes(16, 4).tolist(), 16)
+    assert O.cost(e2, 17, p2, 4).cut_cost <= O.cost(e2, 17, O.default_partition(16, 4), 4).cut_cost
+
+
 def test_epg2_paths_and_equal_cycles():
     for m, k in [(12, 3), (12, 2), (40, 4)]:
         n, e = S.path_graph(m)
@@ -149,17 +171,17 @@ def test_epg2_hierarchical(small_mesh):
     P = 256
     k = O.num_parts(M.m, P)
     s = O.part_sizes(M.m, k)
-    assert np.array_equal(O.partition(M.edges, M.n, P, 1, method=2), O.epg2(M.edges, M.n, s))
+    assert np.array_equal(O.partition(M.edges, M.n, P, 1, method=2), O.epg2(M.edges, M.n, s, 4 * P))
     for G in (2, 4):
         part = O.partition(M.edges, M.n, P, G, method=2)
         assert np.bincount(part, minlength=k).tolist() == s.tolist()
         ssz = [int(s[g * k // G:(g + 1) * k // G].sum()) for g in range(G)]
-        shard = O.epg2(M.edges, M.n, ssz)
+        shard = O.epg2(M.edges, M.n, ssz, 4 * P)
         for g in range(G):
             sel = shard == g
             assert np.all((part[sel] >= g * k // G) & (part[sel] < (g + 1) * k // G))
             # inside a shard: EPG-2 on the shard's tasks, renumbered by ascending id
-            sub = O.epg2(M.edges[sel], M.n, s[g * k // G:(g + 1) * k // G])
+            sub = O.epg2(M.edges[sel], M.n, s[g * k // G:(g + 1) * k // G], 4 * P)
             assert np.array_equal(part[sel], sub + g * k // G)
 
 
