@@ -251,6 +251,24 @@ epg_status epg_remapped_edges(epg_ctx *ctx, const int32_t *edges, int64_t m, con
  * hub vertices under the hub split (epg_set_hub_split; never on cfd meshes). */
 epg_status epg_run(epg_ctx *ctx, const epg_plan *plan, epg_kernel kernel, epg_state *state, int32_t steps);
 
+/* epg_run from and to HOST memory (the end-to-end call): one call copies the state
+ * (state_in_host, [n][row] floats, ORIGINAL vertex order, row = 5 for CFD_FLUX, 1 otherwise)
+ * to the device, moves it into the plan layout (vertex_perm: DEVICE, epg_remap's layout),
+ * runs `steps` time steps as epg_run, moves the result back to the original order and
+ * copies it to state_out_host (same shape). edge_payload / vertex_const: DEVICE, plan
+ * layout, as for epg_run. Asynchronous: the H2D and D2H run on two ctx-owned streams and
+ * the compute on ctx's stream, with double-buffered device staging, so consecutive calls
+ * overlap one call's D2H with the next call's H2D and compute. Host buffers must stay
+ * valid (and unchanged, for state_in_host) until the call's copies finish; pinned host
+ * memory makes the copies truly asynchronous. The outputs of all calls so far are complete
+ * once ctx's stream has executed a later epg_run_host_join(ctx) (which only enqueues a
+ * wait). EPG_ERR_NOMEM if the ctx-owned buffers (5 x n x row floats) cannot be allocated. */
+epg_status epg_run_host(epg_ctx *ctx, const epg_plan *plan, epg_kernel kernel, const int32_t *vertex_perm,
+                        const void *state_in_host, void *state_out_host, const void *edge_payload,
+                        const void *vertex_const, int32_t steps);
+/* Makes ctx's stream wait for every D2H copy epg_run_host has enqueued so far. */
+epg_status epg_run_host_join(epg_ctx *ctx);
+
 /* The default (unscheduled) comparator: the same functor with one thread per task
  * in original order, operands read straight from global memory and results
  * accumulated with global atomics, then a per-vertex update (the original kernel of

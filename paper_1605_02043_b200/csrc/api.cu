@@ -17,9 +17,22 @@
 #include "pipelined_kernel.cuh"
 #include "occupancy_kernel.cuh"
 
+// epg_run_host's pipeline (ctx-owned): copy-in and copy-out streams beside the ctx stream,
+// double-buffered staging so call i+1's H2D and call i's D2H overlap the compute.
+struct HostRun {
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    size_t bytes = 0;                       // capacity of every buffer below
+    void *stage_in[2] = {nullptr, nullptr}, *stage_out[2] = {nullptr, nullptr};
+    void *buf[2] = {nullptr, nullptr};      // plan-layout ping-pong state
+    cudaEvent_t ev_in[2] = {}, ev_consumed[2] = {}, ev_comp[2] = {}, ev_out[2] = {};
+    bool used[2] = {false, false};
+    int parity = 0;
+};
+
 struct epg_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    HostRun *hr = nullptr;
     std::string err;
     float *naive_F = nullptr;
     size_t naive_F_bytes = 0;
@@ -978,6 +991,19 @@ void epg_destroy(epg_ctx *ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     if (ctx->naive_F) cudaFree(ctx->naive_F);
+    if (HostRun *h = ctx->hr) {
+        cudaStreamSynchronize(h->s_in);
+        cudaStreamSynchronize(h->s_out);
+        cudaStreamSynchronize(ctx->stream);
+        for (int j = 0; j < 2; j++) {
+            cudaFree(h->stage_in[j]); cudaFree(h->stage_out[j]); cudaFree(h->buf[j]);
+            cudaEventDestroy(h->ev_in[j]); cudaEventDestroy(h->ev_consumed[j]);
+            cudaEventDestroy(h->ev_comp[j]); cudaEventDestroy(h->ev_out[j]);
+        }
+        cudaStreamDestroy(h->s_in);
+        cudaStreamDestroy(h->s_out);
+        delete h;
+    }
     for (auto &u : ctx->ev_used) { cudaEventDestroy(u.second.first); cudaEventDestroy(u.second.second); }
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
     delete ctx;
@@ -1321,6 +1347,86 @@ epg_status epg_run(epg_ctx *ctx, const epg_plan *plan, epg_kernel kernel, epg_st
             return run_staged<GatherScatter>(ctx, const_cast<epg_plan *>(plan), state, steps);
         default: return run_staged<Spmv>(ctx, const_cast<epg_plan *>(plan), state, steps);
     }
+}
+
+epg_status epg_run_host(epg_ctx *ctx, const epg_plan *plan, epg_kernel kernel, const int32_t *vertex_perm,
+                        const void *state_in_host, void *state_out_host, const void *edge_payload,
+                        const void *vertex_const, int32_t steps) {
+    if (!ctx) return EPG_ERR_STATE;
+    if (!plan) return ctx->fail(EPG_ERR_INPUT, "run_host: plan is NULL");
+    if (plan->ctx != ctx || plan->device != ctx->device)
+        return ctx->fail(EPG_ERR_STATE, "run_host: plan belongs to another context");
+    if (!vertex_perm || !state_in_host || !state_out_host || steps < 0)
+        return ctx->fail(EPG_ERR_INPUT, "run_host: need vertex_perm, host state in/out and steps >= 0");
+    if (kernel < EPG_KERNEL_CFD_FLUX || kernel > EPG_KERNEL_SPMV) return ctx->fail(EPG_ERR_INPUT, "run_host: unknown kernel id");
+    CU(cudaSetDevice(ctx->device));
+    const int row = kernel == EPG_KERNEL_CFD_FLUX ? 5 : 1;
+    const size_t bytes = sizeof(float) * row * (size_t)plan->n;
+    HostRun *h = ctx->hr;
+    if (!h) {
+        h = ctx->hr = new HostRun();
+        CU(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
+        CU(cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
+        for (int j = 0; j < 2; j++) {
+            CU(cudaEventCreateWithFlags(&h->ev_in[j], cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&h->ev_consumed[j], cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&h->ev_comp[j], cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&h->ev_out[j], cudaEventDisableTiming));
+        }
+    }
+    if (h->bytes < bytes) {   // (re)allocate: drain the pipeline first
+        CU(cudaStreamSynchronize(h->s_in));
+        CU(cudaStreamSynchronize(h->s_out));
+        CU(cudaStreamSynchronize(ctx->stream));
+        for (int j = 0; j < 2; j++) {
+            cudaFree(h->stage_in[j]); cudaFree(h->stage_out[j]); cudaFree(h->buf[j]);
+            h->stage_in[j] = h->stage_out[j] = h->buf[j] = nullptr;
+            h->used[j] = false;
+        }
+        for (int j = 0; j < 2; j++) {
+            if (cudaMalloc(&h->stage_in[j], bytes) || cudaMalloc(&h->stage_out[j], bytes) || cudaMalloc(&h->buf[j], bytes)) {
+                cudaGetLastError();
+                h->bytes = 0;
+                return ctx->fail(EPG_ERR_NOMEM, "run_host: device buffers");
+            }
+        }
+        h->bytes = bytes;
+    }
+    const int j = h->parity;
+    h->parity ^= 1;
+    // copy-in: stage_in[j] is free once call i-2's scatter consumed it
+    if (h->used[j]) CU(cudaStreamWaitEvent(h->s_in, h->ev_consumed[j], 0));
+    CU(cudaMemcpyAsync(h->stage_in[j], state_in_host, bytes, cudaMemcpyHostToDevice, h->s_in));
+    CU(cudaEventRecord(h->ev_in[j], h->s_in));
+    // compute on the ctx stream: original order -> plan layout, steps, back
+    CU(cudaStreamWaitEvent(ctx->stream, h->ev_in[j], 0));
+    epg_status st = epg_permute_rows(ctx, h->stage_in[j], h->buf[0], plan->n, 4 * row, vertex_perm, 1);
+    if (st) return st;
+    CU(cudaEventRecord(h->ev_consumed[j], ctx->stream));
+    void *res = h->buf[0];
+    if (steps > 0) {
+        epg_state sst{h->buf[0], h->buf[1], edge_payload, vertex_const};
+        if ((st = epg_run(ctx, plan, kernel, &sst, steps))) return st;
+        res = h->buf[steps & 1];
+    }
+    if (h->used[j]) CU(cudaStreamWaitEvent(ctx->stream, h->ev_out[j], 0));   // call i-2's D2H read stage_out[j]
+    if ((st = epg_permute_rows(ctx, res, h->stage_out[j], plan->n, 4 * row, vertex_perm, 0))) return st;
+    CU(cudaEventRecord(h->ev_comp[j], ctx->stream));
+    // copy-out
+    CU(cudaStreamWaitEvent(h->s_out, h->ev_comp[j], 0));
+    CU(cudaMemcpyAsync(state_out_host, h->stage_out[j], bytes, cudaMemcpyDeviceToHost, h->s_out));
+    CU(cudaEventRecord(h->ev_out[j], h->s_out));
+    h->used[j] = true;
+    return EPG_OK;
+}
+
+epg_status epg_run_host_join(epg_ctx *ctx) {
+    if (!ctx) return EPG_ERR_STATE;
+    if (!ctx->hr) return EPG_OK;
+    CU(cudaSetDevice(ctx->device));
+    for (int j = 0; j < 2; j++)
+        if (ctx->hr->used[j]) CU(cudaStreamWaitEvent(ctx->stream, ctx->hr->ev_out[j], 0));
+    return EPG_OK;
 }
 
 epg_status epg_run_naive(epg_ctx *ctx, epg_kernel kernel, const int32_t *edges, int64_t m, int32_t n,

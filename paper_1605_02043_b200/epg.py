@@ -33,7 +33,8 @@ SYMBOLS = ["epg_create", "epg_destroy", "epg_last_error", "epg_num_parts", "epg_
            "epg_shard_reduce", "epg_accumulate_rows", "epg_remapped_edges", "epg_set_hub_split", "epg_plan_hubs",
            "epg_set_exec_limits", "epg_partition_random_host", "epg_partition_greedy_host",
            "epg_adaptive_create", "epg_adaptive_step", "epg_adaptive_wait", "epg_adaptive_read_state",
-           "epg_adaptive_info", "epg_adaptive_destroy", "epg_partition_host_method", "epg_set_partition_method"]
+           "epg_adaptive_info", "epg_adaptive_destroy", "epg_partition_host_method", "epg_set_partition_method",
+           "epg_run_host", "epg_run_host_join"]
 
 
 class _Report(C.Structure):
@@ -78,6 +79,8 @@ def _load():
         "epg_plan_info": (st, [P, P]),
         "epg_permute_rows": (st, [P, P, P, i64, i32, P, i32]),
         "epg_run": (st, [P, P, C.c_int, C.POINTER(_State), i32]),
+        "epg_run_host": (st, [P, P, C.c_int, P, P, P, P, P, i32]),
+        "epg_run_host_join": (st, [P]),
         "epg_run_naive": (st, [P, C.c_int, P, i64, i32, C.POINTER(_State), i32]),
         "epg_set_variant": (st, [P, i32]),
         "epg_set_hub_split": (st, [P, i32]),
@@ -380,6 +383,22 @@ class Context:
         st = _State(_ptr(state_in), _ptr(state_out), _ptr(payload), _ptr(vconst))
         self._check(lib.epg_run(self.handle, plan.handle, kernel, C.byref(st), steps))
         return state_out if steps % 2 else state_in
+
+    def run_host(self, plan: Plan, kernel: int, vertex_perm: torch.Tensor, state_in_host: torch.Tensor,
+                 state_out_host: torch.Tensor, payload: torch.Tensor | None = None,
+                 vconst: torch.Tensor | None = None, steps: int = 1):
+        """epg_run_host: host (ideally pinned) state in original vertex order -> device ->
+        `steps` steps -> host; asynchronous, complete after join() has run on the stream."""
+        for t in (state_in_host, state_out_host):
+            if t.is_cuda or not t.is_contiguous() or t.dtype != torch.float32:
+                raise ValueError("run_host: host state must be contiguous float32 CPU tensors")
+        self._check(lib.epg_run_host(self.handle, plan.handle, kernel, _ptr(vertex_perm), state_in_host.data_ptr(),
+                                     state_out_host.data_ptr(), _ptr(payload), _ptr(vconst), steps))
+        return state_out_host
+
+    def join(self):
+        """epg_run_host_join: the ctx stream waits for every pending epg_run_host copy-out."""
+        self._check(lib.epg_run_host_join(self.handle))
 
     # -- multi-GPU shards ---------------------------------------------------------------
     def shard_ranges(self, plan: Plan, G: int, g: int) -> dict:
