@@ -113,6 +113,8 @@ def parse():
                          "Eq. (1)'s objective, SURVEY 8(f) rank 2); the other one runs as a comparator")
     ap.add_argument("--exec-rows", type=int, default=0,
                     help="execution-split row cap (epg_set_exec_limits; 0 = the config's default)")
+    ap.add_argument("--exec-edges", type=int, default=0,
+                    help="execution-split edge cap (0: 1024, or 1280 when --part-size > 1024)")
     ap.add_argument("--no-comparators", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-sharded", action="store_true",
@@ -428,7 +430,7 @@ def run_ours(args, rank, local_rank, world):
     KER = M.kernel
     if args.exec_rows:
         M.exec_rows = args.exec_rows
-    ctx.set_exec_limits(M.exec_rows, 1024)
+    ctx.set_exec_limits(M.exec_rows, args.exec_edges or (1280 if P > 1024 else 1024))
     ctx.set_variant(args.variant)
     E = torch.from_numpy(M.edges).to(dev)
     k = epg.num_parts(M.m, P)

@@ -324,10 +324,12 @@ epg_status epg_set_variant(epg_ctx *ctx, int32_t variant);
 /* Execution-split caps for plans created by later epg_remap calls on ctx: an EP
  * partition with more than max_rows staged rows (|V_p|) or max_edges edges is executed
  * as contiguous ranges of its reorganised edges (the public layout is unchanged; see
- * epg_plan_info's k_exec). max_rows in [64, 2048] (above 1024 only one-float functors,
- * GATHER_SCATTER and SPMV, run the occupancy kernel), max_edges in [32, 1024]; -1 keeps
+ * epg_plan_info's k_exec). max_rows in [64, 2048] (above 1280 only one-float functors,
+ * GATHER_SCATTER and SPMV, run the occupancy kernel), max_edges in [32, 1280]; -1 keeps
  * the default: EPG_EXEC_MAX_ROWS / EPG_EXEC_MAX_EDGES from the environment, else 704
- * rows (a cfd CTA at ~55 KB of shared memory, four per SM) and 1024 edges.
+ * rows (a cfd CTA at ~55 KB of shared memory, four per SM) and 1024 edges. Raising both
+ * lets partitions of up to 1280 edges run unsplit, e.g. to size the grid to a multiple of
+ * the SM count.
  * EPG_ERR_INPUT outside these ranges. */
 epg_status epg_set_exec_limits(epg_ctx *ctx, int32_t max_rows, int32_t max_edges);
 

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <map>
 #include <queue>
 #include <climits>
@@ -493,7 +494,7 @@ epg_status build_pipeline_blob(epg_ctx *ctx, epg_plan *pl) {
             return st;
         k_build_blob3<<<(unsigned)k, 256, 0, ctx->stream>>>(pl->peb, pl->pvb, pl->hb, pl->halo_ids, pl->inc,
                                                            pl->inc_off, o3.as<int32_t>(), W,
-                                                           hw == 2 ? hub_of_h.as<int32_t>() : nullptr, pl->blob3,
+                                                           hw == 2 ? hub_of_h.as<int32_t>() : nullptr, pl->Scap, pl->blob3,
                                                            pl->desc3);
         CHECK_LAUNCH();
         CU(cudaStreamSynchronize(ctx->stream));
@@ -658,10 +659,11 @@ epg_status run_pipelined(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t s
     }
 }
 
-// occupancy kernel limits: execution partitions of <= 1024 edges (EPT x BLOCK, the Phi
-// sentinel) and <= 1024 staged rows (VPT 4), 2048 for one-float rows (VPT 8)
-constexpr int kOccThreads = 256, kOccEPT = 4;
-constexpr int kOccMaxEdges = 1024, kOccMaxRows = 1024, kOccMaxRowsScalar = 2048;
+// occupancy kernel limits: execution partitions of <= 1280 edges (EPT 5 x 256 threads) and
+// <= 1280 staged rows (VPT 5), 2048 for one-float rows (VPT 8)
+constexpr int kOccThreads = 256;
+constexpr int kOccMaxEdges = 1280, kOccMaxRows = 1280, kOccMaxRowsScalar = 2048;
+constexpr int kOccDefaultEdges = 1024;   // execution-split default (EPT 4 x 256 threads)
 template <class Fn> constexpr int occ_max_rows() { return Fn::ROW == 1 ? kOccMaxRowsScalar : kOccMaxRows; }
 // execution-split caps of a remap: epg_set_exec_limits, else EPG_EXEC_MAX_EDGES /
 // EPG_EXEC_MAX_ROWS, else 1024 edges and 704 rows (704 rows keep a cfd CTA at ~55 KB of
@@ -669,7 +671,7 @@ template <class Fn> constexpr int occ_max_rows() { return Fn::ROW == 1 ? kOccMax
 int exec_max_edges(const epg_ctx *ctx) {
     if (ctx->exec_edges > 0) return ctx->exec_edges;
     const char *e = std::getenv("EPG_EXEC_MAX_EDGES");
-    const int x = e ? std::atoi(e) : kOccMaxEdges;
+    const int x = e ? std::atoi(e) : kOccDefaultEdges;
     return std::min(kOccMaxEdges, std::max(32, x));
 }
 int exec_max_rows(const epg_ctx *ctx) {
@@ -696,9 +698,9 @@ cudaError_t launch_pdl(K kern, unsigned grid, unsigned block, size_t smem, cudaS
     return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
-template <class Fn, int W, int VPT, int EPT = kOccEPT>
-epg_status launch_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, OccArgs a, size_t smem) {
-    auto kern = k_edge_occ<Fn, kOccThreads, EPT, VPT, W>;
+template <class Fn>
+epg_status launch_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, OccArgs a, size_t smem,
+                      void (*kern)(OccArgs)) {
     CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     {   // early PDL trigger only when the whole grid is resident at once (one wave)
         auto it = pl->resident_ctas.find(reinterpret_cast<const void *>(kern));
@@ -750,6 +752,36 @@ epg_status launch_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t step
     return EPG_OK;
 }
 
+// Instance of the occupancy kernel for a plan: EPT edges and VPT staged rows per thread
+// (256 threads), W the padded incidence width. `go` is called with the chosen instance.
+template <class Fn, class Go>
+epg_status occ_dispatch(const epg_plan *pl, Go &&go) {
+    const int S = pl->Scap, L = pl->Lcap;
+    auto by_w = [&](auto ept, auto vpt) -> epg_status {
+        constexpr int E = decltype(ept)::value, V = decltype(vpt)::value;
+        switch (pl->inc_width) {
+            case 4: return go(k_edge_occ<Fn, kOccThreads, E, V, 4>, E, V);
+            case 8: return go(k_edge_occ<Fn, kOccThreads, E, V, 8>, E, V);
+            default: return go(k_edge_occ<Fn, kOccThreads, E, V, 0>, E, V);
+        }
+    };
+    using I2 = std::integral_constant<int, 2>;
+    using I3 = std::integral_constant<int, 3>;
+    using I4 = std::integral_constant<int, 4>;
+    using I5 = std::integral_constant<int, 5>;
+    using I8 = std::integral_constant<int, 8>;
+    if (S <= 2 * kOccThreads && L <= 2 * kOccThreads) return by_w(I2{}, I2{});   // small partitions
+    if constexpr (Fn::ROW == 1) {   // one-float rows: up to 2048 staged rows, 8 per thread
+        if (L > 4 * kOccThreads) return S > 4 * kOccThreads ? by_w(I5{}, I8{}) : by_w(I4{}, I8{});
+    }
+    if (S > 4 * kOccThreads) {      // 1025..1280 edges (grids sized to the SM count)
+        if (L > 4 * kOccThreads) return by_w(I5{}, I5{});
+        return L > 3 * kOccThreads ? by_w(I5{}, I4{}) : by_w(I5{}, I3{});
+    }
+    if (L > 4 * kOccThreads) return by_w(I4{}, I5{});
+    return L > 3 * kOccThreads ? by_w(I4{}, I4{}) : by_w(I4{}, I3{});
+}
+
 template <class Fn>
 epg_status run_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, bool *fits) {
     *fits = false;
@@ -761,7 +793,8 @@ epg_status run_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, 
     const int recs_bytes = up16i(4 * Fn::REC * pl->Lcap + 64);
     a.rows_land = up16i(recs_bytes - (4 * Fn::ROW * pl->Lcap + 16) - 16);
     a.off_phi = a.off_recs + recs_bytes;
-    const size_t smem = (size_t)a.off_phi + up16i(4 * Fn::PHIREC * (kPhiSentinel + 1));
+    a.sentinel = pl->Scap;
+    const size_t smem = (size_t)a.off_phi + up16i(4 * Fn::PHIREC * (pl->Scap + 1));
     if (smem + 1024 > (size_t)dev_max) return EPG_OK;
     *fits = true;
     a.desc = pl->desc3;
@@ -773,31 +806,9 @@ epg_status run_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, 
     a.first = 0;
     a.hw = pl->hub_words;
     a.hub_acc = pl->n_hub > 0 ? pl->hub_acc : nullptr;
-    const bool v4 = pl->Lcap > 3 * kOccThreads;
-    if (pl->Scap <= 2 * kOccThreads && pl->Lcap <= 2 * kOccThreads) {   // small execution partitions
-        switch (pl->inc_width) {
-            case 4: return launch_occ<Fn, 4, 2, 2>(ctx, pl, state, steps, a, smem);
-            case 8: return launch_occ<Fn, 8, 2, 2>(ctx, pl, state, steps, a, smem);
-            default: return launch_occ<Fn, 0, 2, 2>(ctx, pl, state, steps, a, smem);
-        }
-    }
-    if constexpr (Fn::ROW == 1) {   // more than 1024 staged rows: 8 rows per thread
-        if (pl->Lcap > 4 * kOccThreads) {
-            switch (pl->inc_width) {
-                case 4: return launch_occ<Fn, 4, 8>(ctx, pl, state, steps, a, smem);
-                case 8: return launch_occ<Fn, 8, 8>(ctx, pl, state, steps, a, smem);
-                default: return launch_occ<Fn, 0, 8>(ctx, pl, state, steps, a, smem);
-            }
-        }
-    }
-    switch (pl->inc_width) {
-        case 4: return v4 ? launch_occ<Fn, 4, 4>(ctx, pl, state, steps, a, smem)
-                          : launch_occ<Fn, 4, 3>(ctx, pl, state, steps, a, smem);
-        case 8: return v4 ? launch_occ<Fn, 8, 4>(ctx, pl, state, steps, a, smem)
-                          : launch_occ<Fn, 8, 3>(ctx, pl, state, steps, a, smem);
-        default: return v4 ? launch_occ<Fn, 0, 4>(ctx, pl, state, steps, a, smem)
-                           : launch_occ<Fn, 0, 3>(ctx, pl, state, steps, a, smem);
-    }
+    return occ_dispatch<Fn>(pl, [&](auto kern, int, int) {
+        return launch_occ<Fn>(ctx, pl, state, steps, a, smem, kern);
+    });
 }
 
 // edge kernel over execution partitions [first, first + count) only (no finalise)
@@ -810,7 +821,8 @@ epg_status run_edges_range(epg_ctx *ctx, epg_plan *pl, epg_state *state, int64_t
     const int recs_bytes = up16i(4 * Fn::REC * pl->Lcap + 64);
     a.rows_land = up16i(recs_bytes - (4 * Fn::ROW * pl->Lcap + 16) - 16);
     a.off_phi = a.off_recs + recs_bytes;
-    const size_t smem = (size_t)a.off_phi + up16i(4 * Fn::PHIREC * (kPhiSentinel + 1));
+    a.sentinel = pl->Scap;
+    const size_t smem = (size_t)a.off_phi + up16i(4 * Fn::PHIREC * (pl->Scap + 1));
     a.desc = pl->desc3;
     a.blob = pl->blob3;
     a.slots = pl->slots;
@@ -823,28 +835,13 @@ epg_status run_edges_range(epg_ctx *ctx, epg_plan *pl, epg_state *state, int64_t
     a.hw = pl->hub_words;
     a.hub_acc = nullptr;   // shard ranges sum every halo partial through hv_list
     if (count <= 0) return EPG_OK;
-    auto go = [&](auto kern) -> epg_status {
+    return occ_dispatch<Fn>(pl, [&](auto kern, int, int) -> epg_status {
         CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         cudaEvent_t t0 = ctx->prof_begin();
         CU(launch_pdl(kern, (unsigned)count, kOccThreads, smem, ctx->stream, a));
         ctx->prof_end(0, t0);
         return EPG_OK;
-    };
-    const bool v4 = pl->Lcap > 3 * kOccThreads;
-    if constexpr (Fn::ROW == 1) {
-        if (pl->Lcap > 4 * kOccThreads) {
-            switch (pl->inc_width) {
-                case 4: return go(k_edge_occ<Fn, kOccThreads, kOccEPT, 8, 4>);
-                case 8: return go(k_edge_occ<Fn, kOccThreads, kOccEPT, 8, 8>);
-                default: return go(k_edge_occ<Fn, kOccThreads, kOccEPT, 8, 0>);
-            }
-        }
-    }
-    switch (pl->inc_width) {
-        case 4: return v4 ? go(k_edge_occ<Fn, kOccThreads, kOccEPT, 4, 4>) : go(k_edge_occ<Fn, kOccThreads, kOccEPT, 3, 4>);
-        case 8: return v4 ? go(k_edge_occ<Fn, kOccThreads, kOccEPT, 4, 8>) : go(k_edge_occ<Fn, kOccThreads, kOccEPT, 3, 8>);
-        default: return v4 ? go(k_edge_occ<Fn, kOccThreads, kOccEPT, 4, 0>) : go(k_edge_occ<Fn, kOccThreads, kOccEPT, 3, 0>);
-    }
+    });
 }
 
 template <class Fn>
@@ -1607,7 +1604,7 @@ epg_status epg_set_exec_limits(epg_ctx *ctx, int32_t max_rows, int32_t max_edges
     if (!ctx) return EPG_ERR_STATE;
     if (!(max_rows == -1 || (max_rows >= 64 && max_rows <= kOccMaxRowsScalar)) ||
         !(max_edges == -1 || (max_edges >= 32 && max_edges <= kOccMaxEdges)))
-        return ctx->fail(EPG_ERR_INPUT, "set_exec_limits: max_rows in [64, 2048], max_edges in [32, 1024], or -1");
+        return ctx->fail(EPG_ERR_INPUT, "set_exec_limits: max_rows in [64, 2048], max_edges in [32, 1280], or -1");
     ctx->exec_rows = max_rows;
     ctx->exec_edges = max_edges;
     return EPG_OK;

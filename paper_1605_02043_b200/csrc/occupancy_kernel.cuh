@@ -31,8 +31,8 @@ namespace epg {
 // hubs: hw = 2 words per halo row) pad16 [incidence] (W as in the pipelined blob: W x L u16
 // padded lists, or W = 0: 2s u16 entries + L u16 offsets)
 __host__ __device__ __forceinline__ int blob3_inc_offset(int nH, int hw = 1) { return (4 * hw * nH + 15) & ~15; }
-// padded incidence entries point at this Phi record, kept zero (>= every EPT x BLOCK)
-constexpr int kPhiSentinel = 1024;
+// padded incidence entries point at Phi record `sentinel` (the plan's largest execution
+// partition, >= every edge index), kept zero by the kernel
 __host__ __device__ __forceinline__ int blob3_bytes_for(int nH, int s, int L, int W, int hw = 1) {
     const int inc = W > 0 ? 2 * W * L : 4 * s + 2 * L;
     return (blob3_inc_offset(nH, hw) + inc + 15) & ~15;
@@ -52,6 +52,7 @@ struct OccArgs {
     int hw;                    // blob words per halo row (2: hub indices follow the halo ids)
     float *hub_acc;            // [hubs][ROW] or NULL: hub partials are added here as well
     int early_pdl;             // 1: trigger dependents at the start (single-wave grids)
+    int sentinel;              // zero Phi record of padded incidence entries (plan Scap)
 };
 
 template <class Fn, int BLOCK, int EPT, int VPT, int W>
@@ -165,7 +166,7 @@ __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
         if (i < d.s) Fn::edge_rec_pw(recs, (int)(sl[r] & 0xffffu), (int)(sl[r] >> 16), pw[r], i, phis);
     }
     if constexpr (W > 0) {
-        if (tid == 0) Fn::zero_phi(phis, kPhiSentinel);
+        if (tid == 0) Fn::zero_phi(phis, a.sentinel);
     }
     __syncthreads();
     EPG_TP(0, 4);
@@ -560,7 +561,7 @@ __global__ void k_build_blob3(const int32_t *__restrict__ peb, const int32_t *__
                               const int32_t *__restrict__ hb, const int32_t *__restrict__ halo_ids,
                               const uint16_t *__restrict__ inc, const uint16_t *__restrict__ inc_off,
                               const int32_t *__restrict__ blob16, int W, const int32_t *__restrict__ hub_of_h,
-                              unsigned char *blob, PartDesc *desc) {
+                              int sentinel, unsigned char *blob, PartDesc *desc) {
     const int p = blockIdx.x;
     const int o0 = pvb[p], nO = pvb[p + 1] - o0, h0 = hb[p], nH = hb[p + 1] - h0, e0 = peb[p], s = peb[p + 1] - e0;
     const int L = nO + nH;
@@ -576,7 +577,7 @@ __global__ void k_build_blob3(const int32_t *__restrict__ peb, const int32_t *__
         for (int j = threadIdx.x; j < L; j += blockDim.x) {
             const int q0 = inc_off[lbase + j], q1 = j + 1 < L ? inc_off[lbase + j + 1] : 2 * s;
             for (int r = 0; r < W; r++)
-                ic[W * j + r] = q0 + r < q1 ? inc[2 * (int64_t)e0 + q0 + r] : (uint16_t)(kPhiSentinel << 1);
+                ic[W * j + r] = q0 + r < q1 ? inc[2 * (int64_t)e0 + q0 + r] : (uint16_t)(sentinel << 1);
         }
     } else {
         uint16_t *io = ic + 2 * s;
