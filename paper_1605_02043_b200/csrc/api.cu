@@ -711,6 +711,11 @@ epg_status launch_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t step
             it = pl->resident_ctas.emplace(reinterpret_cast<const void *>(kern), (int64_t)occ * sms).first;
         }
         a.early_pdl = pl->k <= it->second ? 1 : 0;
+        // multi-wave grids: prefetch one resident wave ahead (EPG_PREFETCH_AHEAD=0 disables)
+        const char *e = std::getenv("EPG_PREFETCH_AHEAD");
+        const int64_t ahead = e ? std::atoll(e) : it->second;
+        a.ahead = a.early_pdl ? 0 : ahead;
+        a.count = pl->k;
     }
     float *bufs[2] = {static_cast<float *>(state->state_in), static_cast<float *>(state->state_out)};
     const int64_t fin_work = pl->S + (pl->n - pl->touched);

@@ -53,7 +53,16 @@ struct OccArgs {
     float *hub_acc;            // [hubs][ROW] or NULL: hub partials are added here as well
     int early_pdl;             // 1: trigger dependents at the start (single-wave grids)
     int sentinel;              // zero Phi record of padded incidence entries (plan Scap)
+    int64_t ahead;             // > 0 (multi-wave grids): L2-prefetch partition x + ahead's ranges
+    int64_t count;             // execution partitions of this launch
 };
+
+// L2 prefetch of the aligned body of [g, g + bytes)
+__device__ __forceinline__ void prefetch_region(const void *g, uint32_t bytes) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(g);
+    const uintptr_t lo = (a + 15) & ~uintptr_t(15), hi = (a + bytes) & ~uintptr_t(15);
+    if (hi > lo) ptx::bulk_prefetch_l2(reinterpret_cast<const void *>(lo), (uint32_t)(hi - lo));
+}
 
 template <class Fn, int BLOCK, int EPT, int VPT, int W>
 __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
@@ -102,6 +111,13 @@ __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
         const int j = tid + r * BLOCK;
         dtv[r] = (Fn::kUsesConst && j < d.nO) ? __ldg(a.vconst + d.o0 + j) : 0.0f;
     }
+    // multi-wave grids: the partition one resident wave ahead will need its contiguous ranges;
+    // its descriptor is loaded now (in flight during this CTA's copies) and the ranges are
+    // prefetched into L2 once this CTA's data has landed, so that CTA's first dependent DRAM
+    // trips become L2 hits
+    const bool ahead = a.ahead > 0 && tid == 32 && blockIdx.x + a.ahead < a.count;
+    PartDesc f{};
+    if (ahead) f = a.desc[a.first + blockIdx.x + a.ahead];
     ptx::pdl_wait();                               // state_in is final from here on
     // single-wave grids: every CTA of this grid is resident, so the finalise may launch now
     // and load its (static) records on SMs with room while the edge partitions run
@@ -136,6 +152,13 @@ __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
     EPG_TP(0, 1);
     ptx::mbar_wait(&bar, 0);
     EPG_TP(0, 2);
+    if (ahead) {   // L2 is the point of coherence: a prefetch never returns stale data
+        prefetch_region(a.blob + 16 * (int64_t)f.blob16, (uint32_t)f.blob_bytes);
+        prefetch_region(a.slots + f.e0, 4u * f.s);
+        if (a.payload) prefetch_region(a.payload + (int64_t)PW * f.e0, 4u * PW * f.s);
+        if (Fn::kUsesConst) prefetch_region(a.vconst + f.o0, 4u * f.nO);
+        prefetch_region(a.state_in + (int64_t)ROW * f.o0, 4u * ROW * f.nO);
+    }
     if (tid < 32) region_ragged(rows_base, g_rows, rows_bytes, tid);   // ragged ends of the owned range
     if (!early_halo) gather_halo(reinterpret_cast<const int32_t *>(sblob), false);
     ptx::cp_async_commit();
