@@ -757,6 +757,18 @@ epg_status launch_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t step
     return EPG_OK;
 }
 
+// Phi space of the occupancy kernel: the Phi records (Scap + 1, the last the zero sentinel),
+// which before the edge phase hold the bulk-staged slots, payload (PAYW floats per edge, if
+// any) and dt; returns its size and sets the staging offsets in *a.
+template <class Fn>
+int occ_phi_bytes(const epg_plan *pl, OccArgs *a) {
+    a->st_slots = 0;
+    a->st_pay = up16i(4 * pl->Scap + 32);
+    a->st_vc = a->st_pay + up16i(4 * Fn::PAYW * pl->Scap + 32);
+    const int stage = a->st_vc + (Fn::kUsesConst ? up16i(4 * pl->Ocap + 32) : 0);
+    return std::max(up16i(4 * Fn::PHIREC * (pl->Scap + 1)), stage);
+}
+
 // Instance of the occupancy kernel for a plan: EPT edges and VPT staged rows per thread
 // (256 threads), W the padded incidence width. `go` is called with the chosen instance.
 template <class Fn, class Go>
@@ -799,7 +811,7 @@ epg_status run_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, 
     a.rows_land = up16i(recs_bytes - (4 * Fn::ROW * pl->Lcap + 16) - 16);
     a.off_phi = a.off_recs + recs_bytes;
     a.sentinel = pl->Scap;
-    const size_t smem = (size_t)a.off_phi + up16i(4 * Fn::PHIREC * (pl->Scap + 1));
+    const size_t smem = (size_t)a.off_phi + occ_phi_bytes<Fn>(pl, &a);
     if (smem + 1024 > (size_t)dev_max) return EPG_OK;
     *fits = true;
     a.desc = pl->desc3;
@@ -827,7 +839,7 @@ epg_status run_edges_range(epg_ctx *ctx, epg_plan *pl, epg_state *state, int64_t
     a.rows_land = up16i(recs_bytes - (4 * Fn::ROW * pl->Lcap + 16) - 16);
     a.off_phi = a.off_recs + recs_bytes;
     a.sentinel = pl->Scap;
-    const size_t smem = (size_t)a.off_phi + up16i(4 * Fn::PHIREC * (pl->Scap + 1));
+    const size_t smem = (size_t)a.off_phi + occ_phi_bytes<Fn>(pl, &a);
     a.desc = pl->desc3;
     a.blob = pl->blob3;
     a.slots = pl->slots;

@@ -55,6 +55,9 @@ struct OccArgs {
     int sentinel;              // zero Phi record of padded incidence entries (plan Scap)
     int64_t ahead;             // > 0 (multi-wave grids): L2-prefetch partition x + ahead's ranges
     int64_t count;             // execution partitions of this launch
+    // the partition's endpoint slots, edge payload and dt are bulk-copied into the Phi space
+    // (dead until the edge phase) at these byte offsets from off_phi
+    int st_slots, st_pay, st_vc;
 };
 
 // L2 prefetch of the aligned body of [g, g + bytes)
@@ -82,34 +85,24 @@ __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
     const uint32_t rows_bytes = 4u * ROW * d.nO;
     // Programmatic dependent launch: everything up to pdl_wait() reads only plan data and
     // may overlap the previous kernel in the stream (the finalise of the previous step).
+    // static per-partition ranges (all contiguous after the remap), staged in the Phi space
+    const uint32_t *g_sl = a.slots + d.e0;
+    const float *g_pay = a.payload ? a.payload + (int64_t)PW * d.e0 : nullptr;
+    const float *g_vc = Fn::kUsesConst ? a.vconst + d.o0 : nullptr;
+    unsigned char *st_sl = occ_smem + a.off_phi + a.st_slots, *st_pay = occ_smem + a.off_phi + a.st_pay,
+                  *st_vc = occ_smem + a.off_phi + a.st_vc;
+    const uint32_t sl_bytes = 4u * d.s, pay_bytes = 4u * PW * d.s, vc_bytes = 4u * d.nO;
     if (tid == 0) {
         ptx::mbar_init(&bar, 1);
         ptx::fence_mbar_init();
-        ptx::mbar_arrive_expect_tx(&bar, (uint32_t)d.blob_bytes + region_body(g_rows, rows_bytes));
+        uint32_t tx = (uint32_t)d.blob_bytes + region_body(g_rows, rows_bytes) + region_body(g_sl, sl_bytes);
+        if (g_pay) tx += region_body(g_pay, pay_bytes);
+        if (g_vc) tx += region_body(g_vc, vc_bytes);
+        ptx::mbar_arrive_expect_tx(&bar, tx);
         if (d.blob_bytes) ptx::bulk_g2s(sblob, a.blob + 16 * (int64_t)d.blob16, (uint32_t)d.blob_bytes, &bar);
-    }
-    // register prefetch (plan + static payload) while the copies fly
-    uint32_t sl[EPT];
-    float pw[EPT][PW];
-#pragma unroll
-    for (int r = 0; r < EPT; r++) {
-        const int i = tid + r * BLOCK;
-        sl[r] = 0;
-#pragma unroll
-        for (int c = 0; c < PW; c++) pw[r][c] = i < d.s ? 1.0f : 0.0f;
-        if (i < d.s) {
-            sl[r] = __ldg(a.slots + d.e0 + i);
-            if (a.payload) {
-#pragma unroll
-                for (int c = 0; c < PW; c++) pw[r][c] = __ldg(a.payload + (int64_t)PW * (d.e0 + i) + c);
-            }
-        }
-    }
-    float dtv[VPT];
-#pragma unroll
-    for (int r = 0; r < VPT; r++) {
-        const int j = tid + r * BLOCK;
-        dtv[r] = (Fn::kUsesConst && j < d.nO) ? __ldg(a.vconst + d.o0 + j) : 0.0f;
+        region_bulk(st_sl, g_sl, sl_bytes, &bar);
+        if (g_pay) region_bulk(st_pay, g_pay, pay_bytes, &bar);
+        if (g_vc) region_bulk(st_vc, g_vc, vc_bytes, &bar);
     }
     // multi-wave grids: the partition one resident wave ahead will need its contiguous ranges;
     // its descriptor is loaded now (in flight during this CTA's copies) and the ranges are
@@ -160,11 +153,37 @@ __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
         prefetch_region(a.state_in + (int64_t)ROW * f.o0, 4u * ROW * f.nO);
     }
     if (tid < 32) region_ragged(rows_base, g_rows, rows_bytes, tid);   // ragged ends of the owned range
+    else if (tid < 64) region_ragged(st_sl, g_sl, sl_bytes, tid - 32);   // ... and of the staged ranges
+    else if (tid < 96) { if (g_pay) region_ragged(st_pay, g_pay, pay_bytes, tid - 64); }
+    else if (tid < 128) { if (g_vc) region_ragged(st_vc, g_vc, vc_bytes, tid - 96); }
     if (!early_halo) gather_halo(reinterpret_cast<const int32_t *>(sblob), false);
     ptx::cp_async_commit();
     ptx::cp_async_wait<0>();
     __syncthreads();
     EPG_TP(0, 3);
+    // staged slots / payload / dt -> registers (the Phi space is overwritten by the edge phase)
+    uint32_t sl[EPT];
+    float pw[EPT][PW];
+    {
+        const uint32_t *s_sl = reinterpret_cast<const uint32_t *>(st_sl + (reinterpret_cast<uintptr_t>(g_sl) & 15));
+        const float *s_pay = reinterpret_cast<const float *>(st_pay + (reinterpret_cast<uintptr_t>(g_pay) & 15));
+#pragma unroll
+        for (int r = 0; r < EPT; r++) {
+            const int i = tid + r * BLOCK;
+            sl[r] = i < d.s ? s_sl[i] : 0u;
+#pragma unroll
+            for (int c = 0; c < PW; c++) pw[r][c] = i < d.s ? (g_pay ? s_pay[PW * i + c] : 1.0f) : 0.0f;
+        }
+    }
+    float dtv[VPT];
+    {
+        const float *s_vc = reinterpret_cast<const float *>(st_vc + (reinterpret_cast<uintptr_t>(g_vc) & 15));
+#pragma unroll
+        for (int r = 0; r < VPT; r++) {
+            const int j = tid + r * BLOCK;
+            dtv[r] = (g_vc && j < d.nO) ? s_vc[j] : 0.0f;
+        }
+    }
     // rows -> registers -> derived records (in place: the rows sit in the upper part)
     float rv[VPT][ROW];
 #pragma unroll
