@@ -757,15 +757,31 @@ epg_status launch_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t step
     return EPG_OK;
 }
 
+// EPT / VPT that occ_dispatch picks for a plan
+inline int occ_ept(const epg_plan *pl) {
+    if (pl->Scap <= 2 * kOccThreads && pl->Lcap <= 2 * kOccThreads) return 2;
+    return pl->Scap > 4 * kOccThreads ? 5 : 4;
+}
+template <class Fn>
+int occ_vpt(const epg_plan *pl) {
+    const int L = pl->Lcap;
+    if (pl->Scap <= 2 * kOccThreads && L <= 2 * kOccThreads) return 2;
+    if (Fn::ROW == 1 && L > 4 * kOccThreads) return 8;
+    if (L > 4 * kOccThreads) return 5;
+    return L > 3 * kOccThreads ? 4 : 3;
+}
+
 // Phi space of the occupancy kernel: the Phi records (Scap + 1, the last the zero sentinel),
 // which before the edge phase hold the bulk-staged slots, payload (PAYW floats per edge, if
 // any) and dt; returns its size and sets the staging offsets in *a.
 template <class Fn>
 int occ_phi_bytes(const epg_plan *pl, OccArgs *a) {
+    // every thread reads EPT x 256 edge entries and VPT x 256 dt entries unpredicated
+    const int se = std::max(pl->Scap, occ_ept(pl) * kOccThreads), sv = std::max(pl->Ocap, occ_vpt<Fn>(pl) * kOccThreads);
     a->st_slots = 0;
-    a->st_pay = up16i(4 * pl->Scap + 32);
-    a->st_vc = a->st_pay + up16i(4 * Fn::PAYW * pl->Scap + 32);
-    const int stage = a->st_vc + (Fn::kUsesConst ? up16i(4 * pl->Ocap + 32) : 0);
+    a->st_pay = up16i(4 * se + 32);
+    a->st_vc = a->st_pay + up16i(4 * Fn::PAYW * se + 32);
+    const int stage = a->st_vc + (Fn::kUsesConst ? up16i(4 * sv + 32) : 0);
     return std::max(up16i(4 * Fn::PHIREC * (pl->Scap + 1)), stage);
 }
 

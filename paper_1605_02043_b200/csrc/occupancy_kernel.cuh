@@ -162,27 +162,32 @@ __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
     __syncthreads();
     EPG_TP(0, 3);
     // staged slots / payload / dt -> registers (the Phi space is overwritten by the edge phase)
+    // (unpredicated: the staging areas hold EPT x BLOCK edges and VPT x BLOCK rows, and the
+    // values past s / nO are never used)
     uint32_t sl[EPT];
     float pw[EPT][PW];
     {
         const uint32_t *s_sl = reinterpret_cast<const uint32_t *>(st_sl + (reinterpret_cast<uintptr_t>(g_sl) & 15));
         const float *s_pay = reinterpret_cast<const float *>(st_pay + (reinterpret_cast<uintptr_t>(g_pay) & 15));
 #pragma unroll
-        for (int r = 0; r < EPT; r++) {
-            const int i = tid + r * BLOCK;
-            sl[r] = i < d.s ? s_sl[i] : 0u;
+        for (int r = 0; r < EPT; r++) sl[r] = s_sl[tid + r * BLOCK];
+        if (g_pay) {
 #pragma unroll
-            for (int c = 0; c < PW; c++) pw[r][c] = i < d.s ? (g_pay ? s_pay[PW * i + c] : 1.0f) : 0.0f;
+            for (int r = 0; r < EPT; r++)
+#pragma unroll
+                for (int c = 0; c < PW; c++) pw[r][c] = s_pay[PW * (tid + r * BLOCK) + c];
+        } else {
+#pragma unroll
+            for (int r = 0; r < EPT; r++)
+#pragma unroll
+                for (int c = 0; c < PW; c++) pw[r][c] = 1.0f;
         }
     }
     float dtv[VPT];
     {
         const float *s_vc = reinterpret_cast<const float *>(st_vc + (reinterpret_cast<uintptr_t>(g_vc) & 15));
 #pragma unroll
-        for (int r = 0; r < VPT; r++) {
-            const int j = tid + r * BLOCK;
-            dtv[r] = (g_vc && j < d.nO) ? s_vc[j] : 0.0f;
-        }
+        for (int r = 0; r < VPT; r++) dtv[r] = Fn::kUsesConst ? s_vc[tid + r * BLOCK] : 0.0f;
     }
     // rows -> registers -> derived records (in place: the rows sit in the upper part)
     float rv[VPT][ROW];
