@@ -348,6 +348,7 @@ __global__ void k_finalise3(const int32_t *__restrict__ shared_ids, const int32_
         }
         const float dt = Fn::kUsesConst ? vconst[v] : 0.0f;
         Fn::finalise_add(state_out + Fn::ROW * v, acc, dt);
+        EPG_TP(14, 2);
         return;
     }
     const int64_t v = touched + (t - S);
@@ -516,6 +517,7 @@ __global__ void k_finalise_rec(const int4 *__restrict__ recs, const float *__res
                                const float *__restrict__ state_in, float *__restrict__ state_out,
                                const float *__restrict__ vconst, int32_t S, int64_t touched, int64_t n) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    EPG_TP(14, 0);
     // the records and dt are plan / constant data: loaded before the wait, i.e. while the
     // edge kernel still runs (it triggers this launch as soon as all of its CTAs started)
     int4 r0 = make_int4(0, -1, 0, 0), r1 = make_int4(0, 0, 0, 0);
@@ -526,6 +528,7 @@ __global__ void k_finalise_rec(const int4 *__restrict__ recs, const float *__res
         if (Fn::kUsesConst && r0.y >= 0) dt = vconst[r0.x];
     }
     ptx::pdl_wait();
+    EPG_TP(14, 1);
     ptx::pdl_launch_dependents();
     if (t < S) {
         const int64_t v = r0.x;

@@ -54,6 +54,7 @@ def main():
     ctx = epg.Context(0)
     E = torch.from_numpy(M.edges).cuda()
     k = epg.num_parts(M.m, a.part_size)
+    ctx.set_partition_method(epg.PARTITION_EPG2)
     part, _ = ctx.partition(E, M.n, a.part_size)
     L, plan = ctx.remap(E, M.n, part, k)
     nrm = ctx.permute_rows(torch.from_numpy(M.normals).cuda(), L.edge_perm, epg.PERM_GATHER)
@@ -73,6 +74,7 @@ def main():
         torch.cuda.synchronize()
         buf = np.zeros(1024 * niters * npts, dtype=np.uint64)
         epg.lib.epg_debug_trace(buf.ctypes.data, buf.size)
+        buf = buf.astype(np.uint64)
         t = buf.reshape(1024, niters, npts)[:nblk, 0, :].astype(np.int64)
         epg.lib.epg_debug_trace_clear()
         base = t[:, 0][t[:, 0] > 0].min()
@@ -85,6 +87,15 @@ def main():
             d = (col - base) / 1e3
             print(f"  pt{pt}: n={col.size:4d}  min {d.min():7.2f}  p10 {np.percentile(d, 10):7.2f}  "
                   f"p50 {np.percentile(d, 50):7.2f}  p90 {np.percentile(d, 90):7.2f}  max {d.max():7.2f} us")
+        fin = buf.reshape(1024, niters, npts)[:, 14, :3].astype(np.int64)
+        fin = fin[fin[:, 0] > 0]
+        if fin.size:
+            for pt, name in enumerate(["finalise CTA start", "finalise wait released", "finalise CTA done"]):
+                col = fin[:, pt][fin[:, pt] > 0]
+                if col.size:
+                    d = (col - base) / 1e3
+                    print(f"  {name:24s} n={col.size:4d} min {d.min():7.2f} p50 {np.percentile(d, 50):7.2f} "
+                          f"max {d.max():7.2f} us")
         for pa, pb in [(0, 2), (2, 3), (3, 4), (4, 5), (5, 6), (6, 7), (0, 6), (0, 7)]:
             ok = (t[:, pa] > 0) & (t[:, pb] > 0)
             dd = (t[ok, pb] - t[ok, pa]) / 1e3
