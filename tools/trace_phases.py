@@ -68,8 +68,9 @@ def main():
     runs = [(v, rep) for v in map(int, a.variants.split(",")) for rep in range(a.reps)]
     for v, rep in runs:
         ctx.set_variant(v)
-        flush.fill_(rep & 255)
         torch.cuda.synchronize()
+        torch.cuda._sleep(2_000_000)               # keep the GPU busy while the host enqueues
+        flush.fill_(rep & 255)
         ctx.run(plan, epg.KERNEL_CFD_FLUX, Un, out, nrm, dtn, 1)
         torch.cuda.synchronize()
         buf = np.zeros(1024 * niters * npts, dtype=np.uint64)
