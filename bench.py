@@ -315,11 +315,9 @@ def run_sharded(args, rank, local_rank, world):
     L, plan = ctx.remap(E, M.n, part, k, halo_cap=rep.cut_cost)
     sh = Shard(ctx, plan, L, epg.KERNEL_CFD_FLUX, world, rank)
     comm = Comm()
-    Ud = torch.from_numpy(M.state).to(dev)
-    pay0 = None if M.payload is None else torch.from_numpy(M.payload).to(dev)
-    vc0 = None if M.vconst is None else torch.from_numpy(M.vconst).to(dev)
-    nrm = None if pay0 is None else ctx.permute_rows(pay0, L.edge_perm, epg.PERM_GATHER)
-    dtn = None if vc0 is None else ctx.permute_rows(vc0, L.vertex_perm, epg.PERM_SCATTER)
+    Ud = torch.from_numpy(U).to(dev)
+    nrm = ctx.permute_rows(torch.from_numpy(M.normals).to(dev), L.edge_perm, epg.PERM_GATHER)
+    dtn = ctx.permute_rows(torch.from_numpy(dt).to(dev), L.vertex_perm, epg.PERM_SCATTER)
     bufs = [ctx.permute_rows(Ud, L.vertex_perm, epg.PERM_SCATTER), torch.empty_like(Ud)]
     flushbuf = torch.empty(args.flush_mib * (1 << 20) // 4, dtype=torch.float32, device=dev)
 
