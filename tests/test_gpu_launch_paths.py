@@ -1,0 +1,99 @@
+"""GPU: the launch-path features of epg_run (include/epg.h) must not change results.
+
+* multi-wave grids (more execution partitions than resident CTAs) bulk-prefetch the next
+  wave's ranges into L2 (EPG_PREFETCH_AHEAD) -- bit-identical to no prefetch, and within
+  the Z14 tolerance of the fp64 oracle;
+* the occupancy path replays a cached CUDA graph per (plan, kernel, buffers, steps)
+  (EPG_GRAPHS) -- bit-identical to direct launches, for several buffer pairs and step
+  counts reusing the cache, including after the cache is evicted (> 16 entries)."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import synth as S
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _prep(M, P, method=2):
+    from paper_1605_02043_b200 import epg
+    ctx = epg.Context(0)
+    ctx.set_partition_method(method)
+    part, _ = ctx.partition(dev(M.edges), M.n, P)
+    L, plan = ctx.remap(dev(M.edges), M.n, part, epg.num_parts(M.m, P))
+    U, dt = S.cfd_state(M.n), S.cfd_dt(M.volume)
+    Un = ctx.permute_rows(dev(U), L.vertex_perm, epg.PERM_SCATTER)
+    nrm = ctx.permute_rows(dev(M.normals), L.edge_perm, epg.PERM_GATHER)
+    dtn = ctx.permute_rows(dev(dt), L.vertex_perm, epg.PERM_SCATTER)
+    return ctx, L, plan, U, dt, Un, nrm, dtn
+
+
+def _env(name, value):
+    old = os.environ.get(name)
+    if value is None:
+        os.environ.pop(name, None)
+    else:
+        os.environ[name] = value
+    return old
+
+
+def test_multiwave_prefetch_bitexact_and_oracle():
+    from paper_1605_02043_b200 import epg
+    M = S.config_mesh("c1")
+    ctx, L, plan, U, dt, Un, nrm, dtn = _prep(M, 32)
+    assert plan.k_exec > 148 * 4                   # more partitions than one resident wave
+    outs = {}
+    for ahead in ("0", None):                      # prefetch off, then the default (one wave ahead)
+        old = _env("EPG_PREFETCH_AHEAD", ahead)
+        try:
+            o = torch.empty_like(Un)
+            ctx.run(plan, epg.KERNEL_CFD_FLUX, Un, o, nrm, dtn, 1)
+            outs[ahead] = o.cpu().numpy()
+        finally:
+            _env("EPG_PREFETCH_AHEAD", old)
+    assert np.array_equal(outs["0"], outs[None])
+    got = np.empty_like(outs[None])
+    got[:] = outs[None][L.vertex_perm.cpu().numpy()]   # back to the original vertex order
+    ref, _ = O.cfd_step(M.edges, M.n, M.normals, U, dt)
+    err = np.abs(got - ref).max(axis=0) / np.abs(ref).max(axis=0)
+    assert err.max() <= 1e-5
+
+
+def test_graph_replay_bitexact():
+    from paper_1605_02043_b200 import epg
+    M = S.kuhn_mesh(nbox=12, n_keep=9000)
+    ctx, L, plan, U, dt, Un, nrm, dtn = _prep(M, 256)
+    pairs = [(Un.clone(), torch.empty_like(Un)) for _ in range(3)]
+
+    def sweep():
+        res = []
+        for rep in range(7):                       # 3 buffer pairs x 3 step counts: 9 cache keys
+            for j, (a, b) in enumerate(pairs):
+                for steps in (1, 2, 3):
+                    a.copy_(Un)
+                    out = ctx.run(plan, epg.KERNEL_CFD_FLUX, a, b, nrm, dtn, steps)
+                    res.append(out.cpu().numpy())
+        return res
+
+    old = _env("EPG_GRAPHS", "0")
+    try:
+        direct = sweep()
+    finally:
+        _env("EPG_GRAPHS", old)
+    graphed = sweep()
+    for x, y in zip(direct, graphed):
+        assert np.array_equal(x, y)
+    # more than 16 keys: the cache is evicted and rebuilt, results unchanged
+    extra = [(Un.clone(), torch.empty_like(Un)) for _ in range(8)]
+    for a, b in extra:
+        for steps in (1, 2):
+            a.copy_(Un)
+            out = ctx.run(plan, epg.KERNEL_CFD_FLUX, a, b, nrm, dtn, steps)
+            assert np.array_equal(out.cpu().numpy(), graphed[steps - 1])
