@@ -139,7 +139,7 @@ def ncu_evidence(config: str):
     """DRAM traffic of the dominant kernel and per-schedule bytes/edge from the committed
     ncu summaries (tools/profile_round.sh + tools/summarize_ncu.py), when present."""
     traffic, src, variants = None, None, None
-    p = os.path.join(ROOT, "profiles", "traffic.json")
+    p = os.path.join(ROOT, "profiles", f"traffic_{config}.json")
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)

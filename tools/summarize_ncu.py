@@ -151,7 +151,7 @@ def main():
             traffic = rb + wb
         except (KeyError, IndexError, ValueError):
             pass
-        with open(os.path.join(ROOT, "profiles", "traffic.json"), "w") as f:
+        with open(os.path.join(ROOT, "profiles", f"traffic_{a.config}.json"), "w") as f:
             json.dump({"config": a.config, "round": a.round, "kernel": "k_edge_occ<CfdFlux>",
                        "dram_bytes_per_launch": traffic,
                        "source": f"profiles/{a.round}_{a.config}_full.txt (ncu --set full, one cold launch)"}, f,
