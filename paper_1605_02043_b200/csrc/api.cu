@@ -786,7 +786,8 @@ int occ_phi_bytes(const epg_plan *pl, OccArgs *a) {
     a->st_pay = up16i(4 * se + 32);
     a->st_vc = a->st_pay + up16i(4 * Fn::PAYW * se + 32);
     const int stage = a->st_vc + (Fn::kUsesConst ? up16i(4 * sv + 32) : 0);
-    return std::max(up16i(4 * Fn::PHIREC * (pl->Scap + 1)), stage);
+    a->pstride = (pl->Scap + 1 + 3) & ~3;
+    return std::max(up16i(Fn::PHIBYTES * a->pstride), stage);
 }
 
 // Instance of the occupancy kernel for a plan: EPT edges and VPT staged rows per thread

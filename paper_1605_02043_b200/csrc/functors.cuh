@@ -183,6 +183,29 @@ struct CfdFlux {
 #pragma unroll
         for (int c = 0; c < 5; c++) out[c] = fmaf(dt, acc[c], out[c]);
     }
+    // split Phi layout of the occupancy kernel: a float4 array (Phi_0..3) and, `stride`
+    // records further, a float array (Phi_4) -- 20 B per edge, conflict-free stores and
+    // one 128-bit + one 32-bit shared load per incidence entry instead of three 64-bit
+    static constexpr int PHIBYTES = 20;
+    __device__ __forceinline__ static void edge_split(const float *recs, int a, int b, const float pw[3], int i,
+                                                      float *phis, int stride) {
+        float phi[5];
+        cfd_phi(load_rec(recs, a), load_rec(recs, b), pw[0], pw[1], pw[2], phi);
+        reinterpret_cast<float4 *>(phis)[i] = make_float4(phi[0], phi[1], phi[2], phi[3]);
+        phis[4 * stride + i] = phi[4];
+    }
+    __device__ __forceinline__ static void zero_split(float *phis, int i, int stride) {
+        reinterpret_cast<float4 *>(phis)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        phis[4 * stride + i] = 0.f;
+    }
+    __device__ __forceinline__ static void gather_split(const float *phis, int i, int side, float acc[5],
+                                                        int stride) {
+        const float4 x = reinterpret_cast<const float4 *>(phis)[i];
+        const float y = phis[4 * stride + i];
+        const float sgn = side ? -1.0f : 1.0f;
+        acc[0] = fmaf(sgn, x.x, acc[0]); acc[1] = fmaf(sgn, x.y, acc[1]); acc[2] = fmaf(sgn, x.z, acc[2]);
+        acc[3] = fmaf(sgn, x.w, acc[3]); acc[4] = fmaf(sgn, y, acc[4]);
+    }
     static constexpr bool kUsesConst = true;
 };
 
@@ -234,6 +257,13 @@ struct GatherScatter {
     __device__ __forceinline__ static void finalise_add(float *__restrict__ out, const float acc[1], float) {
         out[0] += acc[0];
     }
+    static constexpr int PHIBYTES = 8;   // same layout as the records above (stride unused)
+    __device__ __forceinline__ static void edge_split(const float *recs, int a, int b, const float pw[1], int i,
+                                                      float *phis, int) { edge_rec_pw(recs, a, b, pw, i, phis); }
+    __device__ __forceinline__ static void zero_split(float *phis, int i, int) { zero_phi(phis, i); }
+    __device__ __forceinline__ static void gather_split(const float *phis, int i, int side, float acc[1], int) {
+        gather_rec(phis, i, side, acc);
+    }
     static constexpr bool kUsesConst = false;
 };
 
@@ -277,6 +307,13 @@ struct Spmv {
     }
     __device__ __forceinline__ static void finalise_add(float *__restrict__ out, const float acc[1], float) {
         out[0] += acc[0];
+    }
+    static constexpr int PHIBYTES = 4;
+    __device__ __forceinline__ static void edge_split(const float *recs, int a, int b, const float pw[1], int i,
+                                                      float *phis, int) { edge_rec_pw(recs, a, b, pw, i, phis); }
+    __device__ __forceinline__ static void zero_split(float *phis, int i, int) { zero_phi(phis, i); }
+    __device__ __forceinline__ static void gather_split(const float *phis, int i, int side, float acc[1], int) {
+        gather_rec(phis, i, side, acc);
     }
     static constexpr bool kUsesConst = false;
 };

@@ -53,6 +53,7 @@ struct OccArgs {
     float *hub_acc;            // [hubs][ROW] or NULL: hub partials are added here as well
     int early_pdl;             // 1: trigger dependents at the start (single-wave grids)
     int sentinel;              // zero Phi record of padded incidence entries (plan Scap)
+    int pstride;               // records of the split Phi layout (>= sentinel + 1, multiple of 4)
     int64_t ahead;             // > 0 (multi-wave grids): L2-prefetch partition x + ahead's ranges
     int64_t count;             // execution partitions of this launch
     // the partition's endpoint slots, edge payload and dt are bulk-copied into the Phi space
@@ -210,10 +211,10 @@ __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
 #pragma unroll
     for (int r = 0; r < EPT; r++) {
         const int i = tid + r * BLOCK;
-        if (i < d.s) Fn::edge_rec_pw(recs, (int)(sl[r] & 0xffffu), (int)(sl[r] >> 16), pw[r], i, phis);
+        if (i < d.s) Fn::edge_split(recs, (int)(sl[r] & 0xffffu), (int)(sl[r] >> 16), pw[r], i, phis, a.pstride);
     }
     if constexpr (W > 0) {
-        if (tid == 0) Fn::zero_phi(phis, a.sentinel);
+        if (tid == 0) Fn::zero_split(phis, a.sentinel, a.pstride);
     }
     __syncthreads();
     EPG_TP(0, 4);
@@ -239,14 +240,14 @@ __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
 #pragma unroll
             for (int q = 0; q < W; q++) {
                 const uint32_t w = (w2[q >> 1] >> (16 * (q & 1))) & 0xffffu;
-                Fn::gather_rec(phis, (int)(w >> 1), (int)(w & 1), acc);
+                Fn::gather_split(phis, (int)(w >> 1), (int)(w & 1), acc, a.pstride);
             }
         } else {
             const uint16_t *ioff = inc + 2 * d.s;
             const int q0 = ioff[j], q1 = j + 1 < L ? ioff[j + 1] : 2 * d.s;
             for (int q = q0; q < q1; q++) {
                 const int w = inc[q];
-                Fn::gather_rec(phis, w >> 1, w & 1, acc);
+                Fn::gather_split(phis, w >> 1, w & 1, acc, a.pstride);
             }
         }
         if (j < d.nO) {
