@@ -33,7 +33,8 @@
  *  - Threads: one ctx per host thread; a ctx is not thread-safe.
  *  - Errors: every call returns an epg_status; the message of the last failure is
  *    epg_last_error(ctx). On error no output is guaranteed to be written.
- *      EPG_ERR_INPUT      m <= 0, n <= 0, an endpoint outside [0, n) (the message
+ *      EPG_ERR_INPUT      m <= 0 (m >= 2^30 for the device layout calls epg_load_count,
+ *                         epg_remap and epg_partition), n <= 0, an endpoint outside [0, n) (the message
  *                         names the first offending edge id), a partition id outside
  *                         [0, k), a too-small output capacity, NULL required pointer.
  *      EPG_ERR_INFEASIBLE part_size outside [1, 4096]; shards not in {1,2,4,8} or

@@ -194,11 +194,17 @@ epg_status apply_ep(epg_adaptive *ad) {
                               ad->vertex_perm, 1)))
         return s;
     ad->cur ^= 1;
-    // first run of the transformed kernel, timed
+    // first run of the transformed kernel, timed. An untimed run of the same step comes
+    // first (its output is overwritten by the timed one): it loads the kernel module and
+    // captures epg_run's CUDA graph, one-off host work that the GPU would otherwise sit
+    // idle through inside the timed window (and that the original kernel, already warm,
+    // never pays) -- the comparison of P:778-779 is between kernel runtimes.
+    epg_state st = make_state(ad, true);
+    if ((s = epg_run(ad->ctx, ad->plan, ad->kernel, &st, 1))) return s;
+    ACU(cudaStreamSynchronize(ad->stream));
     cudaEvent_t a, b;
     ACU(cudaEventCreate(&a));
     ACU(cudaEventCreate(&b));
-    epg_state st = make_state(ad, true);
     ACU(cudaEventRecord(a, ad->stream));
     s = epg_run(ad->ctx, ad->plan, ad->kernel, &st, 1);
     cudaEventRecord(b, ad->stream);

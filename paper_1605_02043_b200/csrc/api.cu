@@ -118,14 +118,16 @@ struct epg_plan {
     std::vector<int32_t> shared_h;                // host copy of shared_ids (lazy, for shard ranges)
     int assign_grid = 0;                          // grid size the assignment was built for
     unsigned long long *bar_ctr = nullptr;        // grid barrier counter (monotone)
-    unsigned long long bar_gen = 0;               // launches so far
+    unsigned long long bar_sum = 0;               // CTAs that have arrived at the counter so far
+                                                  // (cumulative over launches of any grid size)
     int32_t *cta_begin = nullptr, *cta_list = nullptr;
     std::map<const void *, int64_t> resident_ctas;   // per edge-kernel instance: SMs x occupancy
     // epg_run's CUDA graphs: one per (kernel, buffers, steps, variant)
-    std::map<std::vector<uintptr_t>, cudaGraphExec_t> graphs;
+    std::map<std::vector<uintptr_t>, cudaGraphExec_t> graphs;   // nullptr: key not capturable
     std::vector<void *> allocs;
     ~epg_plan() {
-        for (auto &g : graphs) cudaGraphExecDestroy(g.second);
+        for (auto &g : graphs)
+            if (g.second) cudaGraphExecDestroy(g.second);
         for (void *p : allocs) cudaFree(p);
     }
 };
@@ -138,6 +140,7 @@ constexpr int kThreads = 256;
 constexpr int kHeavyHalo = 8;      // halo entries above which a shared vertex leaves the thread path
 constexpr int kBlockHalo = 1024;   // ... and above which a whole CTA (not a warp) finalises it
 constexpr int kHubMinDefault = 7;  // hub split default: >= 7 halo entries (the rest fit k_finalise_rec)
+constexpr int64_t kMaxEdges = int64_t(1) << 30;   // device layout: slot keys 2m + 1 fit int32
 
 int hub_min_for(const epg_ctx *ctx) {
     if (ctx->hub_min >= 0) return ctx->hub_min;
@@ -341,6 +344,8 @@ epg_status read_i32(epg_ctx *ctx, const int32_t *dev, int32_t *host) {
 // cost function on device edges / part: report + optional per-partition counts
 epg_status load_count_dev(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, const int32_t *part, int64_t k,
                           int32_t *per_part_out, epg_report *rep) {
+    if (m >= kMaxEdges)   // endpoint slots 2e + s and the scan / sort sizes are int32
+        return ctx->fail(EPG_ERR_INPUT, "load_count: m must be below 2^30");
     epg_status st = validate(ctx, edges, m, n, part, k);
     if (st) return st;
     Tmp perm(ctx), peb(ctx), distinct(ctx), flag(ctx);
@@ -623,8 +628,10 @@ epg_status launch_pipelined(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_
     for (int32_t s = 0; s < steps; s++) {
         a.state_in = bufs[s & 1];
         a.state_out = bufs[(s + 1) & 1];
-        pl->bar_gen += 1;
-        a.bar_target = pl->bar_gen * (unsigned long long)grid;
+        // the counter is monotone across every launch on this plan, whatever its grid (the
+        // grid depends on the functor and on the payload): the target is the running total
+        pl->bar_sum += (unsigned long long)grid;
+        a.bar_target = pl->bar_sum;
         cudaEvent_t t0 = ctx->prof_begin();
         kern<<<(unsigned)grid, kPipeThreads, smem, ctx->stream>>>(a);
         ctx->prof_end(0, t0);
@@ -1029,7 +1036,8 @@ epg_status run_graphed(epg_ctx *ctx, epg_plan *pl, epg_kernel kernel, epg_state 
     auto it = pl->graphs.find(key);
     if (it == pl->graphs.end()) {
         if (pl->graphs.size() >= 16) {   // bounded cache
-            for (auto &g : pl->graphs) cudaGraphExecDestroy(g.second);
+            for (auto &g : pl->graphs)
+                if (g.second) cudaGraphExecDestroy(g.second);
             pl->graphs.clear();
         }
         if (!ctx->cap_stream) CU(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
@@ -1050,10 +1058,12 @@ epg_status run_graphed(epg_ctx *ctx, epg_plan *pl, epg_kernel kernel, epg_state 
         if (e != cudaSuccess || st != EPG_OK || !ex) {   // not capturable here: launch directly
             cudaGetLastError();
             if (ex) cudaGraphExecDestroy(ex);
+            pl->graphs.emplace(key, nullptr);              // and do not try to capture this key again
             return run_staged<Fn>(ctx, pl, state, steps);
         }
         it = pl->graphs.emplace(key, ex).first;
     }
+    if (!it->second) return run_staged<Fn>(ctx, pl, state, steps);
     CU(cudaGraphLaunch(it->second, ctx->stream));
     return EPG_OK;
 }
@@ -1168,6 +1178,8 @@ epg_status remap_impl(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, 
                       epg_layout *L, epg_plan **plan_out) {
     if (!edges || !part || !L || !plan_out || m <= 0 || n <= 0 || k <= 0)
         return ctx->fail(EPG_ERR_INPUT, "remap: need m > 0, n > 0, k > 0 and non-NULL arrays");
+    if (m >= kMaxEdges)   // first-touch keys 2e' + s and the scan / sort sizes are int32
+        return ctx->fail(EPG_ERR_INPUT, "remap: m must be below 2^30");
     if (!L->edge_perm || !L->part_edge_begin || !L->vertex_perm || !L->part_vertex_begin || !L->halo_begin ||
         !L->slots || (!L->halo_ids && L->halo_cap > 0))
         return ctx->fail(EPG_ERR_INPUT, "remap: every layout array is required");

@@ -97,3 +97,38 @@ def test_graph_replay_bitexact():
             a.copy_(Un)
             out = ctx.run(plan, epg.KERNEL_CFD_FLUX, a, b, nrm, dtn, steps)
             assert np.array_equal(out.cpu().numpy(), graphed[steps - 1])
+
+
+@pytest.mark.timeout(300, method="thread")
+def test_pipelined_variant_one_plan_two_grids():
+    """the persistent pipelined kernel (variant 2) synchronises its CTAs on a
+    per-plan monotone counter. Its grid (SMs x occupancy) depends on the functor's shared
+    memory, so one plan run alternately with the cfd functor and with gather-scatter
+    launches different grids in turn; the barrier target must follow the cumulative
+    arrivals (no deadlock, no early release -- both results stay correct)."""
+    from paper_1605_02043_b200 import epg
+    M = S.config_mesh("c1")
+    P = 64
+    ctx = epg.Context(0)
+    ctx.set_variant(2)
+    ctx.set_partition_method(2)
+    E = dev(M.edges)
+    part, _ = ctx.partition(E, M.n, P)
+    L, plan = ctx.remap(E, M.n, part, epg.num_parts(M.m, P))
+    U, dt = S.cfd_state(M.n), S.cfd_dt(M.volume)
+    Un = ctx.permute_rows(dev(U), L.vertex_perm, epg.PERM_SCATTER)
+    nrm = ctx.permute_rows(dev(M.normals), L.edge_perm, epg.PERM_GATHER)
+    dtn = ctx.permute_rows(dev(dt), L.vertex_perm, epg.PERM_SCATTER)
+    ref_cfd, _ = O.cfd_step(M.edges, M.n, M.normals, U, dt)
+    x = S.int_vector(5, M.n, 0, 7)
+    ref_gs = O.gather_scatter(M.edges, M.n, x)
+    xn = ctx.permute_rows(dev(x), L.vertex_perm, epg.PERM_SCATTER)
+    for rep in range(3):
+        o = torch.empty_like(Un)
+        ctx.run(plan, epg.KERNEL_CFD_FLUX, Un, o, nrm, dtn, 1)
+        got = ctx.permute_rows(o, L.vertex_perm, epg.PERM_GATHER).cpu().numpy()
+        assert (np.abs(got - ref_cfd).max(axis=0) / np.abs(ref_cfd).max(axis=0)).max() <= 1e-5
+        y = torch.empty_like(xn)
+        ctx.run(plan, epg.KERNEL_GATHER_SCATTER, xn, y, None, None, 1)
+        got = ctx.permute_rows(y, L.vertex_perm, epg.PERM_GATHER).cpu().numpy()
+        assert np.array_equal(got.astype(np.float64), ref_gs)

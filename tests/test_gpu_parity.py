@@ -232,15 +232,14 @@ def test_cfd_multi_step_and_determinism(ctx, small_mesh):
     assert normwise_err(s2, ref2).max() <= TOL
 
 
-def test_pipelined_kernel_at_bench_config(ctx):
-    """The bench configuration (C2, P = 1024) runs the pipelined kernel (variant 2 refuses
-    to fall back) and matches the oracle at full size."""
+def test_occupancy_kernel_at_bench_config(ctx):
+    """The bench configuration (C2, P = 1024) runs the occupancy TMA kernel (variant 3,
+    which refuses to fall back to another variant) and matches the oracle at full size."""
     from paper_1605_02043_b200 import epg
     M = S.config_mesh("c2")
     k = O.num_parts(M.m, 1024)
     c2 = epg.Context(0)
-    c2.set_variant(ctx_variant := 3)
-    assert ctx_variant == 3
+    c2.set_variant(3)
     U, dt = _cfd_inputs(M)
     got = _run_cfd(c2, M, O.partition(M.edges, M.n, 1024), k, U, dt)
     ref, _ = O.cfd_step(M.edges, M.n, M.normals, U, dt)

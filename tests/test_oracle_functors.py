@@ -28,6 +28,76 @@ def test_pressure_force_at_rest():
     assert np.allclose(F[1], -F[0], atol=1e-15)
 
 
+def _one_face(Ua, Ub, n):
+    e = np.array([[0, 1]], np.int32)
+    U = np.array([Ua, Ub], np.float32)
+    return O.cfd_flux(e, 2, np.array([n], np.float32), U)
+
+
+def test_uniform_flow_along_normal_is_textbook_euler_flux():
+    """A uniform state (U_a = U_b, so the dissipation f (U_a - U_b) vanishes) moving along
+    the face normal: Phi = -n.(G(U) + G(U))/2 = -n.G(U), the textbook Euler flux.
+    rho = 1, u = (0.3, 0, 0), p = 1, gamma = 1.4:
+      E = p/(gamma-1) + rho|u|^2/2 = 2.5 + 0.045 = 2.545,  m = rho u = (0.3, 0, 0);
+      n = (1, 0, 0):  G.n = (rho u_x, rho u_x^2 + p, 0, 0, u_x (E + p))
+                          = (0.3, 0.09 + 1 = 1.09, 0, 0, 0.3 * 3.545 = 1.0635).
+    F_a = -G.n (the flux leaves a through n), F_b = +G.n. Fails for G_E = E u (0.7635),
+    a dropped m_x (u.n) (1.0 instead of 1.09) or a dropped p (0.09)."""
+    U = [1.0, 0.3, 0.0, 0.0, 2.545]
+    F = _one_face(U, U, [1.0, 0.0, 0.0])
+    Gn = np.array([0.3, 1.09, 0.0, 0.0, 1.0635])
+    assert np.allclose(F[0], -Gn, rtol=1e-6, atol=1e-7)
+    assert np.allclose(F[1], Gn, rtol=1e-6, atol=1e-7)
+
+
+def test_uniform_flow_general_direction():
+    """Uniform state, velocity and normal in general position (every component of the
+    momentum flux m (u.n) + p n is exercised with a different value).
+    rho = 2, u = (0.1, -0.2, 0.3), p = 1.5:  m = (0.2, -0.4, 0.6), |u|^2 = 0.14,
+      E = 1.5/0.4 + 0.5 * 2 * 0.14 = 3.75 + 0.14 = 3.89.
+    n = (0.5, 1, -2):  u.n = 0.05 - 0.2 - 0.6 = -0.75,  m.n = 0.1 - 0.4 - 1.2 = -1.5;
+      (G.n)_rho = m.n = -1.5
+      (G.n)_mx  = m_x (u.n) + p n_x = -0.15 + 0.75 =  0.6
+      (G.n)_my  = m_y (u.n) + p n_y =  0.3  + 1.5  =  1.8
+      (G.n)_mz  = m_z (u.n) + p n_z = -0.45 - 3.0  = -3.45
+      (G.n)_E   = (E + p)(u.n) = 5.39 * -0.75      = -4.0425
+    F_a = -G.n."""
+    U = [2.0, 0.2, -0.4, 0.6, 3.89]
+    F = _one_face(U, U, [0.5, 1.0, -2.0])
+    assert np.allclose(F[0], [1.5, -0.6, -1.8, 3.45, 4.0425], rtol=1e-6, atol=1e-6)
+    assert np.allclose(F[1], -F[0], rtol=0, atol=1e-12)
+
+
+def test_dissipation_magnitude_at_rest():
+    """Two fluids at rest (u = 0: no convective flux; only the pressure and the
+    dissipation act). gamma = 1.4, sigma = 0.2, n = (2, 0, 0), |n| = 2:
+      a: rho = 1.2, E = 2.5 -> p = 0.4 * 2.5 = 1.0, c_a = sqrt(1.4 * 1.0 / 1.2) = 1.0801234497346435
+      b: rho = 1.0, E = 2.0 -> p = 0.4 * 2.0 = 0.8, c_b = sqrt(1.4 * 0.8 / 1.0) = 1.0583005244258363
+      f = -|n| sigma (|u_a| + |u_b| + c_a + c_b)/2 = -0.2 (c_a + c_b) = -0.427684794832096
+      Phi_rho = f (1.2 - 1.0)                 = -0.0855369589664192
+      Phi_mx  = f * 0 - (p_a + p_b) n_x / 2   = -1.8
+      Phi_E   = f (2.5 - 2.0)                 = -0.213842397416048
+    Fails for c = sqrt(p/rho), a missing 1/2 or sigma, or |n| dropped from f."""
+    F = _one_face([1.2, 0, 0, 0, 2.5], [1.0, 0, 0, 0, 2.0], [2.0, 0.0, 0.0])
+    want = [-0.0855369589664192, -1.8, 0.0, 0.0, -0.213842397416048]
+    assert np.allclose(F[0], want, rtol=1e-6, atol=1e-12)
+    assert np.allclose(F[1], -F[0], rtol=0, atol=1e-15)
+
+
+def test_dissipation_speed_includes_velocity():
+    """The dissipation speed is |u| + c of both sides. a moves across the face
+    (u_a = (0, 0.4, 0), u_a.n = 0: no convective flux through n = (1, 0, 0)), b is at rest;
+    rho = 1, p = 1 on both sides: E_a = 2.5 + 0.16/2 = 2.58, E_b = 2.5, c = sqrt(1.4) =
+    1.1832159566199232 on both sides.
+      f = -1 * 0.2 * (0.4 + 2c)/2 = -0.2766431913239846
+      U_a - U_b = (0, 0, 0.4, 0, 0.08)
+      n.G_a = n.G_b = (0, p, 0, 0, 0) = (0, 1, 0, 0, 0)
+      Phi = (0, -1, 0.4 f, 0, 0.08 f) = (0, -1, -0.11065727652959385, 0, -0.02213145530591877)."""
+    F = _one_face([1.0, 0.0, 0.4, 0.0, 2.58], [1.0, 0.0, 0.0, 0.0, 2.5], [1.0, 0.0, 0.0])
+    want = [0.0, -1.0, -0.11065727652959385, 0.0, -0.02213145530591877]
+    assert np.allclose(F[0], want, rtol=1e-6, atol=1e-7)
+
+
 def test_dissipation_direction():
     """At rest, mass and energy diffuse from the denser/hotter cell to the other."""
     e = np.array([[0, 1]], np.int32)

@@ -195,3 +195,100 @@ def test_epg1_quality_on_cfd_mesh(mesh_c1):
     r_def = O.cost(M.edges, M.n, O.default_partition(M.m, 1024), k)
     assert r_ep.max_size - r_ep.min_size <= 1 and r_ep.balance_factor < 1.03
     assert r_def.replication / r_ep.replication > 2.0
+
+
+# ------------------------------------------------------------------------------------
+# O4 + O5 transcribed literally (pure Python, small inputs only): a second, independent
+# statement of EPG-1 that shares nothing with oracle/epg_oracle.c but the text of
+# SURVEY §8(c) O4/O5 (Def. 3, P:377 weight, P:380 chain order).
+def T_python(edges, n):
+    """O4: every vertex's endpoint slots (e, s) in ascending (e, s); each consecutive pair
+    (e_j, e_j+1) with e_j != e_j+1 adds weight 1 to the undirected T-edge {e_j, e_j+1}."""
+    slots = [[] for _ in range(n)]
+    for e, (u, v) in enumerate(edges):
+        slots[u].append((e, 0))
+        slots[v].append((e, 1))
+    W = {}
+    for v in range(n):
+        ch = sorted(slots[v])
+        for (e0, _), (e1, _) in zip(ch, ch[1:]):
+            if e0 != e1:
+                a, b = min(e0, e1), max(e0, e1)
+                W[(a, b)] = W.get((a, b), 0) + 1
+    nbrs = [dict() for _ in range(len(edges))]
+    for (a, b), w in W.items():
+        nbrs[a][b] = w
+        nbrs[b][a] = w
+    return [sorted(d.items()) for d in nbrs]      # (nb, w), ascending nb
+
+
+def epg1_python(nbrs, sizes):
+    """O5 flat mode, step by step."""
+    m = len(nbrs)
+    INF = float("inf")
+    part, gst, G = [-1] * m, [INF] * m, 0
+    for i, size in enumerate(sizes):
+        cand = [t for t in range(m) if part[t] == -1 and gst[t] != INF]
+        seed = min(cand, key=lambda t: gst[t]) if cand else min(t for t in range(m) if part[t] == -1)
+        g, lst, c = [0] * m, [INF] * m, 0
+        if size == 0:
+            continue
+        lst[seed] = c
+        c += 1
+        for _ in range(size):
+            front = [t for t in range(m) if part[t] == -1 and lst[t] != INF]
+            if not front:
+                t = min(t for t in range(m) if part[t] == -1)
+                lst[t] = c
+                c += 1
+            else:
+                t = max(front, key=lambda t: (g[t], -lst[t]))
+            part[t] = i
+            for nb, w in nbrs[t]:
+                if part[nb] != -1:
+                    continue
+                if lst[nb] == INF:
+                    lst[nb] = c
+                    c += 1
+                g[nb] += w
+                if gst[nb] == INF:
+                    gst[nb] = G
+                    G += 1
+    return part
+
+
+def partition_python(edges, n, P, shards=1):
+    """O1 sizes + O5 (flat, or hierarchical: shard-level EPG-1, then EPG-1 on T restricted to
+    each shard with tasks renumbered by ascending id, partition ids offset by floor(gk/G))."""
+    m = len(edges)
+    k = -(-m // P)
+    s = [m // k + (1 if i < m % k else 0) for i in range(k)]
+    nbrs = T_python(edges, n)
+    if shards == 1:
+        return epg1_python(nbrs, s)
+    G = shards
+    ssize = [sum(s[g * k // G:(g + 1) * k // G]) for g in range(G)]
+    shard = epg1_python(nbrs, ssize)
+    part = [-1] * m
+    for g in range(G):
+        mem = [t for t in range(m) if shard[t] == g]
+        loc = {t: j for j, t in enumerate(mem)}
+        sub = [[(loc[nb], w) for nb, w in nbrs[t] if shard[nb] == g] for t in mem]
+        res = epg1_python(sub, s[g * k // G:(g + 1) * k // G])
+        for j, t in enumerate(mem):
+            part[t] = res[j] + g * k // G
+    return part
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_epg1_literal_transcription(seed):
+    """The oracle's EPG-1 equals a line-by-line transcription of O4/O5 on random
+    multigraphs (self-loops and parallel edges kept), flat and with two shards."""
+    rng = np.random.default_rng(7000 + seed)
+    m, n0 = int(rng.integers(8, 70)), int(rng.integers(3, 30))
+    n, e = S.random_multigraph(500 + seed, m, n0)
+    P = int(rng.integers(2, 12))
+    el = [tuple(map(int, x)) for x in e]
+    assert O.partition(e, n, P).tolist() == partition_python(el, n, P)
+    if O.num_parts(m, P) >= 2:
+        assert O.partition(e, n, P, shards=2).tolist() == partition_python(el, n, P, shards=2)
