@@ -44,6 +44,10 @@ WORKLOADS = {
     "c5": "C5 per-GPU share: SpMV of a 2D 5-point Laplacian on a 3536^2 grid (12.5M rows, 62.5M nnz = 1/8 "
           "of the 500M-nnz 8-GPU config) as a bipartite COO data-affinity graph",
 }
+FUNCTORS = {"c1": "cfd_flux", "c2": "cfd_flux", "c3": "cfd_flux", "c4": "gather_scatter", "c5": "spmv"}
+L2_MODE = ("inputs larger than L2: the timed steps cycle round-robin over R independent replicas of the "
+           "workload (own plan, state, payload and constants each; R x working set >= 3 x L2), so every "
+           "step's inputs were evicted by the others' traffic; per-step L2-flushed timing reported beside it")
 
 
 class Workload:
@@ -108,9 +112,12 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="bounded oracle sample for cpu_baseline")
     ap.add_argument("--variant", type=int, default=0,
                     help="staged-kernel variant (epg_set_variant): 0 auto, 3 occupancy + finalise, 4 persistent fused")
-    ap.add_argument("--partitioner", choices=["epg1", "epg2"], default="epg2",
-                    help="EP partitioner: epg1 (growing on the clone-and-connect graph T) or epg2 (growing on "
-                         "Eq. (1)'s objective, SURVEY 8(f) rank 2); the other one runs as a comparator")
+    ap.add_argument("--partitioner", choices=["epg1", "epg2", "rb"], default="rb",
+                    help="EP partitioner: epg1 (growing on the clone-and-connect graph T), epg2 (growing on "
+                         "Eq. (1)'s objective) or rb (GPU recursive bisection + EPG-2 leaves on all host cores; "
+                         "SURVEY 8(f) rank 2); on C2 (k = 448 < 512) rb has depth 0 and equals epg2")
+    ap.add_argument("--no-c3", action="store_true", help="skip the C3 (bandwidth-regime) sub-record")
+    ap.add_argument("--c3-steps", type=int, default=20)
     ap.add_argument("--exec-rows", type=int, default=0,
                     help="execution-split row cap (epg_set_exec_limits; 0 = the config's default)")
     ap.add_argument("--exec-edges", type=int, default=0,
@@ -122,7 +129,7 @@ def parse():
     return ap.parse_args()
 
 
-PARTITIONERS = {"epg1": 1, "epg2": 2}
+PARTITIONERS = {"epg1": 1, "epg2": 2, "rb": 3}
 
 
 def dist_env():
@@ -245,6 +252,52 @@ def oracle_steps(w: "Workload", steps: int, budget_s: float | None = None):
     return done, time.perf_counter() - t0
 
 
+def cpu_info():
+    """Host cores and CPU model of the box the bench runs on."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.lower().startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return {"nproc": len(os.sched_getaffinity(0)), "cpu_model": model}
+
+
+def bench_config(args):
+    """The `config` dict both arms print (the driver compares them): only keys that do
+    not depend on running the library."""
+    P = args.part_size
+    return {"workload": WORKLOADS[args.config], "part_size": P, "functor": FUNCTORS[args.config],
+            "schedule": f"EP ({args.partitioner.upper()} partitioner) + cpack remap",
+            "step": "one time step of the hot path: staged edge kernel (a5) + boundary finalise (a6)",
+            "l2": L2_MODE,
+            "parallelism": "single GPU" if args.gpus == 1 else f"{args.gpus} GPUs"}
+
+
+def oracle_baseline(w: "Workload", budget_s: float, steps_min: int = 1):
+    """The fp64 oracle step, as it stands, single thread and (cfd) over all host cores."""
+    steps, secs = oracle_steps(w, steps_min, budget_s=budget_s)
+    one = w.m * steps / secs
+    out = {"value": one, "unit": "edges/s", "cores": 1, "kind": "oracle",
+           "sample": f"{steps} full steps of the fp64 oracle ({w.oracle_name()} in oracle/epg_oracle.c) on the "
+                     f"{w.config} workload, single thread, ~{budget_s:.0f} s budget"}
+    if w.kernel == 1:
+        import oracle as O
+        done, t0, th = 0, time.perf_counter(), 1
+        while done < steps_min or time.perf_counter() - t0 < budget_s / 2:
+            th = O.cfd_step_omp(w.edges, w.n, w.payload, w.state, w.vconst)[2]
+            done += 1
+        all_core = w.m * done / (time.perf_counter() - t0)
+        out["all_cores"] = {"value": all_core, "unit": "edges/s", "cores": th,
+                            "sample": f"{done} full steps of orc_cfd_step_omp (OpenMP, per-thread private "
+                                      f"accumulators; timing only) on {th} threads"}
+    out.update(cpu_info())
+    return out
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -252,14 +305,15 @@ def run_reference(args, rank, world):
     oracle_steps(w, args.warmup)
     steps, secs = oracle_steps(w, args.steps)
     v = w.m * steps / secs
+    info = cpu_info()
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "edges/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.config], "part_size": args.part_size, "functor": w.functor},
+        "config": bench_config(args),
         "cpu_baseline": {"value": v, "unit": "edges/s", "cores": 1, "kind": "oracle",
                          "sample": f"{steps} full steps of the fp64 oracle ({w.oracle_name()} in oracle/epg_oracle.c) "
-                                   f"on the {args.config} workload, single thread"},
+                                   f"on the {args.config} workload, single thread", **info},
         "e2e": {"value": v, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -277,6 +331,17 @@ def timed_steps(torch, ctx, stream, K, step_fn, flush):
         evs[i][1].record(stream)
     torch.cuda.synchronize()
     return sum(a.elapsed_time(b) for a, b in evs)
+
+
+def timed_block(torch, stream, K, step_fn):
+    """K steps back to back between one pair of CUDA events on the library's stream."""
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(K):
+        step_fn(i)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1)
 
 
 def run_sharded(args, rank, local_rank, world):
@@ -404,18 +469,123 @@ def run_sharded(args, rank, local_rank, world):
         dist.destroy_process_group()
 
 
+class Replica:
+    """One independent copy of a workload's per-step inputs in the plan layout: its own plan
+    (remapped from the same map), state ping-pong buffers, payload and constants."""
+
+    def __init__(self, ctx, epg, M, E, part, k, halo_cap, pay0, vc0, Ud):
+        self.L, self.plan = ctx.remap(E, M.n, part, k, halo_cap=halo_cap)
+        self.nrm = None if pay0 is None else ctx.permute_rows(pay0, self.L.edge_perm, epg.PERM_GATHER)
+        self.dt = None if vc0 is None else ctx.permute_rows(vc0, self.L.vertex_perm, epg.PERM_SCATTER)
+        self.bufs = [ctx.permute_rows(Ud, self.L.vertex_perm, epg.PERM_SCATTER), None]
+        self.bufs[1] = self.bufs[0].clone()
+        self.t = 0
+
+    def step(self, ctx, kernel, pingpong: bool):
+        j = self.t & 1 if pingpong else 0
+        ctx.run(self.plan, kernel, self.bufs[j], self.bufs[1 - j], self.nrm, self.dt, 1)
+        self.t += 1
+
+    def footprint(self) -> int:
+        b = sum(x.numel() * x.element_size() for x in self.bufs)
+        for x in (self.nrm, self.dt, self.L.slots):
+            if x is not None:
+                b += x.numel() * x.element_size()
+        return b
+
+
+def l2_bytes(torch, dev):
+    try:
+        return int(torch.cuda.get_device_properties(dev).L2_cache_size)
+    except Exception:
+        return 126 << 20
+
+
+def run_c3(args, torch, epg, ctx, stream, peak):
+    """C3 sub-record (SURVEY §8(d) bandwidth regime: 64M cells, working set >> L2): EP step on
+    an EPG-RB map, back-to-back steps (inputs 5 GB: nothing survives in L2 between steps), the
+    edge kernel's and the step's fraction of the HBM roofline, partition time against the step
+    time (the paper's yardstick), and the default-schedule step on the same box."""
+    import synth as S
+    t0 = time.perf_counter()
+    M = S.config_mesh("c3")
+    gen = time.perf_counter() - t0
+    dev = ctx.device
+    P = args.part_size
+    E = torch.from_numpy(M.edges).to(dev)
+    k = epg.num_parts(M.m, P)
+    ctx.set_exec_limits(704, 1024)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    part, rep = ctx.partition_rb(E, M.n, P)
+    t_part = time.perf_counter() - t0
+    pay0 = torch.from_numpy(M.normals).to(dev)
+    vc0 = torch.from_numpy(S.cfd_dt(M.volume)).to(dev)
+    Ud = torch.from_numpy(S.cfd_state(M.n)).to(dev)
+    del M
+    t0 = time.perf_counter()
+    R = Replica(ctx, epg, _MeshN(Ud.shape[0]), E, part, k, rep.cut_cost, pay0, vc0, Ud)
+    torch.cuda.synchronize()
+    t_remap = time.perf_counter() - t0
+    K = args.c3_steps
+    for _ in range(3):
+        R.step(ctx, epg.KERNEL_CFD_FLUX, True)
+    torch.cuda.synchronize()
+    ms = timed_block(torch, stream, K, lambda i: R.step(ctx, epg.KERNEL_CFD_FLUX, True)) / K
+    ctx.set_profiling(True)
+    ctx.profile_read()
+    timed_block(torch, stream, K, lambda i: R.step(ctx, epg.KERNEL_CFD_FLUX, True))
+    (edge_ms, fin_ms), (ne, nf) = ctx.profile_read()
+    ctx.set_profiling(False)
+    edge_ms, fin_ms = edge_ms / K, fin_ms / K
+    m = E.shape[0]
+    B = alg_bytes_per_step(m, rep.touched)
+    traffic, traffic_src, variants = ncu_evidence("c3")
+    out = {
+        "workload": WORKLOADS["c3"], "m": m, "n": rep.touched, "part_size": P, "k": k, "k_exec": R.plan.k_exec,
+        "partitioner": "EPG-RB (GPU bisection levels + EPG-2 leaves on the host cores)",
+        "ms_per_step": ms, "edges_per_s": m / (ms * 1e-3),
+        "edge_kernel_ms": edge_ms, "finalise_ms": fin_ms,
+        "roofline_edge_kernel": {"bound": "hbm", "achieved": B / (edge_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                                 "frac": B / (edge_ms * 1e-3) / 1e9 / peak, "algorithmic_bytes": B,
+                                 "traffic": traffic, "traffic_source": traffic_src},
+        "roofline_step": {"achieved": B / (ms * 1e-3) / 1e9, "frac": B / (ms * 1e-3) / 1e9 / peak},
+        "partition": {"replication": rep.replication, "cut_cost": rep.cut_cost, "load_count": rep.load_count,
+                      "host_partition_s": t_part, "partition_over_step": t_part / (ms * 1e-3),
+                      "remap_s": t_remap, "mesh_gen_s": gen},
+        "bytes_per_edge_ncu": variants,
+        "timing": "K back-to-back epg_run(steps=1) calls between one CUDA event pair (inputs >> L2)",
+    }
+    if not args.no_comparators:
+        dpart = ctx.default_partition(m, P)
+        drep = ctx.load_count(E, Ud.shape[0], dpart, k)
+        del R
+        D = Replica(ctx, epg, _MeshN(Ud.shape[0]), E, dpart, k, drep.cut_cost, pay0, vc0, Ud)
+        for _ in range(2):
+            D.step(ctx, epg.KERNEL_CFD_FLUX, True)
+        dms = timed_block(torch, stream, 5, lambda i: D.step(ctx, epg.KERNEL_CFD_FLUX, True)) / 5
+        out["default_staged"] = {"ms_per_step": dms, "replication": drep.replication,
+                                 "ep_speedup": dms / ms}
+        del D
+    del E, pay0, vc0, Ud
+    torch.cuda.empty_cache()
+    return out
+
+
+class _MeshN:
+    def __init__(self, n):
+        self.n = n
+
+
 def run_ours(args, rank, local_rank, world):
     import torch
     import torch.distributed as dist
 
-    import synth as S
     from paper_1605_02043_b200 import epg
 
     if world > 1 or args.force_sharded:
         return run_sharded(args, rank, local_rank, world)
     torch.cuda.set_device(local_rank)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     dev = torch.device("cuda", local_rank)
     stream = torch.cuda.current_stream(dev)
     ctx = epg.Context(local_rank, stream)
@@ -435,18 +605,21 @@ def run_ours(args, rank, local_rank, world):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     ctx.set_partition_method(PARTITIONERS[args.partitioner])
-    part, rep = ctx.partition(E, M.n, P)                      # host EPG + GPU cost kernel
+    part, rep = ctx.partition(E, M.n, P)                      # EP partition + GPU cost kernel
     t_part = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    L, plan = ctx.remap(E, M.n, part, k, halo_cap=rep.cut_cost)
-    torch.cuda.synchronize()
-    t_remap = time.perf_counter() - t0
     Ud = torch.from_numpy(M.state).to(dev)
     pay0 = None if M.payload is None else torch.from_numpy(M.payload).to(dev)
     vc0 = None if M.vconst is None else torch.from_numpy(M.vconst).to(dev)
-    nrm = None if pay0 is None else ctx.permute_rows(pay0, L.edge_perm, epg.PERM_GATHER)
-    dtn = None if vc0 is None else ctx.permute_rows(vc0, L.vertex_perm, epg.PERM_SCATTER)
-    bufs = [ctx.permute_rows(Ud, L.vertex_perm, epg.PERM_SCATTER), torch.empty_like(Ud)]
+    t0 = time.perf_counter()
+    reps = [Replica(ctx, epg, M, E, part, k, rep.cut_cost, pay0, vc0, Ud)]
+    torch.cuda.synchronize()
+    t_remap = time.perf_counter() - t0
+    plan, L = reps[0].plan, reps[0].L
+    # enough replicas that the round-robin working set is >= 3 x L2
+    l2 = l2_bytes(torch, dev)
+    nrep = int(min(64, max(2, -(-3 * l2 // max(1, reps[0].footprint())))))
+    while len(reps) < nrep:
+        reps.append(Replica(ctx, epg, M, E, part, k, rep.cut_cost, pay0, vc0, Ud))
     flushbuf = torch.empty(args.flush_mib * (1 << 20) // 4, dtype=torch.float32, device=dev)
 
     def flush():
@@ -455,54 +628,51 @@ def run_ours(args, rank, local_rank, world):
     # gather-scatter / SpMV read x and write y: keep x fixed (state_in) across steps
     pingpong = KER == epg.KERNEL_CFD_FLUX
 
-    def ep_step(i):
-        j = i & 1 if pingpong else 0
-        ctx.run(plan, KER, bufs[j], bufs[1 - j], nrm, dtn, 1)
+    def rr_step(i):
+        reps[i % nrep].step(ctx, KER, pingpong)
 
-    def barrier():
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    # ---------------- headline: resident inputs, L2 flushed between steps
-    for i in range(W):
-        ep_step(i)
-    barrier()
+    # ---------------- headline: K steps round-robin over the replicas, inputs >> L2
+    for i in range(max(W, nrep)):
+        rr_step(i)
+    torch.cuda.synchronize()
     with clocks.window():
-        tot_ms = timed_steps(torch, ctx, stream, K, lambda i: ep_step(i + W), flush)
-    barrier()
+        tot_ms = timed_block(torch, stream, K, rr_step)
     step_ms = tot_ms / K
-    if world > 1:
-        t = torch.tensor([step_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        step_ms = float(t.item())
-    value = world * M.m / (step_ms * 1e-3)
+    value = M.m / (step_ms * 1e-3)
 
-    # ---------------- per-kernel breakdown (library events around each launch)
+    # ---------------- per-kernel breakdown (library events around each launch, same mode)
     ctx.set_profiling(True)
     ctx.profile_read()
-    timed_steps(torch, ctx, stream, K, lambda i: ep_step(i), flush)
+    timed_block(torch, stream, K, rr_step)
     (edge_ms, fin_ms), (n_edge, n_fin) = ctx.profile_read()
     ctx.set_profiling(False)
-    launches = K * (n_edge + n_fin) // K             # our kernels per step x K timed steps
+    launches = n_edge + n_fin                        # our kernels in K steps
     edge_ms, fin_ms = edge_ms / K, fin_ms / K         # per step
 
+    # ---------------- the same step, L2 flushed before each one and timed alone
+    R0 = reps[0]
+    with clocks.window():
+        cold_ms = timed_steps(torch, ctx, stream, K, lambda i: R0.step(ctx, KER, pingpong), flush) / K
+    # ---------------- steady state: K steps in one epg_run call (one CUDA graph), L2 warm
+    a, b = R0.bufs[0].clone(), R0.bufs[1].clone()
+    ctx.run(plan, KER, a, b, R0.nrm, R0.dt, K)
+    torch.cuda.synchronize()
+    steady_ms = timed_block(torch, stream, 1, lambda i: ctx.run(plan, KER, a, b, R0.nrm, R0.dt, K)) / K
+    del a, b
+
     # ---------------- e2e: host (pinned) state in, result out, through the C-ABI host call
-    # (epg_run_host: H2D + layout + step + layout + D2H per call, calls pipelined across two
-    # copy streams). Total device time of K calls (L2 flush included) / K.
     Uh = torch.from_numpy(M.state).pin_memory()
     Uout_h = [torch.empty_like(Uh).pin_memory() for _ in range(2)]
     n_bytes = Uh.numel() * 4
 
     def e2e_step(i):
         flush()
-        ctx.run_host(plan, KER, L.vertex_perm, Uh, Uout_h[i & 1], nrm, dtn, 1)
+        ctx.run_host(plan, KER, L.vertex_perm, Uh, Uout_h[i & 1], R0.nrm, R0.dt, 1)
 
     for i in range(W):
         e2e_step(i)
     ctx.join()
-    barrier()
+    torch.cuda.synchronize()
     with clocks.window():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -512,14 +682,9 @@ def run_ours(args, rank, local_rank, world):
         e1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = e0.elapsed_time(e1) / K
-    barrier()
-    if world > 1:
-        t = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    e2e_value = world * M.m / (e2e_ms * 1e-3)
+    e2e_value = M.m / (e2e_ms * 1e-3)
 
-    # ---------------- comparators on the same box: default schedule, staged and naive
+    # ---------------- comparators on the same box (per-step L2 flush, like cold_single_step)
     comparators = None
     if not args.no_comparators:
         dpart = ctx.default_partition(M.m, P)
@@ -542,20 +707,19 @@ def run_ours(args, rank, local_rank, world):
 
         # the paper's hardware-cache variant: EP order + cpack layout, no staging
         Ex = ctx.remapped_edges(E, L)
-        hbufs = [bufs[0].clone(), torch.empty_like(Ud)]
+        hbufs = [R0.bufs[0].clone(), torch.empty_like(Ud)]
 
         def hwcache_step(i):
-            ctx.run_naive(KER, Ex, M.n, hbufs[pp(i)], hbufs[1 - pp(i)], nrm, dtn, 1)
+            ctx.run_naive(KER, Ex, M.n, hbufs[pp(i)], hbufs[1 - pp(i)], R0.nrm, R0.dt, 1)
 
-        # PowerGraph's random / greedy edge placements through the same staged
-        # kernel: the paper's quality comparators (greedy is skipped on power-law graphs,
-        # whose hubs make its per-edge candidate scan quadratic)
         runs = [("default_staged", def_step, drep), ("naive_original_order", naive_step, None),
                 ("ep_hardware_cache", hwcache_step, None)]
-        other = "epg1" if args.partitioner == "epg2" else "epg2"
         baselines = []
-        if not (other == "epg2" and KER == epg.KERNEL_GATHER_SCATTER):   # EPG-2 is too slow on R-MAT hubs
-            baselines.append((f"ep_{other}", lambda: epg.partition_host(M.edges, M.n, P, method=PARTITIONERS[other])))
+        for other in ("epg1", "epg2"):
+            if other == args.partitioner or (other == "epg2" and KER == epg.KERNEL_GATHER_SCATTER):
+                continue                                  # EPG-2 flat is too slow on R-MAT hubs
+            baselines.append((f"ep_{other}", lambda o=other: epg.partition_host(M.edges, M.n, P,
+                                                                                method=PARTITIONERS[o])))
         baselines.append(("powergraph_random", lambda: epg.partition_random_host(M.m, P, 1605)))
         if KER != epg.KERNEL_GATHER_SCATTER:
             baselines.append(("powergraph_greedy", lambda: epg.partition_greedy_host(M.edges, M.n, P)))
@@ -576,11 +740,11 @@ def run_ours(args, rank, local_rank, world):
                 ctx.run(bplan, KER, bb[pp(i)], bb[1 - pp(i)], bn, bd, 1)
             brep.partition_s = t_b
             runs.append((bname, b_step, brep))
-        out = {}
+        out = {"timing": "per-step L2 flush + CUDA events around each step (the cold_single_step method)"}
         for name, fn, r in runs:
             for i in range(W):
                 fn(i)
-            barrier()
+            torch.cuda.synchronize()
             ms = timed_steps(torch, ctx, stream, K, fn, flush) / K
             out[name] = {"edges_per_s": M.m / (ms * 1e-3), "ms_per_step": ms}
             if r is not None:
@@ -588,17 +752,19 @@ def run_ours(args, rank, local_rank, world):
                                   "replication": r.replication})
                 if hasattr(r, "partition_s"):
                     out[name]["host_partition_s"] = r.partition_s
-        best_default = max(out[k]["edges_per_s"] for k in ("default_staged", "naive_original_order"))
-        out["ep_speedup_vs_best_default"] = (M.m / (step_ms * 1e-3)) / best_default
+        best_default = max(out[k2]["edges_per_s"] for k2 in ("default_staged", "naive_original_order"))
+        out["ep_speedup_vs_best_default"] = (M.m / (cold_ms * 1e-3)) / best_default
         comparators = out
-
-    clk = clocks.summary()
-    if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
-        return
+        del base_keep, dplan, DL, dbufs, nbufs, hbufs, Ex
 
     peak, peak_src = measured_peaks()
+    c3 = None
+    if args.config == "c2" and not args.no_c3:
+        del reps, R0
+        torch.cuda.empty_cache()
+        c3 = run_c3(args, torch, epg, ctx, stream, peak)
+
+    clk = clocks.summary()
     B = M.alg_bytes(rep.touched)
     # every compulsory byte of the step (edge records, each touched row read and written
     # once) is moved by the edge kernel; the finalise only re-touches shared rows
@@ -614,51 +780,50 @@ def run_ours(args, rank, local_rank, world):
         "algorithmic_bytes_per_launch": B,
         "bytes_per_edge_algorithmic": B / M.m,
         "edge_kernel_ms": edge_ms, "finalise_ms": fin_ms,
-        "kernel_times": "CUDA events around each launch on the library stream (they also hold the "
-                        "launch gaps; the step time is measured without them)",
+        "kernel_times": "CUDA events around each launch on the library stream, round-robin replica mode (they "
+                        "also hold the launch gaps; the step time is measured without them)",
         "step_achieved_gbs": B / (step_ms * 1e-3) / 1e9,
+        "step_frac": B / (step_ms * 1e-3) / 1e9 / peak,
         "peak_source": peak_src,
         "traffic_source": traffic_src,
     }
-
-    cpu = None
-    if world == 1 and not args.no_cpu_baseline:
-        steps, secs = oracle_steps(M, 1, budget_s=args.cpu_seconds)
-        cpu = {"value": M.m * steps / secs, "unit": "edges/s", "cores": 1, "kind": "oracle",
-               "sample": f"{steps} full steps of the fp64 oracle ({M.oracle_name()} in oracle/epg_oracle.c) "
-                         f"on the {args.config} workload, single thread, ~{args.cpu_seconds:.0f} s budget"}
+    cpu = None if args.no_cpu_baseline else oracle_baseline(M, args.cpu_seconds)
 
     line = {
         "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.config], "part_size": P, "k": k, "k_exec": plan.k_exec,
-                   "functor": M.functor,
-                   "schedule": f"EP (host {args.partitioner.upper()}) + cpack remap", "step": "epg_run(steps=1): staged edge kernel + boundary finalise",
-                   "l2": f"flushed between timed steps ({args.flush_mib} MiB write)",
-                   "parallelism": "replicas" if world > 1 else "single"},
+        "config": bench_config(args),
+        "replicas": nrep,
+        "cold_single_step": {"ms_per_step": cold_ms, "edges_per_s": M.m / (cold_ms * 1e-3),
+                             "timing": f"L2 flushed ({args.flush_mib} MiB write) before each step, CUDA events "
+                                       "around each step (includes ~6 us of event/launch floor, "
+                                       "profiles/r02_c2_flush_floor.json)"},
+        "steady_state": {"ms_per_step": steady_ms, "edges_per_s": M.m / (steady_ms * 1e-3),
+                         "timing": f"one epg_run(steps={K}) call (one CUDA graph), L2 warm, one replica"},
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "edges/s", "h2d_bytes_per_step": n_bytes, "d2h_bytes_per_step": n_bytes,
                 "ms_per_step": e2e_ms,
-                "path": "epg_run_host per step: pinned host state -> H2D -> layout -> epg_run -> layout -> D2H, "
-                        "consecutive calls overlapped on copy-in / compute / copy-out streams; "
-                        "total of K calls incl. the per-step L2 flush, / K"},
+                "path": "epg_run_host per step: pinned host state -> H2D -> layout -> epg_run -> layout -> D2H; "
+                        "K independent calls on the same host input (a throughput figure, not a dependent "
+                        "time-stepping loop), overlapped on copy-in / compute / copy-out streams; total of K "
+                        "calls incl. the per-step L2 flush, / K"},
         "gpu_launches": launches,
         "clocks": clk,
-        "partition": {"load_count": rep.load_count, "touched": rep.touched, "cut_cost": rep.cut_cost,
+        "partition": {"method": args.partitioner, "k": k, "k_exec": plan.k_exec,
+                      "load_count": rep.load_count, "touched": rep.touched, "cut_cost": rep.cut_cost,
                       "replication": rep.replication, "redundant_fraction": rep.redundant_fraction,
                       "max_size": rep.max_size, "min_size": rep.min_size, "shared_vertices": plan.shared,
-                      "hubs": plan.hubs, "hub_min_halo_entries": plan.hub_min, "k_exec": plan.k_exec,
+                      "hubs": plan.hubs, "hub_min_halo_entries": plan.hub_min,
                       "exec_max_rows": M.exec_rows,
                       "host_partition_s": t_part, "remap_s": t_remap, "mesh_gen_s": t_gen},
         "comparators": comparators,
         "bytes_per_edge_ncu": variants,
+        "c3": c3,
         "seeds": {"mesh": 1605, "state": 1606, "rmat": 1607, "x": [1608, 1609]},
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
 
 
 def main():

@@ -168,6 +168,18 @@ epg_status epg_partition_host(const int32_t *edges, int64_t m, int32_t n_vertice
  * determinism as EPG-1. */
 #define EPG_PARTITION_EPG1 1
 #define EPG_PARTITION_EPG2 2
+/* EPG_PARTITION_RB (the GPU-parallel EP partitioner; DESIGN.md reading
+ * Z21): recursive graph-growing bisection of the task set on the GPU, then EPG-2 in every
+ * leaf on all host cores. Bisection depth d = log2(shards), raised while every leaf keeps at
+ * least leaf_parts partitions (d <= 10). Node a of level l holds the partitions
+ * [floor(a k/2^l), floor((a+1) k/2^l)) and exactly their tasks; it is split by a BFS over
+ * tasks sharing a non-hub endpoint (hub: more than 4 x part_size tasks) from a
+ * pseudo-peripheral task (the farthest from the node's smallest task id, ties to the smaller
+ * id): in ascending (distance, id) the first tasks -- as many as its first half of
+ * partitions holds -- form child 2a. Leaves run EPG-2 on their own tasks. With shards = G the
+ * first log2(G) levels are the shards. Deterministic; needs a device (epg_partition /
+ * epg_partition_rb), so epg_partition_host_method rejects it. */
+#define EPG_PARTITION_RB 3
 /* epg_partition_host with a method (EPG_ERR_INPUT for any other value). */
 epg_status epg_partition_host_method(const int32_t *edges, int64_t m, int32_t n_vertices, int32_t part_size,
                                      int32_t shards, int32_t method, int32_t *part_of_edge, char *errbuf,
@@ -189,14 +201,22 @@ epg_status epg_partition_random_host(int64_t m, int32_t part_size, uint64_t seed
 epg_status epg_partition_greedy_host(const int32_t *edges, int64_t m, int32_t n_vertices, int32_t part_size,
                                      int32_t *part_of_edge, char *errbuf, int64_t errbuf_len);
 
-/* Partitioner used by epg_partition and the adaptive executor on ctx (default EPG1);
- * EPG_ERR_INPUT for an unknown method. */
+/* Partitioner used by epg_partition and the adaptive executor on ctx (default EPG1; the
+ * adaptive executor's host thread runs EPG-2 in place of EPG-RB); EPG_ERR_INPUT for an
+ * unknown method. */
 epg_status epg_set_partition_method(epg_ctx *ctx, int32_t method);
 
 /* epg_partition_host (with ctx's method), then the GPU cost function on the result (epg_load_count).
  *   edges [m][2] host or device; part_of_edge [m] host or device out; out report. */
 epg_status epg_partition(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n_vertices, int32_t part_size,
                          int32_t shards, int32_t *part_of_edge, epg_report *out);
+
+/* epg_partition with EPG_PARTITION_RB and an explicit leaf size (epg_partition uses 512, or
+ * the EPG_RB_LEAF_PARTS environment variable). EPG_ERR_INPUT for leaf_parts < 1 or m >= 2^30;
+ * EPG_ERR_INFEASIBLE as for epg_partition_host, or if a BFS is deeper than 2^22 - 2 levels.
+ *   edges [m][2] host or device; part_of_edge [m] host or device out; out report. */
+epg_status epg_partition_rb(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n_vertices, int32_t part_size,
+                            int32_t shards, int32_t leaf_parts, int32_t *part_of_edge, epg_report *out);
 
 /* Default task schedule (O3; "default task scheduling" P:75): task e goes to
  * the i-th contiguous chunk of sizes s_i.  part_of_edge [m] DEVICE out. */

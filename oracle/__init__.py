@@ -26,7 +26,7 @@ OK, ERR_INPUT, ERR_INFEASIBLE = 0, 2, 3
 
 def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-std=c99", "-fPIC", "-shared", "-o", _LIB, _SRC, "-lm"])
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-fopenmp", "-fPIC", "-shared", "-o", _LIB, _SRC, "-lm"])
     return _LIB
 
 
@@ -49,10 +49,14 @@ def lib():
             "orc_partition": (C.c_int, [P, i64, i32, i32, i32, P]),
             "orc_partition_method": (C.c_int, [P, i64, i32, i32, i32, i32, P]),
             "orc_epg2": (C.c_int, [i64, P, i32, P, i64, i64, P]),
+            "orc_partition_rb": (C.c_int, [P, i64, i32, i32, i32, i32, P]),
+            "orc_rb_depth": (C.c_int, [i64, i32, i32]),
             "orc_remap": (C.c_int, [P, i64, i32, P, i64, P, P, P, P, P, P, i64, P]),
             "orc_shard_halos": (C.c_int, [P, i64, i32, P, i64, i32, P, P, P, P, i64]),
             "orc_cfd_flux": (None, [P, i64, i32, P, P, P]),
+            "orc_cfd_flux_abs": (None, [P, i64, i32, P, P, P]),
             "orc_cfd_step": (None, [P, i64, i32, P, P, P, P, P]),
+            "orc_cfd_step_omp": (C.c_int, [P, i64, i32, P, P, P, P, P]),
             "orc_gather_scatter": (None, [P, i64, i32, P, P, P]),
             "orc_spmv": (None, [P, i64, i32, P, P, P]),
             "orc_partition_random": (C.c_int, [i64, i32, C.c_uint64, P]),
@@ -198,6 +202,21 @@ class Layout:
     slots: np.ndarray              # [m][2] uint16
 
 
+def rb_depth(k: int, shards: int = 1, leaf_parts: int = 256) -> int:
+    """Bisection depth of EPG-RB (O5'', reading Z21)."""
+    return int(lib().orc_rb_depth(k, shards, leaf_parts))
+
+
+def partition_rb(edges, n: int, P: int, shards: int = 1, leaf_parts: int = 256) -> np.ndarray:
+    """EPG-RB (O5''): recursive graph-growing bisection, EPG-2 in every leaf."""
+    e, m = _edges(edges)
+    part = np.zeros(max(m, 1), np.int32)
+    st = lib().orc_partition_rb(_p(e), m, n, P, shards, leaf_parts, _p(part))
+    if st:
+        raise OracleError(st, "orc_partition_rb")
+    return part[:m]
+
+
 def remap(edges, n: int, part, k: int) -> Layout:
     e, m = _edges(edges)
     part = np.ascontiguousarray(part, dtype=np.int32)
@@ -236,6 +255,16 @@ def cfd_flux(edges, n: int, normals, U) -> np.ndarray:
     return F
 
 
+def cfd_flux_abs(edges, n: int, normals, U) -> np.ndarray:
+    """S[v] = sum of |Phi_e| over v's edges (scale of the componentwise metric, Z14)."""
+    e, m = _edges(edges)
+    Sv = np.zeros((n, 5), np.float64)
+    normals = np.ascontiguousarray(normals, np.float32)
+    U = np.ascontiguousarray(U, np.float32)
+    lib().orc_cfd_flux_abs(_p(e), m, n, _p(normals), _p(U), _p(Sv))
+    return Sv
+
+
 def cfd_step(edges, n: int, normals, U, dt):
     e, m = _edges(edges)
     Uout = np.zeros((n, 5), np.float64)
@@ -245,6 +274,18 @@ def cfd_step(edges, n: int, normals, U, dt):
     dt = np.ascontiguousarray(dt, np.float32)
     lib().orc_cfd_step(_p(e), m, n, _p(normals), _p(U), _p(dt), _p(Uout), _p(F))
     return Uout, F
+
+
+def cfd_step_omp(edges, n: int, normals, U, dt):
+    """orc_cfd_step over all host cores (CPU-baseline timing only) -> (U', F, threads)."""
+    e, m = _edges(edges)
+    Uout = np.zeros((n, 5), np.float64)
+    F = np.zeros((n, 5), np.float64)
+    normals = np.ascontiguousarray(normals, np.float32)
+    U = np.ascontiguousarray(U, np.float32)
+    dt = np.ascontiguousarray(dt, np.float32)
+    th = lib().orc_cfd_step_omp(_p(e), m, n, _p(normals), _p(U), _p(dt), _p(Uout), _p(F))
+    return Uout, F, int(th)
 
 
 def gather_scatter(edges, n: int, x, w=None) -> np.ndarray:

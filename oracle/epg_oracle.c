@@ -19,6 +19,9 @@
 #include <stdlib.h>
 #include <string.h>
 #include <math.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 #define ORC_OK 0
 #define ORC_ERR_INPUT 2
@@ -425,6 +428,151 @@ int orc_partition_method(const int32_t *edges, int64_t m, int32_t n, int32_t P, 
 }
 
 /* ------------------------------------------------------------------------- */
+/* O5''. EPG-RB: recursive graph-growing bisection, then EPG-2 in every leaf   */
+/* ("multilevel ... GPU-parallel EP partitioner"; the     */
+/* paper's partitioner is multilevel METIS, P:384-386 / P:418, and its cost   */
+/* is judged against the kernel time). Reading Z21:    */
+/*  - depth d: d = log2(shards); while d < 10 and leaf_parts * 2^(d+1) <= k,  */
+/*    d += 1 (each leaf keeps at least leaf_parts partitions);                */
+/*  - node a of level l (0 <= a < 2^l) holds the partitions                   */
+/*    [floor(a k / 2^l), floor((a+1) k / 2^l)) and exactly their tasks;       */
+/*    level 0 is all tasks;                                                   */
+/*  - bisection of node a: tasks are adjacent when they share an endpoint     */
+/*    that is not a hub (more than 4P incident tasks, as in EPG-2) and both   */
+/*    lie in node a. BFS from the node's smallest task id gives dist1; the    */
+/*    seed is the reached task with the largest dist1, ties by smallest id     */
+/*    (a pseudo-peripheral task); BFS from the seed gives dist (unreached =    */
+/*    infinite). The node's tasks in ascending (dist, id) order: the first     */
+/*    N0 = sum of s_i over [floor(a k/2^l), floor((2a+1) k/2^(l+1))) go to    */
+/*    node 2a of level l+1, the rest to node 2a+1;                            */
+/*  - leaf j (level d) runs EPG-2 (O5', hub 4P) on its tasks, renumbered by  */
+/*    ascending id, with the sizes s_i of its partitions [floor(j k/2^d),     */
+/*    floor((j+1) k/2^d)); partition ids are offset by floor(j k / 2^d).       */
+/* With shards = G the first log2(G) levels are the shards: shard g is the     */
+/* node g of level log2(G), i.e. partitions [floor(g k/G), floor((g+1)k/G)).   */
+/* Every leaf and every node of a level is independent: the bisection levels  */
+/* run on the GPU and the leaves on all host cores in the library.            */
+/* ------------------------------------------------------------------------- */
+int orc_rb_depth(int64_t k, int32_t shards, int32_t leaf_parts) {
+    int d = 0;
+    while ((1 << d) < shards) d++;
+    while (d < 10 && (int64_t)leaf_parts * ((int64_t)1 << (d + 1)) <= k) d++;
+    return d;
+}
+
+/* BFS over the tasks of node `a` (node[] labels) from task `src`; dist[t] of the node's */
+/* tasks is written (INF64 if unreached). vis[] stamps vertices already expanded.       */
+static void rb_bfs(const int32_t *edges, const int64_t *ip, const int64_t *inc, int64_t hub, const int32_t *node,
+                   int32_t a, int64_t src, const int64_t *tasks, int64_t nt, int64_t *dist, int64_t *queue,
+                   int64_t *vis, int64_t stamp) {
+    for (int64_t j = 0; j < nt; j++) dist[tasks[j]] = INF64;
+    int64_t head = 0, tail = 0;
+    dist[src] = 0;
+    queue[tail++] = src;
+    while (head < tail) {
+        int64_t t = queue[head++];
+        for (int side = 0; side < 2; side++) {
+            int32_t v = edges[2 * t + side];
+            if (ip[v + 1] - ip[v] > hub) continue;          /* hubs carry no adjacency */
+            if (vis[v] == stamp) continue;                   /* expanded already       */
+            vis[v] = stamp;
+            for (int64_t q = ip[v]; q < ip[v + 1]; q++) {
+                int64_t u = inc[q];
+                if (node[u] != a || dist[u] != INF64) continue;
+                dist[u] = dist[t] + 1;
+                queue[tail++] = u;
+            }
+        }
+    }
+}
+
+static int64_t *rb_sort_dist;   /* qsort context: distances of the node being ordered */
+static int cmp_dist_id(const void *x, const void *y) {
+    int64_t a = *(const int64_t *)x, b = *(const int64_t *)y;
+    if (rb_sort_dist[a] != rb_sort_dist[b]) return rb_sort_dist[a] < rb_sort_dist[b] ? -1 : 1;
+    return (a > b) - (a < b);
+}
+
+int orc_partition_rb(const int32_t *edges, int64_t m, int32_t n, int32_t P, int32_t shards, int32_t leaf_parts,
+                     int32_t *part) {
+    if (m <= 0 || n <= 0 || leaf_parts < 1) return ORC_ERR_INPUT;
+    if (orc_first_bad_edge(edges, m, n) >= 0) return ORC_ERR_INPUT;
+    if (P < 1 || P > ORC_MAX_PART) return ORC_ERR_INFEASIBLE;
+    int64_t k = orc_num_parts(m, P);
+    if (!(shards == 1 || shards == 2 || shards == 4 || shards == 8) || shards > k) return ORC_ERR_INFEASIBLE;
+    const int64_t hub = 4 * (int64_t)P;
+    int64_t *s = (int64_t *)malloc(sizeof(int64_t) * k);
+    orc_part_sizes(m, k, s);
+    int64_t *S = (int64_t *)malloc(sizeof(int64_t) * (k + 1));          /* S[i] = s_0 + .. + s_{i-1} */
+    S[0] = 0;
+    for (int64_t i = 0; i < k; i++) S[i + 1] = S[i] + s[i];
+    /* incidence: vertex -> tasks, ascending, a self-loop once */
+    int64_t *ip = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
+    for (int64_t t = 0; t < m; t++) {
+        ip[edges[2 * t] + 1]++;
+        if (edges[2 * t + 1] != edges[2 * t]) ip[edges[2 * t + 1] + 1]++;
+    }
+    for (int32_t v = 0; v < n; v++) ip[v + 1] += ip[v];
+    int64_t *fill = (int64_t *)malloc(sizeof(int64_t) * ((size_t)n + 1));
+    memcpy(fill, ip, sizeof(int64_t) * ((size_t)n + 1));
+    int64_t *inc = (int64_t *)malloc(sizeof(int64_t) * (ip[n] > 0 ? ip[n] : 1));
+    for (int64_t t = 0; t < m; t++) {
+        inc[fill[edges[2 * t]]++] = t;
+        if (edges[2 * t + 1] != edges[2 * t]) inc[fill[edges[2 * t + 1]]++] = t;
+    }
+    free(fill);
+    const int d = orc_rb_depth(k, shards, leaf_parts);
+    int32_t *node = (int32_t *)calloc((size_t)m, sizeof(int32_t));
+    int32_t *next = (int32_t *)malloc(sizeof(int32_t) * m);
+    int64_t *dist = (int64_t *)malloc(sizeof(int64_t) * m);
+    int64_t *queue = (int64_t *)malloc(sizeof(int64_t) * m);
+    int64_t *tasks = (int64_t *)malloc(sizeof(int64_t) * m);
+    int64_t *vis = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    for (int32_t v = 0; v < n; v++) vis[v] = -1;
+    int64_t stamp = 0;
+    for (int l = 0; l < d; l++) {
+        const int64_t nodes = (int64_t)1 << l;
+        for (int64_t a = 0; a < nodes; a++) {
+            int64_t nt = 0;
+            for (int64_t t = 0; t < m; t++) if (node[t] == a) tasks[nt++] = t;   /* ascending */
+            if (nt == 0) continue;
+            const int64_t lo = a * k / nodes, mid = (2 * a + 1) * k / (2 * nodes);
+            const int64_t N0 = S[mid] - S[lo];
+            /* BFS 1 from the smallest task id: the seed is the farthest reached task */
+            rb_bfs(edges, ip, inc, hub, node, (int32_t)a, tasks[0], tasks, nt, dist, queue, vis, stamp++);
+            int64_t seed = tasks[0];
+            for (int64_t j = 0; j < nt; j++) {
+                int64_t t = tasks[j];
+                if (dist[t] != INF64 && dist[t] > dist[seed]) seed = t;   /* ascending j: smallest id on ties */
+            }
+            /* BFS 2 from the seed; order by (dist, id); the first N0 tasks form child 2a */
+            rb_bfs(edges, ip, inc, hub, node, (int32_t)a, seed, tasks, nt, dist, queue, vis, stamp++);
+            rb_sort_dist = dist;
+            qsort(tasks, (size_t)nt, sizeof(int64_t), cmp_dist_id);
+            for (int64_t j = 0; j < nt; j++) next[tasks[j]] = (int32_t)(2 * a + (j < N0 ? 0 : 1));
+        }
+        for (int64_t t = 0; t < m; t++) node[t] = next[t];
+    }
+    /* leaves: EPG-2 on each leaf's tasks (ascending id), original endpoints */
+    const int64_t leaves = (int64_t)1 << d;
+    int32_t *sedges = (int32_t *)malloc(sizeof(int32_t) * 2 * m);
+    int32_t *sub = (int32_t *)malloc(sizeof(int32_t) * m);
+    int st = ORC_OK;
+    for (int64_t j = 0; j < leaves && st == ORC_OK; j++) {
+        int64_t nt = 0;
+        for (int64_t t = 0; t < m; t++)
+            if (node[t] == j) { tasks[nt] = t; sedges[2 * nt] = edges[2 * t]; sedges[2 * nt + 1] = edges[2 * t + 1]; nt++; }
+        const int64_t p0 = j * k / leaves, p1 = (j + 1) * k / leaves;
+        if (nt == 0) continue;
+        st = orc_epg2(nt, sedges, n, s + p0, p1 - p0, hub, sub);
+        for (int64_t q = 0; q < nt; q++) part[tasks[q]] = (int32_t)(sub[q] + p0);
+    }
+    free(s); free(S); free(ip); free(inc); free(node); free(next); free(dist); free(queue); free(tasks); free(vis);
+    free(sedges); free(sub);
+    return st;
+}
+
+/* ------------------------------------------------------------------------- */
 /* O6. Remap: task reorganisation + cpack data layout*/
 /*  1. new edge order = sort by (part, original id) -> edge_perm (new->old), */
 /*     part_edge_begin;                                                      */
@@ -606,6 +754,29 @@ void orc_cfd_flux(const int32_t *edges, int64_t m, int32_t n, const float *norma
     }
 }
 
+/* Scale of the flux sum for the componentwise parity metric of reading Z14:          */
+/* S[v][j] = sum over edges e incident to v of |Phi_e[j]| (the same per-edge Phi as     */
+/* orc_cfd_flux). |F_gpu - F_ref| <= (a few eps_32) * S bounds the reordered fp32 sum.  */
+void orc_cfd_flux_abs(const int32_t *edges, int64_t m, int32_t n, const float *normals, const float *U, double *S) {
+    for (int64_t v = 0; v < (int64_t)n * 5; v++) S[v] = 0.0;
+    for (int64_t e = 0; e < m; e++) {
+        int32_t a = edges[2 * e], b = edges[2 * e + 1];
+        double nv[3] = {normals[3 * e], normals[3 * e + 1], normals[3 * e + 2]};
+        double Ua[5], Ub[5], ua[3], ub[3], pa, pb, ca, cb, sa, sb, Ga[5], Gb[5];
+        cfd_vertex(U + 5 * (int64_t)a, Ua, ua, &pa, &ca, &sa);
+        cfd_vertex(U + 5 * (int64_t)b, Ub, ub, &pb, &cb, &sb);
+        cfd_flux_dot(Ua, ua, pa, nv, Ga);
+        cfd_flux_dot(Ub, ub, pb, nv, Gb);
+        double nlen = sqrt(nv[0] * nv[0] + nv[1] * nv[1] + nv[2] * nv[2]);
+        double f = -nlen * ORC_SIGMA * 0.5 * (sa + sb + ca + cb);
+        for (int j = 0; j < 5; j++) {
+            double phi = f * (Ua[j] - Ub[j]) - 0.5 * (Ga[j] + Gb[j]);
+            S[5 * (int64_t)a + j] += fabs(phi);
+            S[5 * (int64_t)b + j] += fabs(phi);
+        }
+    }
+}
+
 void orc_cfd_step(const int32_t *edges, int64_t m, int32_t n, const float *normals, const float *U,
                   const float *dt, double *Uout, double *F) {
     orc_cfd_flux(edges, m, n, normals, U, F);
@@ -615,6 +786,65 @@ void orc_cfd_step(const int32_t *edges, int64_t m, int32_t n, const float *norma
         for (int j = 0; j < 5; j++)
             Uout[5 * v + j] = (double)U[5 * v + j] + (touched[v] ? (double)dt[v] * F[5 * v + j] : 0.0);
     free(touched);
+}
+
+/* The same time step over all host cores, for the CPU baseline's timing only (SURVEY    */
+/* 8(d): "OpenMP over all host cores. Per-thread private accumulators are used"): the    */
+/* edges are split into contiguous ranges, each thread accumulates orc_cfd_flux's Phi of  */
+/* its range into a private F, the private arrays are summed, then U' = U + dt F. Same    */
+/* arithmetic per edge as orc_cfd_flux; only the summation order of F differs. Returns    */
+/* the thread count used (1 when built without OpenMP).                                  */
+int orc_cfd_step_omp(const int32_t *edges, int64_t m, int32_t n, const float *normals, const float *U,
+                     const float *dt, double *Uout, double *F) {
+    int nth = 1;
+#ifdef _OPENMP
+    nth = omp_get_max_threads();
+#endif
+    double *priv = (double *)calloc((size_t)nth * (size_t)n * 5, sizeof(double));
+    unsigned char *touched = (unsigned char *)calloc((size_t)n, 1);
+#ifdef _OPENMP
+#pragma omp parallel num_threads(nth)
+#endif
+    {
+        int tid = 0;
+#ifdef _OPENMP
+        tid = omp_get_thread_num();
+#endif
+        double *Fp = priv + (size_t)tid * (size_t)n * 5;
+        int64_t e0 = m * tid / nth, e1 = m * (tid + 1) / nth;
+        for (int64_t e = e0; e < e1; e++) {
+            int32_t a = edges[2 * e], b = edges[2 * e + 1];
+            double nv[3] = {normals[3 * e], normals[3 * e + 1], normals[3 * e + 2]};
+            double Ua[5], Ub[5], ua[3], ub[3], pa, pb, ca, cb, sa, sb, Ga[5], Gb[5];
+            cfd_vertex(U + 5 * (int64_t)a, Ua, ua, &pa, &ca, &sa);
+            cfd_vertex(U + 5 * (int64_t)b, Ub, ub, &pb, &cb, &sb);
+            cfd_flux_dot(Ua, ua, pa, nv, Ga);
+            cfd_flux_dot(Ub, ub, pb, nv, Gb);
+            double nlen = sqrt(nv[0] * nv[0] + nv[1] * nv[1] + nv[2] * nv[2]);
+            double f = -nlen * ORC_SIGMA * 0.5 * (sa + sb + ca + cb);
+            for (int j = 0; j < 5; j++) {
+                double phi = f * (Ua[j] - Ub[j]) - 0.5 * (Ga[j] + Gb[j]);
+                Fp[5 * (int64_t)a + j] += phi;
+                Fp[5 * (int64_t)b + j] -= phi;
+            }
+            touched[a] = 1;
+            touched[b] = 1;
+        }
+    }
+#ifdef _OPENMP
+#pragma omp parallel for num_threads(nth)
+#endif
+    for (int64_t v = 0; v < n; v++) {
+        for (int j = 0; j < 5; j++) {
+            double acc = 0.0;
+            for (int t = 0; t < nth; t++) acc += priv[(size_t)t * (size_t)n * 5 + 5 * v + j];
+            F[5 * v + j] = acc;
+            Uout[5 * v + j] = (double)U[5 * v + j] + (touched[v] ? (double)dt[v] * acc : 0.0);
+        }
+    }
+    free(priv);
+    free(touched);
+    return nth;
 }
 
 /* GATHER_SCATTER (config C4): y_a += w_e x_b, y_b += w_e x_a (w = 1 if NULL).  */

@@ -295,7 +295,9 @@ epg_status epg_adaptive_create(epg_ctx *ctx, epg_kernel kernel, const int32_t *e
     if ((e = cudaStreamSynchronize(ad->stream))) return fail("adaptive_create", e);
     // the optimisation thread (host only; never touches the context or the device)
     ad->part_h.assign((size_t)m, 0);
-    const int32_t method = epg::ctx_partition_method(ctx);
+    // (EPG-RB bisects on the device; this thread stays on the host and runs EPG-2 instead)
+    const int32_t method = epg::ctx_partition_method(ctx) == EPG_PARTITION_RB ? EPG_PARTITION_EPG2
+                                                                               : epg::ctx_partition_method(ctx);
     ad->worker = std::thread([ad, method] {
         const auto t0 = std::chrono::steady_clock::now();
         ad->part_status = epg::host_partition(ad->edges_h.data(), ad->m, ad->n, ad->part_size, 1, ad->part_h.data(),

@@ -3,9 +3,13 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <type_traits>
 #include <map>
+#include <memory>
 #include <queue>
+#include <thread>
 #include <climits>
 #include <cstdlib>
 #include <cstring>
@@ -17,6 +21,7 @@
 #include "run_kernels.cuh"
 #include "pipelined_kernel.cuh"
 #include "occupancy_kernel.cuh"
+#include "rb_kernels.cuh"
 
 // epg_run_host's pipeline (ctx-owned): copy-in and copy-out streams beside the ctx stream,
 // double-buffered staging so call i+1's H2D and call i's D2H overlap the compute.
@@ -175,6 +180,10 @@ struct Tmp {
         if (p) cudaFreeAsync(p, ctx->stream);
     }
     cudaError_t alloc(size_t bytes) { return cudaMallocAsync(&p, std::max<size_t>(bytes, 16), ctx->stream); }
+    void release() {
+        if (p) cudaFreeAsync(p, ctx->stream);
+        p = nullptr;
+    }
     template <class T> T *as() { return static_cast<T *>(p); }
 };
 
@@ -1068,6 +1077,283 @@ epg_status run_graphed(epg_ctx *ctx, epg_plan *pl, epg_kernel kernel, epg_state 
     return EPG_OK;
 }
 
+// ---- EPG-RB (O5'', reading Z21): GPU bisection levels ------------------------------------
+int rb_depth(int64_t k, int32_t shards, int32_t leaf_parts) {
+    int d = 0;
+    while ((1 << d) < shards) d++;
+    while (d < 10 && (int64_t)leaf_parts * ((int64_t)1 << (d + 1)) <= k) d++;
+    return d;
+}
+
+// One BFS pass over every node of a level at once (rb_kernels.cuh): levels are launched in
+// chunks of kRbChunk with device-side frontier counts, one host round trip per chunk.
+// front/next: [m] each; cnt: [kRbChunk + 1] device counters.
+constexpr int kRbChunk = 32;
+epg_status rb_bfs(epg_ctx *ctx, const int32_t *edges, const int32_t *ip, const int32_t *inc, int32_t hub,
+                  const int32_t *node, int32_t nodes, int32_t *dist, unsigned long long *vis, bool bits,
+                  unsigned long long pass, int32_t *front, int32_t *next, int32_t *cnt, int64_t nfront, int64_t m,
+                  int grid) {
+    int32_t level = 0;
+    while (nfront > 0) {
+        if ((uint32_t)level + kRbChunk + 2 >= kRbDistCap)
+            return ctx->fail(EPG_ERR_INFEASIBLE, "partition (RB): BFS depth exceeds 2^22");
+        const int32_t nf32 = (int32_t)nfront;
+        CU(cudaMemsetAsync(cnt + 1, 0, sizeof(int32_t) * kRbChunk, ctx->stream));
+        CU(cudaMemcpyAsync(cnt, &nf32, sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+        for (int c = 0; c < kRbChunk; c++) {
+            k_rb_expand<<<grid, kThreads, 0, ctx->stream>>>(edges, ip, inc, hub, node, nodes, dist, vis, bits, pass,
+                                                            front, cnt + c, next, cnt + c + 1, level + c);
+            std::swap(front, next);
+        }
+        CHECK_LAUNCH();
+        int32_t h = 0;
+        CU(cudaMemcpyAsync(&h, cnt + kRbChunk, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));   // (also keeps nf32 alive for its copy)
+        if (h < 0 || h > m) return ctx->fail(EPG_ERR_STATE, "partition (RB): frontier overflow");
+        nfront = h;
+        level += kRbChunk;
+    }
+    return EPG_OK;
+}
+
+double rb_now() { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); }
+
+// Leaf of every task after the bisection levels (leaf_d [m], DEVICE); *depth_out = d.
+epg_status rb_bisect(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, int32_t P, int32_t shards,
+                     int32_t leaf_parts, int32_t *leaf_d, int *depth_out) {
+    const int64_t k = (m + P - 1) / P;
+    const int d = rb_depth(k, shards, leaf_parts);
+    *depth_out = d;
+    if (d == 0) {
+        CU(cudaMemsetAsync(leaf_d, 0, sizeof(int32_t) * m, ctx->stream));
+        return EPG_OK;
+    }
+    std::vector<int64_t> S(k + 1, 0);
+    for (int64_t i = 0; i < k; i++) S[i + 1] = S[i] + m / k + (i < m % k ? 1 : 0);
+    const int32_t hub = 4 * P;
+    // incidence: vertex -> tasks, ascending (stable sort of the task-ordered endpoint slots)
+    Tmp key(ctx), val(ctx), skey(ctx), inc(ctx), ip(ctx), temp(ctx);
+    CU(key.alloc(sizeof(int32_t) * 2 * m));
+    CU(val.alloc(sizeof(int32_t) * 2 * m));
+    CU(skey.alloc(sizeof(int32_t) * 2 * m));
+    CU(inc.alloc(sizeof(int32_t) * 2 * m));
+    CU(ip.alloc(sizeof(int32_t) * ((int64_t)n + 1)));
+    k_rb_slot_keys<<<grid_for(2 * m), kThreads, 0, ctx->stream>>>(edges, m, n, key.as<int32_t>(), val.as<int32_t>());
+    CHECK_LAUNCH();
+    {
+        size_t tb = 0;
+        CU(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.as<int32_t>(), skey.as<int32_t>(), val.as<int32_t>(),
+                                           inc.as<int32_t>(), (int)(2 * m), 0, bits_for(n), ctx->stream));
+        CU(temp.alloc(tb));
+        CU(cub::DeviceRadixSort::SortPairs(temp.p, tb, key.as<int32_t>(), skey.as<int32_t>(), val.as<int32_t>(),
+                                           inc.as<int32_t>(), (int)(2 * m), 0, bits_for(n), ctx->stream));
+    }
+    k_rb_offsets<<<grid_for((int64_t)n + 1), kThreads, 0, ctx->stream>>>(skey.as<int32_t>(), 2 * m, n, ip.as<int32_t>());
+    CHECK_LAUNCH();
+    // per-task state; the slot buffers are reused for the level sorts
+    Tmp node(ctx), nnode(ctx), dist(ctx), front(ctx), next(ctx), vis(ctx), cnt(ctx), nmin(ctx), far(ctx), nb(ctx),
+        n0(ctx), stemp(ctx);
+    CU(node.alloc(sizeof(int32_t) * m));
+    CU(nnode.alloc(sizeof(int32_t) * m));
+    CU(dist.alloc(sizeof(int32_t) * m));
+    CU(front.alloc(sizeof(int32_t) * m));
+    CU(next.alloc(sizeof(int32_t) * m));
+    // per-(vertex, node) expansion bitmap of the deepest level, if it fits 16 GiB
+    const uint64_t vis_words_max = ((uint64_t)n * (uint64_t)(1 << (d - 1)) + 63) / 64;
+    const bool bits = vis_words_max * 8 <= (16ull << 30);
+    CU(vis.alloc(sizeof(unsigned long long) * (bits ? vis_words_max : (uint64_t)n)));
+    CU(cnt.alloc(sizeof(int32_t) * (kRbChunk + 1)));
+    int sms = 0;
+    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    const int grid = sms * 8;
+    CU(nmin.alloc(sizeof(int32_t) << d));
+    CU(far.alloc(sizeof(unsigned long long) << d));
+    CU(nb.alloc(sizeof(int64_t) << d));
+    CU(n0.alloc(sizeof(int64_t) << d));
+    CU(cudaMemsetAsync(node.p, 0, sizeof(int32_t) * m, ctx->stream));
+    if (!bits) CU(cudaMemsetAsync(vis.p, 0, sizeof(unsigned long long) * n, ctx->stream));
+    Tmp vals2(ctx);
+    CU(vals2.alloc(sizeof(int32_t) * m));
+    uint32_t *skeys = reinterpret_cast<uint32_t *>(key.p), *skeys2 = reinterpret_cast<uint32_t *>(skey.p);
+    int32_t *svals = val.as<int32_t>(), *svals2 = vals2.as<int32_t>();
+    size_t stb = 0;
+    CU(cub::DeviceRadixSort::SortPairs(nullptr, stb, skeys, skeys2, svals, svals2, (int)m, 0, 32, ctx->stream));
+    CU(stemp.alloc(stb));
+    unsigned long long pass = 0;
+    epg_status st;
+    for (int l = 0; l < d; l++) {
+        const int32_t nodes = 1 << l;
+        std::vector<int64_t> begin_h(nodes), n0_h(nodes);
+        for (int64_t a = 0; a < nodes; a++) {
+            const int64_t lo = a * k / nodes, mid = (2 * a + 1) * k / (2 * nodes);
+            begin_h[a] = S[lo];
+            n0_h[a] = S[mid] - S[lo];
+        }
+        // pass 1: from each node's smallest task id
+        k_rb_init_dist<<<grid_for(m), kThreads, 0, ctx->stream>>>(dist.as<int32_t>(), m);
+        k_fill<int32_t><<<grid_for(nodes), kThreads, 0, ctx->stream>>>(nmin.as<int32_t>(), nodes, INT32_MAX);
+        k_rb_node_min<<<grid, kThreads, sizeof(int32_t) * nodes, ctx->stream>>>(node.as<int32_t>(), m, nodes,
+                                                                                 nmin.as<int32_t>());
+        k_rb_sources<<<grid_for(nodes), kThreads, 0, ctx->stream>>>(nmin.as<int32_t>(), far.as<unsigned long long>(),
+                                                                    nodes, 0, dist.as<int32_t>(), front.as<int32_t>());
+        CHECK_LAUNCH();
+        if (bits)
+            CU(cudaMemsetAsync(vis.p, 0, sizeof(unsigned long long) * (((uint64_t)n * nodes + 63) / 64), ctx->stream));
+        if ((st = rb_bfs(ctx, edges, ip.as<int32_t>(), inc.as<int32_t>(), hub, node.as<int32_t>(), nodes,
+                         dist.as<int32_t>(), vis.as<unsigned long long>(), bits, ++pass, front.as<int32_t>(),
+                         next.as<int32_t>(), cnt.as<int32_t>(), nodes, m, grid)))
+            return st;
+        // pass 2: from each node's farthest reached task (ties: smallest id)
+        CU(cudaMemsetAsync(far.p, 0, sizeof(unsigned long long) * nodes, ctx->stream));
+        k_rb_far_key<<<grid, kThreads, sizeof(unsigned long long) * nodes, ctx->stream>>>(
+            node.as<int32_t>(), dist.as<int32_t>(), m, nodes, far.as<unsigned long long>());
+        k_rb_init_dist<<<grid_for(m), kThreads, 0, ctx->stream>>>(dist.as<int32_t>(), m);
+        k_rb_sources<<<grid_for(nodes), kThreads, 0, ctx->stream>>>(nmin.as<int32_t>(), far.as<unsigned long long>(),
+                                                                    nodes, 1, dist.as<int32_t>(), front.as<int32_t>());
+        CHECK_LAUNCH();
+        if (bits)
+            CU(cudaMemsetAsync(vis.p, 0, sizeof(unsigned long long) * (((uint64_t)n * nodes + 63) / 64), ctx->stream));
+        if ((st = rb_bfs(ctx, edges, ip.as<int32_t>(), inc.as<int32_t>(), hub, node.as<int32_t>(), nodes,
+                         dist.as<int32_t>(), vis.as<unsigned long long>(), bits, ++pass, front.as<int32_t>(),
+                         next.as<int32_t>(), cnt.as<int32_t>(), nodes, m, grid)))
+            return st;
+        // order (node, dist, id) and cut every node after its first half's task count
+        k_rb_sort_keys<<<grid_for(m), kThreads, 0, ctx->stream>>>(node.as<int32_t>(), dist.as<int32_t>(), m, skeys,
+                                                                  svals);
+        CHECK_LAUNCH();
+        CU(cub::DeviceRadixSort::SortPairs(stemp.p, stb, skeys, skeys2, svals, svals2, (int)m, 0,
+                                           kRbDistBits + bits_for(nodes), ctx->stream));
+        CU(cudaMemcpyAsync(nb.p, begin_h.data(), sizeof(int64_t) * nodes, cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaMemcpyAsync(n0.p, n0_h.data(), sizeof(int64_t) * nodes, cudaMemcpyHostToDevice, ctx->stream));
+        k_rb_split<<<grid_for(m), kThreads, 0, ctx->stream>>>(skeys2, svals2, m, nb.as<int64_t>(), n0.as<int64_t>(),
+                                                              nnode.as<int32_t>());
+        CHECK_LAUNCH();
+        CU(cudaStreamSynchronize(ctx->stream));   // begin_h / n0_h are host vectors
+        std::swap(node.p, nnode.p);
+    }
+    CU(cudaMemcpyAsync(leaf_d, node.p, sizeof(int32_t) * m, cudaMemcpyDeviceToDevice, ctx->stream));
+    return EPG_OK;
+}
+
+// EPG-RB end to end on the device edges: bisection levels (GPU), leaf grouping and leaf-local
+// vertex ids (GPU), EPG-2 per leaf (host threads), scatter of the map (GPU) into part_d.
+epg_status rb_partition(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, int32_t P, int32_t shards,
+                        int32_t leaf_parts, int32_t *part_d, std::string *err) {
+    const bool trace = std::getenv("EPG_RB_TRACE") != nullptr;
+    double t0 = rb_now();
+    auto mark = [&](const char *what) {
+        if (!trace) return;
+        cudaStreamSynchronize(ctx->stream);
+        const double t = rb_now();
+        std::fprintf(stderr, "[epg rb] %-28s %8.3f s\n", what, t - t0);
+        t0 = t;
+    };
+    const int64_t k = (m + P - 1) / P;
+    Tmp leaf(ctx);
+    CU(leaf.alloc(sizeof(int32_t) * m));
+    int d = 0;
+    epg_status st = rb_bisect(ctx, edges, m, n, P, shards, leaf_parts, leaf.as<int32_t>(), &d);
+    if (st) return st;
+    mark("bisection levels (GPU)");
+    const int32_t leaves = 1 << d;
+    std::vector<int64_t> S(k + 1, 0), slot_begin(leaves + 1);
+    for (int64_t i = 0; i < k; i++) S[i + 1] = S[i] + m / k + (i < m % k ? 1 : 0);
+    for (int64_t j = 0; j <= leaves; j++) slot_begin[j] = 2 * S[j * k / leaves];
+    Tmp key(ctx), skey(ctx), val(ctx), sval(ctx), flag(ctx), incl(ctx), local(ctx), sb(ctx), nloc(ctx), temp(ctx),
+        order(ctx), iota(ctx), lkey(ctx), grouped(ctx), pl(ctx);
+    const int64_t len = 2 * m;
+    CU(key.alloc(sizeof(unsigned long long) * len));
+    CU(skey.alloc(sizeof(unsigned long long) * len));
+    CU(val.alloc(sizeof(int32_t) * len));
+    CU(sval.alloc(sizeof(int32_t) * len));
+    CU(sb.alloc(sizeof(int64_t) * (leaves + 1)));
+    CU(nloc.alloc(sizeof(int32_t) * leaves));
+    CU(cudaMemcpyAsync(sb.p, slot_begin.data(), sizeof(int64_t) * (leaves + 1), cudaMemcpyHostToDevice, ctx->stream));
+    k_rb_leaf_slot_keys<<<grid_for(len), kThreads, 0, ctx->stream>>>(edges, m, leaf.as<int32_t>(),
+                                                                     key.as<unsigned long long>(), val.as<int32_t>());
+    CHECK_LAUNCH();
+    {
+        size_t tb = 0;
+        const int eb = 32 + bits_for(leaves);
+        CU(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.as<unsigned long long>(), skey.as<unsigned long long>(),
+                                           val.as<int32_t>(), sval.as<int32_t>(), (int)len, 0, eb, ctx->stream));
+        CU(temp.alloc(tb));
+        CU(cub::DeviceRadixSort::SortPairs(temp.p, tb, key.as<unsigned long long>(), skey.as<unsigned long long>(),
+                                           val.as<int32_t>(), sval.as<int32_t>(), (int)len, 0, eb, ctx->stream));
+    }
+    key.release();
+    CU(flag.alloc(sizeof(int32_t) * len));
+    CU(incl.alloc(sizeof(int32_t) * len));
+    k_rb_heads<<<grid_for(len), kThreads, 0, ctx->stream>>>(skey.as<unsigned long long>(), len, flag.as<int32_t>());
+    CHECK_LAUNCH();
+    {
+        Tmp t2(ctx);
+        size_t tb = 0;
+        CU(cub::DeviceScan::InclusiveSum(nullptr, tb, flag.as<int32_t>(), incl.as<int32_t>(), (int)len, ctx->stream));
+        CU(t2.alloc(tb));
+        CU(cub::DeviceScan::InclusiveSum(t2.p, tb, flag.as<int32_t>(), incl.as<int32_t>(), (int)len, ctx->stream));
+    }
+    CU(local.alloc(sizeof(int32_t) * len));
+    k_rb_local_ids<<<grid_for(len), kThreads, 0, ctx->stream>>>(skey.as<unsigned long long>(), sval.as<int32_t>(),
+                                                                incl.as<int32_t>(), len, sb.as<int64_t>(),
+                                                                local.as<int32_t>());
+    k_rb_nlocal<<<grid_for(leaves), kThreads, 0, ctx->stream>>>(incl.as<int32_t>(), sb.as<int64_t>(), leaves,
+                                                                nloc.as<int32_t>());
+    CHECK_LAUNCH();
+    // tasks grouped by leaf, ascending inside (stable sort of the task-ordered leaf ids)
+    CU(order.alloc(sizeof(int32_t) * m));
+    CU(iota.alloc(sizeof(int32_t) * m));
+    CU(lkey.alloc(sizeof(int32_t) * m));
+    k_iota<<<grid_for(m), kThreads, 0, ctx->stream>>>(iota.as<int32_t>(), m);
+    {
+        Tmp t2(ctx);
+        size_t tb = 0;
+        CU(cub::DeviceRadixSort::SortPairs(nullptr, tb, leaf.as<int32_t>(), lkey.as<int32_t>(), iota.as<int32_t>(),
+                                           order.as<int32_t>(), (int)m, 0, std::max(1, d), ctx->stream));
+        CU(t2.alloc(tb));
+        CU(cub::DeviceRadixSort::SortPairs(t2.p, tb, leaf.as<int32_t>(), lkey.as<int32_t>(), iota.as<int32_t>(),
+                                           order.as<int32_t>(), (int)m, 0, std::max(1, d), ctx->stream));
+    }
+    CU(grouped.alloc(sizeof(int32_t) * len));
+    k_rb_group_edges<<<grid_for(m), kThreads, 0, ctx->stream>>>(order.as<int32_t>(), m, local.as<int32_t>(),
+                                                                grouped.as<int32_t>());
+    CHECK_LAUNCH();
+    std::vector<int32_t> nl(leaves);
+    CU(cudaMemcpyAsync(nl.data(), nloc.p, sizeof(int32_t) * leaves, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    mark("leaf grouping + local ids");
+    // the grouped edges stream to the host in leaf order (a copy thread, chunk by chunk)
+    // while the leaf workers start on the chunks that have arrived
+    std::unique_ptr<int32_t[]> ge(new int32_t[len]), part_local(new int32_t[m]);
+    std::atomic<int32_t> ready{0};
+    cudaError_t copy_err = cudaSuccess;
+    std::thread copier([&]() {
+        cudaSetDevice(ctx->device);
+        const int chunks = std::min<int32_t>(leaves, 16);
+        for (int c = 0; c < chunks; c++) {
+            const int32_t j0 = (int32_t)((int64_t)c * leaves / chunks), j1 = (int32_t)((int64_t)(c + 1) * leaves / chunks);
+            const int64_t a = slot_begin[j0], b = slot_begin[j1];
+            if (b > a && copy_err == cudaSuccess)
+                copy_err = cudaMemcpy(ge.get() + a, grouped.as<int32_t>() + a, sizeof(int32_t) * (b - a),
+                                      cudaMemcpyDeviceToHost);
+            ready.store(copy_err == cudaSuccess ? j1 : leaves, std::memory_order_release);
+        }
+    });
+    st = epg::rb_leaves(ge.get(), m, nl.data(), leaves, P, part_local.get(), err, 0, &ready);
+    copier.join();
+    if (copy_err != cudaSuccess) return ctx->fail(EPG_ERR_CUDA, std::string("partition (RB): ") +
+                                                                cudaGetErrorString(copy_err));
+    if (st) return st;
+    mark("copy-out + EPG-2 leaves (host)");
+    CU(pl.alloc(sizeof(int32_t) * m));
+    CU(cudaMemcpyAsync(pl.p, part_local.get(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx->stream));
+    k_rb_scatter<<<grid_for(m), kThreads, 0, ctx->stream>>>(order.as<int32_t>(), pl.as<int32_t>(), m, part_d);
+    CHECK_LAUNCH();
+    CU(cudaStreamSynchronize(ctx->stream));   // part_local is a host vector
+    mark("scatter");
+    return EPG_OK;
+}
+
 }  // namespace
 
 // =====================================================================================
@@ -1114,25 +1400,18 @@ void epg_destroy(epg_ctx *ctx) {
 
 const char *epg_last_error(const epg_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
-epg_status epg_partition(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, int32_t part_size,
-                         int32_t shards, int32_t *part_of_edge, epg_report *out) {
-    if (!ctx) return EPG_ERR_STATE;
+}  // extern "C"
+
+namespace {
+// epg_partition / epg_partition_rb: host partitioner (or, for EPG-RB, GPU bisection levels +
+// host leaves), then the GPU cost function on the map
+epg_status partition_impl(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, int32_t part_size, int32_t shards,
+                          int32_t method, int32_t leaf_parts, int32_t *part_of_edge, epg_report *out) {
     if (!edges || !part_of_edge || !out || m <= 0 || n <= 0)
         return ctx->fail(EPG_ERR_INPUT, "partition: need m > 0, n > 0 and non-NULL arrays");
+    if (m >= kMaxEdges) return ctx->fail(EPG_ERR_INPUT, "partition: m must be below 2^30");
     CU(cudaSetDevice(ctx->device));
     const bool edges_dev = is_device_ptr(edges), part_dev = is_device_ptr(part_of_edge);
-    std::vector<int32_t> eh, ph(m);
-    const int32_t *edges_h = edges;
-    if (edges_dev) {
-        eh.resize(2 * m);
-        CU(cudaMemcpyAsync(eh.data(), edges, sizeof(int32_t) * 2 * m, cudaMemcpyDeviceToHost, ctx->stream));
-        CU(cudaStreamSynchronize(ctx->stream));
-        edges_h = eh.data();
-    }
-    std::string err;
-    epg_status st = epg::host_partition(edges_h, m, n, part_size, shards, ph.data(), &err, nullptr,
-                                        ctx->partition_method);
-    if (st) return ctx->fail(st, err);
     Tmp ed(ctx), pd(ctx);
     const int32_t *edges_d = edges;
     if (!edges_dev) {
@@ -1142,12 +1421,62 @@ epg_status epg_partition(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t 
     }
     int32_t *part_d = part_of_edge;
     if (!part_dev) {
-        std::memcpy(part_of_edge, ph.data(), sizeof(int32_t) * m);
         CU(pd.alloc(sizeof(int32_t) * m));
         part_d = pd.as<int32_t>();
     }
-    CU(cudaMemcpyAsync(part_d, ph.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx->stream));
+    std::string err;
+    epg_status st;
+    if (method == EPG_PARTITION_RB) {
+        if (leaf_parts < 1) return ctx->fail(EPG_ERR_INPUT, "partition (RB): leaf_parts must be >= 1");
+        if ((st = validate(ctx, edges_d, m, n, nullptr, 0))) return st;
+        if (part_size < 1 || part_size > EPG_MAX_PART_SIZE)
+            return ctx->fail(EPG_ERR_INFEASIBLE, "partition: part_size must be in [1, 4096]");
+        const int64_t k = epg_num_parts(m, part_size);
+        if (!(shards == 1 || shards == 2 || shards == 4 || shards == 8) || shards > k)
+            return ctx->fail(EPG_ERR_INFEASIBLE, "partition: shards must be 1, 2, 4 or 8 and at most k");
+        if ((st = rb_partition(ctx, edges_d, m, n, part_size, shards, leaf_parts, part_d, &err)))
+            return err.empty() ? st : ctx->fail(st, err);
+        if (!part_dev) {
+            CU(cudaMemcpyAsync(part_of_edge, part_d, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, ctx->stream));
+            CU(cudaStreamSynchronize(ctx->stream));
+        }
+    } else {
+        std::vector<int32_t> eh, ph(m);
+        const int32_t *edges_h = edges;
+        if (edges_dev) {
+            eh.resize(2 * m);
+            CU(cudaMemcpyAsync(eh.data(), edges, sizeof(int32_t) * 2 * m, cudaMemcpyDeviceToHost, ctx->stream));
+            CU(cudaStreamSynchronize(ctx->stream));
+            edges_h = eh.data();
+        }
+        st = epg::host_partition(edges_h, m, n, part_size, shards, ph.data(), &err, nullptr, method);
+        if (st) return ctx->fail(st, err);
+        if (!part_dev) std::memcpy(part_of_edge, ph.data(), sizeof(int32_t) * m);
+        CU(cudaMemcpyAsync(part_d, ph.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));   // ph is a host vector
+    }
     return load_count_dev(ctx, edges_d, m, n, part_d, epg_num_parts(m, part_size), nullptr, out);
+}
+
+int rb_leaf_parts_default() {
+    const char *e = std::getenv("EPG_RB_LEAF_PARTS");
+    return e ? std::max(1, std::atoi(e)) : 512;
+}
+}  // namespace
+
+extern "C" {
+
+epg_status epg_partition(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, int32_t part_size,
+                         int32_t shards, int32_t *part_of_edge, epg_report *out) {
+    if (!ctx) return EPG_ERR_STATE;
+    return partition_impl(ctx, edges, m, n, part_size, shards, ctx->partition_method, rb_leaf_parts_default(),
+                          part_of_edge, out);
+}
+
+epg_status epg_partition_rb(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, int32_t part_size,
+                            int32_t shards, int32_t leaf_parts, int32_t *part_of_edge, epg_report *out) {
+    if (!ctx) return EPG_ERR_STATE;
+    return partition_impl(ctx, edges, m, n, part_size, shards, EPG_PARTITION_RB, leaf_parts, part_of_edge, out);
 }
 
 epg_status epg_default_partition(epg_ctx *ctx, int64_t m, int32_t part_size, int32_t *part_of_edge) {
@@ -1701,8 +2030,8 @@ epg_status epg_set_variant(epg_ctx *ctx, int32_t variant) {
 
 epg_status epg_set_partition_method(epg_ctx *ctx, int32_t method) {
     if (!ctx) return EPG_ERR_STATE;
-    if (method != EPG_PARTITION_EPG1 && method != EPG_PARTITION_EPG2)
-        return ctx->fail(EPG_ERR_INPUT, "set_partition_method: 1 (EPG-1) or 2 (EPG-2)");
+    if (method != EPG_PARTITION_EPG1 && method != EPG_PARTITION_EPG2 && method != EPG_PARTITION_RB)
+        return ctx->fail(EPG_ERR_INPUT, "set_partition_method: 1 (EPG-1), 2 (EPG-2) or 3 (EPG-RB)");
     ctx->partition_method = method;
     return EPG_OK;
 }

@@ -25,11 +25,14 @@
 //  with more than 4 x part_size tasks (hubs) attract none.
 #include "epg_internal.h"
 
+#include <sched.h>
+
 #include <algorithm>
 #include <atomic>
 #include <cstring>
 #include <queue>
 #include <string>
+#include <thread>
 #include <vector>
 
 namespace epg {
@@ -197,7 +200,8 @@ Incidence build_incidence(const int32_t *edges, int64_t m, int32_t n) {
 // whatever happens) attracts no tasks -- the hub discussion of P:642-683, reading Z20.
 bool grow_direct(const int32_t *edges, int64_t ntask, int32_t n, const int64_t *sizes, int64_t nparts, int64_t hub,
                  int32_t *part, const std::atomic<int> *cancel) {
-    const Incidence I = build_incidence(edges, ntask, n);
+    Incidence I = build_incidence(edges, ntask, n);
+    std::vector<int64_t> live_end(I.beg.begin() + 1, I.beg.end());   // end of v's live (unassigned) tasks
     std::vector<TaskState> st(ntask, TaskState{-1, kNoStamp, kNoStamp, 0});
     std::vector<int64_t> mark(static_cast<size_t>(n), 0);
     std::vector<int32_t> by_gst;
@@ -238,11 +242,16 @@ bool grow_direct(const int32_t *edges, int64_t ntask, int32_t n, const int64_t *
                 if (side == 1 && v == ends[0]) break;   // distinct endpoints only
                 if (mark[v] == i + 1) continue;         // already loaded by this partition
                 mark[v] = i + 1;
-                if (I.beg[v + 1] - I.beg[v] > hub) continue;
-                for (int64_t q = I.beg[v]; q < I.beg[v + 1]; q++) {
+                if (I.beg[v + 1] - I.beg[v] > hub) continue;   // the hub rule uses the full degree
+                // scan v's live tasks, dropping assigned ones from the list on the way (order
+                // kept, so the visit order is still ascending id: same result, and a
+                // high-degree vertex is not rescanned in full by every partition loading it)
+                int64_t wr = I.beg[v];
+                for (int64_t q = I.beg[v]; q < live_end[v]; q++) {
                     const int32_t w = I.task[q];
                     TaskState &u = st[w];
                     if (u.part != -1) continue;
+                    I.task[wr++] = w;
                     if (u.lst == kNoStamp) {
                         u.lst = clock++;
                         dirty.push_back(w);
@@ -251,6 +260,7 @@ bool grow_direct(const int32_t *edges, int64_t ntask, int32_t n, const int64_t *
                     if (u.gst == kNoStamp) { u.gst = gclock++; by_gst.push_back(w); }
                     fr.push(u.gain, u.lst, w);
                 }
+                live_end[v] = wr;
             }
         }
     }
@@ -259,8 +269,51 @@ bool grow_direct(const int32_t *edges, int64_t ntask, int32_t n, const int64_t *
 
 }  // namespace
 
+int host_cpus() {
+    cpu_set_t set;
+    if (sched_getaffinity(0, sizeof(set), &set) == 0) return std::max(1, CPU_COUNT(&set));
+    return std::max(1u, std::thread::hardware_concurrency());
+}
+
+epg_status rb_leaves(const int32_t *local_edges, int64_t m, const int32_t *n_local, int32_t leaves,
+                     int32_t part_size, int32_t *part_local, std::string *err, int threads,
+                     const std::atomic<int32_t> *ready) {
+    const int64_t k = (m + part_size - 1) / part_size;
+    std::vector<int64_t> s(k), S(k + 1, 0);
+    for (int64_t i = 0; i < k; i++) {
+        s[i] = m / k + (i < m % k ? 1 : 0);
+        S[i + 1] = S[i] + s[i];
+    }
+    const int64_t hub = 4 * static_cast<int64_t>(part_size);
+    std::atomic<int32_t> next_leaf{0};
+    auto worker = [&]() {
+        for (;;) {
+            const int32_t j = next_leaf.fetch_add(1);
+            if (j >= leaves) return;
+            const int64_t p0 = static_cast<int64_t>(j) * k / leaves, p1 = static_cast<int64_t>(j + 1) * k / leaves;
+            const int64_t b = S[p0], nt = S[p1] - S[p0];   // the leaf's tasks, grouped and ascending
+            if (nt == 0) continue;
+            if (ready)   // the leaf's edges are still being copied in
+                while (ready->load(std::memory_order_acquire) <= j) std::this_thread::yield();
+            grow_direct(local_edges + 2 * b, nt, n_local[j], s.data() + p0, p1 - p0, hub, part_local + b, nullptr);
+            for (int64_t q = 0; q < nt; q++) part_local[b + q] += static_cast<int32_t>(p0);
+        }
+    };
+    const int nth = std::max(1, std::min<int>(threads > 0 ? threads : host_cpus(), leaves));
+    std::vector<std::thread> pool;
+    for (int i = 1; i < nth; i++) pool.emplace_back(worker);
+    worker();
+    for (auto &th : pool) th.join();
+    (void)err;
+    return EPG_OK;
+}
+
 epg_status host_partition(const int32_t *edges, int64_t m, int32_t n, int32_t part_size, int32_t shards,
                           int32_t *part, std::string *err, const std::atomic<int> *cancel, int32_t method) {
+    if (method == EPG_PARTITION_RB) {
+        *err = "partition: EPG-RB bisects on the GPU -- use epg_partition / epg_partition_rb";
+        return EPG_ERR_INPUT;
+    }
     if (method != EPG_PARTITION_EPG1 && method != EPG_PARTITION_EPG2) {
         *err = "partition: method must be 1 (EPG-1) or 2 (EPG-2)";
         return EPG_ERR_INPUT;

@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("EPG_LIB_PATH", os.path.join(_HERE, "libepg.so"))
 
 OK, ERR_INPUT, ERR_INFEASIBLE, ERR_CUDA, ERR_NCCL, ERR_NOMEM, ERR_STATE = 0, 2, 3, 4, 5, 6, 7
 KERNEL_CFD_FLUX, KERNEL_GATHER_SCATTER, KERNEL_SPMV = 1, 2, 3
-PARTITION_EPG1, PARTITION_EPG2 = 1, 2
+PARTITION_EPG1, PARTITION_EPG2, PARTITION_RB = 1, 2, 3
 KERNELS = {"cfd": KERNEL_CFD_FLUX, "gather_scatter": KERNEL_GATHER_SCATTER, "spmv": KERNEL_SPMV}
 ROW = {KERNEL_CFD_FLUX: 5, KERNEL_GATHER_SCATTER: 1, KERNEL_SPMV: 1}
 MAX_PART_SIZE = 4096
@@ -34,7 +34,7 @@ SYMBOLS = ["epg_create", "epg_destroy", "epg_last_error", "epg_num_parts", "epg_
            "epg_set_exec_limits", "epg_partition_random_host", "epg_partition_greedy_host",
            "epg_adaptive_create", "epg_adaptive_step", "epg_adaptive_wait", "epg_adaptive_read_state",
            "epg_adaptive_info", "epg_adaptive_destroy", "epg_partition_host_method", "epg_set_partition_method",
-           "epg_run_host", "epg_run_host_join"]
+           "epg_run_host", "epg_run_host_join", "epg_partition_rb"]
 
 
 class _Report(C.Structure):
@@ -72,6 +72,7 @@ def _load():
         "epg_partition_host_method": (st, [P, i64, i32, i32, i32, i32, P, C.c_char_p, i64]),
         "epg_set_partition_method": (st, [P, i32]),
         "epg_partition": (st, [P, P, i64, i32, i32, i32, P, C.POINTER(_Report)]),
+        "epg_partition_rb": (st, [P, P, i64, i32, i32, i32, i32, P, C.POINTER(_Report)]),
         "epg_default_partition": (st, [P, i64, i32, P]),
         "epg_load_count": (st, [P, P, i64, i32, P, i64, P, C.POINTER(_Report)]),
         "epg_remap": (st, [P, P, i64, i32, P, i64, C.POINTER(_Layout), C.POINTER(P)]),
@@ -331,6 +332,17 @@ class Context:
             out = torch.empty(m, dtype=torch.int32, device=edges.device)
         r = _Report()
         self._check(lib.epg_partition(self.handle, _ptr(edges), m, n, part_size, shards, _ptr(out), C.byref(r)))
+        return out, _rep(r)
+
+    def partition_rb(self, edges: torch.Tensor, n: int, part_size: int, shards: int = 1, leaf_parts: int = 256,
+                     out: torch.Tensor | None = None):
+        """EPG-RB (epg_partition_rb): GPU bisection levels + EPG-2 leaves on the host cores."""
+        m = edges.shape[0]
+        if out is None:
+            out = torch.empty(m, dtype=torch.int32, device=edges.device)
+        r = _Report()
+        self._check(lib.epg_partition_rb(self.handle, _ptr(edges), m, n, part_size, shards, leaf_parts, _ptr(out),
+                                         C.byref(r)))
         return out, _rep(r)
 
     def default_partition(self, m: int, part_size: int) -> torch.Tensor:

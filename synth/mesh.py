@@ -107,6 +107,28 @@ def _normals(a, kind, N, h):
     return nrm
 
 
+def _normal_table(N, h):
+    """Area-normals of the three face kinds of the six Kuhn tets, out of the tet (float64
+    [18, 3], row 3q + kind). Every tet of permutation q is a translate of tet q of the
+    cube at the origin, so its faces have these normals (computed once, from the exact
+    corner at the origin, instead of per cell from rounded absolute coordinates)."""
+    q = np.repeat(np.arange(6, dtype=np.int64), 3)
+    kind = np.tile(np.array([0, 1, 2], dtype=np.int8), 6)
+    return _normals(q, kind, N, h)
+
+
+def _argsort_unique(keys: np.ndarray) -> np.ndarray:
+    """argsort of distinct int64 keys (any correct sort gives the same order): on the GPU
+    when one is present (the 64M-cell C3 mesh), else numpy."""
+    try:
+        import torch
+        if torch.cuda.is_available() and keys.size > (1 << 22):
+            return torch.sort(torch.from_numpy(keys).cuda(), stable=True)[1].cpu().numpy()
+    except ImportError:
+        pass
+    return np.argsort(keys, kind="stable")
+
+
 def kuhn_mesh(nbox: int, n_keep: int | None = None, seed: int = 1605, relabel: bool = True,
               chunk: int = 1 << 23) -> Mesh:
     N = int(nbox)
@@ -120,13 +142,14 @@ def kuhn_mesh(nbox: int, n_keep: int | None = None, seed: int = 1605, relabel: b
         new = np.empty(n, dtype=np.int64)
         new[order] = np.arange(n, dtype=np.int64)
         del order
+    table = _normal_table(N, h)
     los, his, nrms = [], [], []
     # faces are emitted from their first cell, which is < n when both cells are kept
     for c0 in range(0, n, chunk):
         a, b, kind = _faces(N, c0, min(n, c0 + chunk))
         keep = b < n
         a, b, kind = a[keep], b[keep], kind[keep]
-        nrm = _normals(a, kind, N, h)
+        nrm = table[(a % 6) * 3 + kind]
         if relabel:
             a, b = new[a], new[b]
         swap = a > b
@@ -138,7 +161,7 @@ def kuhn_mesh(nbox: int, n_keep: int | None = None, seed: int = 1605, relabel: b
     lo = np.concatenate(los); del los
     hi = np.concatenate(his); del his
     nrm = np.concatenate(nrms); del nrms
-    idx = np.argsort(lo.astype(np.int64) * n + hi, kind="stable")
+    idx = _argsort_unique(lo.astype(np.int64) * n + hi)
     edges = np.empty((lo.size, 2), dtype=np.int32)
     edges[:, 0] = lo[idx]
     edges[:, 1] = hi[idx]

@@ -44,4 +44,13 @@ def random_permutation(seed: int, n: int) -> np.ndarray:
     Sort by 64-bit SplitMix64 keys (ties broken by id, stable), so it is O(n log n)
     in numpy and reproducible on any machine."""
     keys = splitmix64(seed, np.arange(n, dtype=np.uint64))
+    try:
+        import torch
+        if torch.cuda.is_available() and n > (1 << 22):
+            # same order as numpy's stable argsort of the unsigned keys: flip the sign bit so
+            # that signed int64 order is unsigned order; stable, so equal keys keep id order
+            k = (keys ^ np.uint64(1 << 63)).view(np.int64)
+            return torch.sort(torch.from_numpy(k).cuda(), stable=True)[1].cpu().numpy().astype(np.int64)
+    except ImportError:
+        pass
     return np.argsort(keys, kind="stable").astype(np.int64)

@@ -196,3 +196,155 @@ def test_epg2_quality_on_cfd_mesh(mesh_c1):
     assert r2.max_size - r2.min_size <= 1
     assert r2.replication < r1.replication - 0.05
     assert rd.replication / r2.replication > 2.0
+
+
+# ------------------------------------------------------------------------------------
+# EPG-RB (O5'', reading Z21): recursive graph-growing bisection, EPG-2 in every leaf.
+def rb_python(edges, n, P, shards=1, leaf_parts=256):
+    """O5'' transcribed literally (pure Python, small inputs only)."""
+    from collections import deque
+    m = len(edges)
+    k = -(-m // P)
+    s = [m // k + (1 if i < m % k else 0) for i in range(k)]
+    S = [0]
+    for x in s:
+        S.append(S[-1] + x)
+    hub = 4 * P
+    d = 0
+    while (1 << d) < shards:
+        d += 1
+    while d < 10 and leaf_parts * (1 << (d + 1)) <= k:
+        d += 1
+    inc = [[] for _ in range(n)]
+    for t, (u, v) in enumerate(edges):
+        inc[u].append(t)
+        if v != u:
+            inc[v].append(t)
+    INF = float("inf")
+
+    def bfs(node, a, src):
+        dist = {t: INF for t in range(m) if node[t] == a}
+        dist[src] = 0
+        q = deque([src])
+        while q:
+            t = q.popleft()
+            for v in set(edges[t]):
+                if len(inc[v]) > hub:
+                    continue
+                for u in inc[v]:
+                    if node[u] == a and dist[u] == INF:
+                        dist[u] = dist[t] + 1
+                        q.append(u)
+        return dist
+
+    node = [0] * m
+    for lv in range(d):
+        nodes = 1 << lv
+        nxt = [None] * m
+        for a in range(nodes):
+            tasks = [t for t in range(m) if node[t] == a]
+            if not tasks:
+                continue
+            lo, mid = a * k // nodes, (2 * a + 1) * k // (2 * nodes)
+            N0 = S[mid] - S[lo]
+            d1 = bfs(node, a, min(tasks))
+            seed = min((t for t in tasks if d1[t] != INF), key=lambda t: (-d1[t], t))
+            d2 = bfs(node, a, seed)
+            for j, t in enumerate(sorted(tasks, key=lambda t: (d2[t], t))):
+                nxt[t] = 2 * a + (0 if j < N0 else 1)
+        node = nxt
+    part = [-1] * m
+    leaves = 1 << d
+    for j in range(leaves):
+        tasks = [t for t in range(m) if node[t] == j]
+        p0, p1 = j * k // leaves, (j + 1) * k // leaves
+        if not tasks:
+            continue
+        sub = epg2_python([edges[t] for t in tasks], n, s[p0:p1], hub)
+        for t, x in zip(tasks, sub):
+            part[t] = x + p0
+    return part
+
+
+def test_rb_fig_mot():
+    """fig:mot with leaf_parts = 1: k = 2 gives one bisection (1 * 2^1 <= 2). Trace (star +
+    triangle, tasks e1..e6 = 0..5): BFS from e1 reaches e2, e4 (via 1), then e5, e6 (via 4),
+    then e3 (via 5): the seed is e3. BFS from e3: e5, e6 at 1, e4 at 2, e1, e2 at 3. In
+    (dist, id) order the first s_0 = 3 tasks {e3, e5, e6} form the first half; each half is
+    one leaf = one partition: schedule (b), 7 loads, C = C* = 1."""
+    g = golden("fig_mot.json")
+    for name, topo in g["topologies"].items():
+        e = np.array(topo, np.int32)
+        n = int(e.max()) + 1
+        part = O.partition_rb(e, n, 3, leaf_parts=1)
+        assert part.tolist() == [1, 1, 0, 1, 0, 0]
+        assert O.cost(e, n, part, 2).load_count == 7
+
+
+def test_rb_depth_rule():
+    assert O.rb_depth(448, 1, 256) == 0 and O.rb_depth(512, 1, 256) == 1
+    assert O.rb_depth(124_710, 1, 256) == 8 and O.rb_depth(124_710, 8, 256) == 8
+    assert O.rb_depth(10, 8, 256) == 3                      # the shards set the minimum depth
+    assert O.rb_depth(1 << 30, 1, 1) == 10                  # at most 1024 leaves
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_rb_literal_transcription(seed):
+    """The oracle equals a line-by-line transcription of O5'' on random multigraphs (self
+    loops and parallel edges kept), at bisection depths 0-3, flat and with shards."""
+    rng = np.random.default_rng(9100 + seed)
+    m, n0 = int(rng.integers(10, 90)), int(rng.integers(3, 40))
+    n, e = S.random_multigraph(900 + seed, m, n0)
+    P = int(rng.integers(2, 9))
+    el = [tuple(map(int, x)) for x in e]
+    k = O.num_parts(m, P)
+    for shards in (1, 2, 4):
+        if shards > k:
+            continue
+        for lp in (1, 2, 1000):
+            assert O.partition_rb(e, n, P, shards, lp).tolist() == rb_python(el, n, P, shards, lp)
+
+
+def test_rb_invariants_and_shards(small_mesh):
+    """Exact sizes; with shards = G every shard holds exactly the partitions
+    [floor(gk/G), floor((g+1)k/G)) (the first bisection levels); deterministic; depth 0 is
+    EPG-2 itself."""
+    M = small_mesh
+    P = 64
+    k = O.num_parts(M.m, P)
+    s = O.part_sizes(M.m, k)
+    for shards in (1, 2, 4, 8):
+        part = O.partition_rb(M.edges, M.n, P, shards, leaf_parts=8)
+        assert np.array_equal(np.bincount(part, minlength=k), s)
+        assert np.array_equal(part, O.partition_rb(M.edges, M.n, P, shards, leaf_parts=8))
+    assert np.array_equal(O.partition_rb(M.edges, M.n, P, 1, leaf_parts=k),
+                          O.partition(M.edges, M.n, P, method=2))
+
+
+def test_rb_vs_bruteforce():
+    """A valid balanced map, hence C >= C* (brute force, m <= 8), at depth >= 1."""
+    for seed in range(60):
+        rng = np.random.default_rng(300 + seed)
+        m = int(rng.integers(4, 9))
+        n, e = S.random_multigraph(3000 + seed, m, int(rng.integers(2, 7)))
+        for k in (2, 3, 4):
+            if k > m:
+                continue
+            P = -(-m // k)
+            if O.num_parts(m, P) != k:
+                continue
+            part = O.partition_rb(e, n, P, leaf_parts=1)
+            assert np.array_equal(np.bincount(part, minlength=k), O.part_sizes(m, k))
+            _, c = loads_and_cut(e, part)
+            assert c >= optimum(e, list(O.part_sizes(m, k)))[0]
+
+
+def test_rb_quality_on_cfd_mesh(mesh_c1):
+    """C1, P = 1024 (k = 186): leaves of >= 16 partitions (depth 3) cost little replication
+    against flat EPG-2, and stay far below the default schedule."""
+    M = mesh_c1
+    k = O.num_parts(M.m, 1024)
+    r_rb = O.cost(M.edges, M.n, O.partition_rb(M.edges, M.n, 1024, leaf_parts=16), k).replication
+    r_2 = O.cost(M.edges, M.n, O.partition(M.edges, M.n, 1024, method=2), k).replication
+    r_def = O.cost(M.edges, M.n, O.default_partition(M.m, 1024), k).replication
+    assert r_rb <= r_2 + 0.03 and 2 * (r_rb - 1) < r_def - 1

@@ -189,3 +189,31 @@ def test_wrappers_keep_converted_inputs_alive():
         assert np.array_equal(O.spmv(e, n, np.ones(len(e)), x64), O.spmv(e, n, np.ones(len(e), np.float32),
                                                                           x64.astype(np.float32)))
         del junk
+
+
+def test_flux_abs_scale(small_mesh):
+    """S_v = sum_e |Phi_e| (the componentwise scale of Z14) bounds |F_v| and equals it for
+    a vertex with a single edge; for one face S_a = S_b = |Phi| (hand value of
+    test_dissipation_magnitude_at_rest)."""
+    M = small_mesh
+    U = S.cfd_state(M.n, seed=3)
+    F = O.cfd_flux(M.edges, M.n, M.normals, U)
+    Sv = O.cfd_flux_abs(M.edges, M.n, M.normals, U)
+    assert np.all(np.abs(F) <= Sv * (1 + 1e-12))
+    e = np.array([[0, 1]], np.int32)
+    Sab = O.cfd_flux_abs(e, 2, np.array([[2.0, 0, 0]], np.float32),
+                         np.array([[1.2, 0, 0, 0, 2.5], [1.0, 0, 0, 0, 2.0]], np.float32))
+    want = [0.0855369589664192, 1.8, 0.0, 0.0, 0.213842397416048]
+    assert np.allclose(Sab[0], want, rtol=1e-6) and np.allclose(Sab[1], want, rtol=1e-6)
+
+
+def test_cfd_step_omp_matches_sequential(small_mesh):
+    """The all-core timing variant (private accumulators, CPU baseline only) computes the
+    same step up to the summation order of F."""
+    M = small_mesh
+    U, dt = S.cfd_state(M.n), S.cfd_dt(M.volume)
+    ref, F = O.cfd_step(M.edges, M.n, M.normals, U, dt)
+    got, F2, th = O.cfd_step_omp(M.edges, M.n, M.normals, U, dt)
+    assert th >= 1
+    assert np.allclose(F2, F, rtol=0, atol=1e-12 * np.abs(F).max())
+    assert np.allclose(got, ref, rtol=0, atol=1e-12)
