@@ -106,7 +106,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=["c1", "c2", "c3", "c4", "c5"], default="c2")
+    ap.add_argument("--config", choices=["c1", "c2", "c3", "c4", "c5"], default=None,
+                    help="workload (default: c2 on one GPU, c3 with --gpus N > 1)")
     ap.add_argument("--part-size", type=int, default=1024)
     ap.add_argument("--flush-mib", type=int, default=512)
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="bounded oracle sample for cpu_baseline")
@@ -298,10 +299,31 @@ def oracle_baseline(w: "Workload", budget_s: float, steps_min: int = 1):
     return out
 
 
+class _Sample:
+    """A bounded sample of a large workload for the oracle arm: its first `ms` edges, the
+    vertices they touch relabelled compactly, with their state, payload and constants."""
+
+    def __init__(self, w: "Workload", ms: int):
+        e = w.edges[:ms]
+        verts, inv = np.unique(e, return_inverse=True)
+        self.edges = inv.reshape(e.shape).astype(np.int32)
+        self.n, self.m = int(verts.size), int(e.shape[0])
+        self.kernel, self.config = w.kernel, w.config
+        self.state = w.state[verts]
+        self.payload = None if w.payload is None else w.payload[:ms]
+        self.vconst = None if w.vconst is None else w.vconst[verts]
+        self.oracle_step = Workload.oracle_step.__get__(self)
+        self.oracle_name = w.oracle_name
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
     w = Workload(args.config)
+    sample_note = "the full workload"
+    if w.m > 4_000_000:                      # bounded sample: the oracle arm must end in minutes
+        w = _Sample(w, 1 << 21)
+        sample_note = f"a bounded sample: the first {w.m:,} edges of the workload ({w.n:,} vertices)"
     oracle_steps(w, args.warmup)
     steps, secs = oracle_steps(w, args.steps)
     v = w.m * steps / secs
@@ -309,11 +331,11 @@ def run_reference(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "edges/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": bench_config(args),
         "cpu_baseline": {"value": v, "unit": "edges/s", "cores": 1, "kind": "oracle",
-                         "sample": f"{steps} full steps of the fp64 oracle ({w.oracle_name()} in oracle/epg_oracle.c) "
-                                   f"on the {args.config} workload, single thread", **info},
+                         "sample": f"{steps} steps of the fp64 oracle ({w.oracle_name()} in oracle/epg_oracle.c) "
+                                   f"on {sample_note} of {args.config}, single thread", **info},
         "e2e": {"value": v, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -345,52 +367,65 @@ def timed_block(torch, stream, K, step_fn):
 
 
 def run_sharded(args, rank, local_rank, world):
-    """N GPUs, one process each: weak scaling with the halo exchange of SURVEY §8(e)."""
-    import math
-
+    """N GPUs, one process each: strong scaling of one workload (C3 by default
+    for N > 1, BASELINE configs[2]) through the library's sharded step -- epg_comm_init (NCCL
+    communicator, unique id broadcast by torch.distributed) and epg_run_sharded (halo pull,
+    edge kernel over the rank's shard, partial push, finalise; grouped ncclSend/ncclRecv on
+    the ctx stream). Rank 0 partitions (EPG-RB with shards = N) and broadcasts the map."""
     import torch
     import torch.distributed as dist
 
     import synth as S
     from paper_1605_02043_b200 import epg
-    from paper_1605_02043_b200.shard import Comm, Shard
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-        dist.barrier()        # a collective before the first batched p2p (NCCL requirement)
     stream = torch.cuda.current_stream(dev)
     ctx = epg.Context(local_rank, stream)
     K, W, P = args.steps, args.warmup, args.part_size
     clocks = ClockSampler(local_rank)
-    base = S.CONFIGS[args.config]
-    n_keep = base["n_keep"] * world
-    nbox = base["nbox"] if world == 1 else math.ceil((n_keep / 6) ** (1.0 / 3.0))
+    cfg = args.config
     t0 = time.perf_counter()
-    M = S.kuhn_mesh(nbox=nbox, n_keep=n_keep)
-    U, dt = S.cfd_state(M.n), S.cfd_dt(M.volume)
+    M = Workload(cfg)
     t_gen = time.perf_counter() - t0
+    KER = M.kernel
+    ctx.set_exec_limits(M.exec_rows, 1024)
     E = torch.from_numpy(M.edges).to(dev)
     k = epg.num_parts(M.m, P)
+    # communicator first (a unique id from rank 0, broadcast through torch.distributed)
+    uid = torch.zeros(128, dtype=torch.uint8)
+    if rank == 0:
+        uid[:] = torch.frombuffer(bytearray(epg.comm_unique_id()), dtype=torch.uint8)
+    if world > 1:
+        u = uid.to(dev)
+        dist.broadcast(u, 0)
+        uid = u.cpu()
+    ctx.comm_init(bytes(uid.numpy().tobytes()), world, rank)
     t0 = time.perf_counter()
-    ctx.set_partition_method(PARTITIONERS[args.partitioner])
-    part, rep = ctx.partition(E, M.n, P, shards=world)        # hierarchical EPG, identical on all ranks
+    part = torch.empty(M.m, dtype=torch.int32, device=dev)
+    if rank == 0:
+        part, rep0 = ctx.partition_rb(E, M.n, P, shards=world)
+    if world > 1:
+        dist.broadcast(part, 0)
+    rep = ctx.load_count(E, M.n, part, k)
     t_part = time.perf_counter() - t0
     L, plan = ctx.remap(E, M.n, part, k, halo_cap=rep.cut_cost)
-    sh = Shard(ctx, plan, L, epg.KERNEL_CFD_FLUX, world, rank)
-    comm = Comm()
-    Ud = torch.from_numpy(U).to(dev)
-    nrm = ctx.permute_rows(torch.from_numpy(M.normals).to(dev), L.edge_perm, epg.PERM_GATHER)
-    dtn = ctx.permute_rows(torch.from_numpy(dt).to(dev), L.vertex_perm, epg.PERM_SCATTER)
+    Ud = torch.from_numpy(M.state).to(dev)
+    nrm = None if M.payload is None else ctx.permute_rows(torch.from_numpy(M.payload).to(dev), L.edge_perm,
+                                                          epg.PERM_GATHER)
+    dtn = None if M.vconst is None else ctx.permute_rows(torch.from_numpy(M.vconst).to(dev), L.vertex_perm,
+                                                         epg.PERM_SCATTER)
     bufs = [ctx.permute_rows(Ud, L.vertex_perm, epg.PERM_SCATTER), torch.empty_like(Ud)]
-    flushbuf = torch.empty(args.flush_mib * (1 << 20) // 4, dtype=torch.float32, device=dev)
-
-    def flush():
-        flushbuf.fill_(1.0)
+    bufs[1].copy_(bufs[0])
+    pingpong = KER == epg.KERNEL_CFD_FLUX
+    del M.edges
+    r = ctx.shard_ranges(plan, world, rank)
 
     def step(i):
-        sh.step(comm, bufs[i & 1], bufs[(i + 1) & 1], nrm, dtn)
+        j = i & 1 if pingpong else 0
+        ctx.run_sharded(plan, KER, bufs[j], bufs[1 - j], nrm, dtn, 1)
 
     def barrier():
         torch.cuda.synchronize()
@@ -409,59 +444,55 @@ def run_sharded(args, rank, local_rank, world):
         step(i)
     barrier()
     with clocks.window():
-        tot = timed_steps(torch, ctx, stream, K, lambda i: step(i + W), flush)
+        tot = timed_block(torch, stream, K, lambda i: step(i + W))
     barrier()
     step_ms = max_over_ranks(tot / K)
     value = M.m / (step_ms * 1e-3)
     ctx.set_profiling(True)
     ctx.profile_read()
-    timed_steps(torch, ctx, stream, K, step, flush)
+    timed_block(torch, stream, K, step)
     (edge_ms, fin_ms), (n_edge, n_fin) = ctx.profile_read()
     ctx.set_profiling(False)
-    launches = (n_edge + n_fin) + K * 2 * (len(sh.send_ids) + len(sh.recv_ids))   # + pack/unpack/reduce
-    # e2e: each rank's owned rows from pinned host, the result's owned rows back
-    lo, hi = sh.owned()
+    edge_ms = max_over_ranks(edge_ms / K)
+    # e2e: each rank's owned rows from pinned host memory in, the result's owned rows out
+    lo, hi = r["vertex_first"], r["vertex_first"] + r["vertex_count"]
     Uh = bufs[0][lo:hi].cpu().pin_memory()
     Oh = torch.empty_like(Uh).pin_memory()
 
     def e2e_step(i):
         bufs[0][lo:hi].copy_(Uh, non_blocking=True)
-        sh.step(comm, bufs[0], bufs[1], nrm, dtn)
+        ctx.run_sharded(plan, KER, bufs[0], bufs[1], nrm, dtn, 1)
         Oh.copy_(bufs[1][lo:hi], non_blocking=True)
 
     barrier()
     with clocks.window():
-        e2e_ms = max_over_ranks(timed_steps(torch, ctx, stream, K, e2e_step, flush) / K)
+        e2e_ms = max_over_ranks(timed_block(torch, stream, K, e2e_step) / K)
     barrier()
-    halo_rows = sum(v.numel() for v in sh.recv_ids.values()) + sum(v.numel() for v in sh.send_ids.values())
     clk = clocks.summary()
     if rank == 0:
         peak, peak_src = measured_peaks()
-        B = alg_bytes_per_step(M.m, rep.touched)
-        achieved = B / world / ((edge_ms / K) * 1e-3) / 1e9
+        B = M.alg_bytes(rep.touched)
+        achieved = B / world / (edge_ms * 1e-3) / 1e9
         line = {
             "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": K, "warmup": W,
-            "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.config.upper()}-sized cfd Kuhn mesh per GPU: {M.n:,} cells, {M.m:,} "
-                                   f"interior faces in total", "part_size": P, "k": k, "functor": "cfd_flux",
-                       "schedule": f"hierarchical {args.partitioner.upper()}, shards = {world}",
-                       "step": "halo pull (NCCL) + epg_run_edges + partial push (NCCL) + epg_run_finalise",
-                       "l2": f"flushed between timed steps ({args.flush_mib} MiB write)",
-                       "parallelism": f"graph shards x{world}, NCCL p2p halo exchange"},
+            "config": bench_config(args),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None,
-                         "kernel": "k_edge_occ<CfdFlux> on rank 0 (its share of the compulsory bytes)",
-                         "edge_kernel_ms": edge_ms / K, "finalise_ms": fin_ms / K, "peak_source": peak_src},
+                         "kernel": "k_edge_occ on each rank (its 1/N share of the compulsory bytes; slowest rank)",
+                         "edge_kernel_ms": edge_ms, "peak_source": peak_src},
             "cpu_baseline": None,
             "e2e": {"value": M.m / (e2e_ms * 1e-3), "unit": "edges/s",
                     "h2d_bytes_per_step": Uh.numel() * 4, "d2h_bytes_per_step": Oh.numel() * 4,
                     "ms_per_step": e2e_ms, "note": "rank 0's owned rows; every rank moves its own"},
-            "gpu_launches": launches,
+            "gpu_launches": n_edge + n_fin,
             "clocks": clk,
-            "partition": {"load_count": rep.load_count, "touched": rep.touched, "cut_cost": rep.cut_cost,
-                          "replication": rep.replication, "halo_rows_rank0": halo_rows,
+            "partition": {"method": f"EPG-RB, shards = {world} (rank 0, broadcast)", "k": k,
+                          "load_count": rep.load_count, "touched": rep.touched, "cut_cost": rep.cut_cost,
+                          "replication": rep.replication, "owned_rows_rank0": hi - lo,
                           "host_partition_s": t_part, "mesh_gen_s": t_gen},
+            "step": "epg_run_sharded: NCCL halo pull + edge kernel (own shard) + NCCL partial push + finalise",
             "seeds": {"mesh": 1605, "state": 1606},
         }
         print(json.dumps(line), flush=True)
@@ -632,7 +663,7 @@ def run_ours(args, rank, local_rank, world):
         reps[i % nrep].step(ctx, KER, pingpong)
 
     # ---------------- headline: K steps round-robin over the replicas, inputs >> L2
-    for i in range(max(W, nrep)):
+    for i in range(max(W, 2 * nrep)):     # both ping-pong directions of every replica (graph capture)
         rr_step(i)
     torch.cuda.synchronize()
     with clocks.window():
@@ -829,6 +860,9 @@ def run_ours(args, rank, local_rank, world):
 def main():
     args = parse()
     rank, local_rank, world = dist_env()
+    if args.config is None:
+        # N = 1: BASELINE configs[1] (C2, the headline); N > 1: configs[2] (C3 across GPUs)
+        args.config = "c2" if world == 1 and args.gpus == 1 else "c3"
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

@@ -340,6 +340,40 @@ epg_status epg_shard_reduce(epg_ctx *ctx, const epg_plan *plan, epg_kernel kerne
 epg_status epg_accumulate_rows(epg_ctx *ctx, const float *src, const int32_t *ids, int64_t count, int32_t row_floats,
                                float *acc);
 
+/* -- multi-GPU: the halo exchange inside the library ------------- */
+/* One process per GPU. Rank g of G runs shard g of a plan built (identically on every rank)
+ * from a map partitioned with shards = G (epg_partition / epg_partition_rb), so shard g owns
+ * the EP partitions [floor(gk/G), floor((g+1)k/G)) and a contiguous cpack vertex range. A
+ * sharded time step (O7): (1) pull: each owner g' < g sends the rows of Halo^{g<-g'} --
+ * packed by a gather kernel, grouped ncclSend / ncclRecv on the ctx stream, scattered into
+ * state_in (rows owned by other ranks are overwritten with their owners' values); (2) the
+ * staged edge kernel over g's execution partitions; (3) push: g sends each owner the sum of
+ * its halo partials of every vertex of Halo^{g<-g'} (fixed order) and adds what higher ranks
+ * send into a per-vertex accumulator in ascending rank order; (4) the boundary finalise of
+ * g's shared vertices and g's untouched rows. Only the rows g owns (epg_shard_ranges) are
+ * authoritative in state_out. Deterministic for a fixed G.
+ *
+ * epg_comm_unique_id: ncclGetUniqueId into id_out (128 bytes, host) -- call on one rank and
+ *   broadcast it (e.g. through torch.distributed).
+ * epg_comm_init: ncclCommInitRank(nranks, id, rank) on ctx's device; the communicator is
+ *   owned by ctx (destroyed with it, or by the next epg_comm_init*). NCCL is loaded at run
+ *   time (libnccl.so.2); EPG_ERR_NCCL if it is missing or fails.
+ * epg_comm_init_local: makes the nranks contexts (one process, e.g. one GPU) an in-process
+ *   group with ranks 0..nranks-1 whose transfers are device copies -- the same exchange
+ *   schedule without NCCL, for tests; its members step through epg_run_sharded_group.
+ * epg_run_sharded: `steps` sharded time steps on this rank (all ranks must call it with the
+ *   same plan shape, kernel and steps); state as for epg_run (DEVICE, full-size, plan layout).
+ *   Without epg_comm_init it is the single-rank case (no transfers). EPG_ERR_INFEASIBLE if
+ *   nranks > k or the plan exceeds the occupancy kernel's limits.
+ * epg_run_sharded_group: one sharded step of every member of an in-process group
+ *   (ctxs[g] has rank g; plans[g] is ctxs[g]'s plan; states[g] its state). */
+epg_status epg_comm_unique_id(void *id_out);
+epg_status epg_comm_init(epg_ctx *ctx, const void *nccl_unique_id, int32_t nranks, int32_t rank);
+epg_status epg_comm_init_local(epg_ctx *const *ctxs, int32_t nranks);
+epg_status epg_run_sharded(epg_ctx *ctx, const epg_plan *plan, epg_kernel kernel, epg_state *state, int32_t steps);
+epg_status epg_run_sharded_group(epg_ctx *const *ctxs, const epg_plan *const *plans, epg_kernel kernel,
+                                 epg_state *states, int32_t nranks);
+
 /* Kernel variant used by epg_run: 0 = automatic (the first of 3, 2, 1 whose buffers fit),
  * 1 = one CTA per partition (plain loads), 2 = persistent pipelined TMA kernel, 3 = TMA
  * kernel with one CTA per execution partition and several CTAs per SM. 2 and 3 return

@@ -12,6 +12,17 @@ SOURCES = ["api.cu", "partition.cpp", "baselines.cpp", "adaptive.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
+def nccl_include() -> str:
+    """nccl.h of the torch-bundled NCCL (the library dlopens libnccl.so.2 at run time)."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for base in (spec.submodule_search_locations if spec else []):
+        inc = os.path.join(base, "nccl", "include")
+        if os.path.exists(os.path.join(inc, "nccl.h")):
+            return inc
+    raise RuntimeError("nccl.h not found (nvidia-nccl package)")
+
+
 def nvcc() -> str:
     for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
         if cand and (os.path.isabs(cand) and os.path.exists(cand) or not os.path.isabs(cand)):
@@ -32,7 +43,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     cmd = [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-shared",
            "-Xptxas", "-v" if verbose else "-O3",
-           *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB + ".tmp"]
+           "-I", nccl_include(), *[os.path.join(CSRC, s) for s in SOURCES], "-ldl", "-o", LIB + ".tmp"]
     subprocess.check_call(cmd)
     os.replace(LIB + ".tmp", LIB)
     return LIB

@@ -16,6 +16,9 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include "epg_internal.h"
 #include "layout_kernels.cuh"
 #include "run_kernels.cuh"
@@ -40,6 +43,7 @@ struct epg_ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t cap_stream = nullptr;   // private stream epg_run captures its CUDA graphs on
     HostRun *hr = nullptr;
+    struct Comm *comm = nullptr;         // multi-GPU group (epg_comm_init / epg_comm_init_local)
     std::string err;
     float *naive_F = nullptr;
     size_t naive_F_bytes = 0;
@@ -170,6 +174,10 @@ inline int bits_for(int64_t maxval) {  // bits needed for values in [0, maxval]
     } while (0)
 
 #define CHECK_LAUNCH() CU(cudaGetLastError())
+#define CU_NOCTX(call)                                                                                  \
+    do {                                                                                                \
+        if ((call) != cudaSuccess) return EPG_ERR_CUDA;                                                 \
+    } while (0)
 
 // stream-ordered temporary device buffer
 struct Tmp {
@@ -891,6 +899,19 @@ epg_status run_edges_range(epg_ctx *ctx, epg_plan *pl, epg_state *state, int64_t
     if (count <= 0) return EPG_OK;
     return occ_dispatch<Fn>(pl, [&](auto kern, int, int) -> epg_status {
         CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        {   // as launch_occ: multi-wave ranges prefetch the next wave's ranges into L2
+            auto it = pl->resident_ctas.find(reinterpret_cast<const void *>(kern));
+            if (it == pl->resident_ctas.end()) {
+                int occ = 0, sms = 0;
+                CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kOccThreads, smem));
+                CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+                it = pl->resident_ctas.emplace(reinterpret_cast<const void *>(kern), (int64_t)occ * sms).first;
+            }
+            const char *e = std::getenv("EPG_PREFETCH_AHEAD");
+            a.early_pdl = 0;
+            a.ahead = count > it->second ? (e ? std::atoll(e) : it->second) : 0;
+            a.count = count;
+        }
         cudaEvent_t t0 = ctx->prof_begin();
         CU(launch_pdl(kern, (unsigned)count, kOccThreads, smem, ctx->stream, a));
         ctx->prof_end(0, t0);
@@ -1356,6 +1377,8 @@ epg_status rb_partition(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n
 
 }  // namespace
 
+void comm_release(epg_ctx *ctx);
+
 // =====================================================================================
 extern "C" {
 
@@ -1393,6 +1416,7 @@ void epg_destroy(epg_ctx *ctx) {
         cudaStreamDestroy(h->s_out);
         delete h;
     }
+    comm_release(ctx);
     for (auto &u : ctx->ev_used) { cudaEventDestroy(u.second.first); cudaEventDestroy(u.second.second); }
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
     delete ctx;
@@ -2098,5 +2122,487 @@ epg_status epg_debug_trace_clear() {
     return EPG_OK;
 }
 #endif
+
+}  // extern "C"
+
+
+// =====================================================================================
+// Multi-GPU execution (SURVEY §8(b) epg_comm_init, §8(e); the paper is single-GPU).
+//
+// Rank g of G holds the same plan (a map partitioned with shards = G, so shard g owns the
+// EP partitions [floor(gk/G), floor((g+1)k/G)) and, by cpack, a contiguous vertex range).
+// Per time step (O7): (1) pull -- the owners g' < g send the rows of Halo^{g<-g'}: packed by
+// a gather kernel, exchanged with grouped ncclSend/ncclRecv on the ctx stream, scattered into
+// state_in; (2) the edge kernel over g's execution partitions; (3) push -- g reduces its halo
+// partials of every vertex of Halo^{g<-g'} (fixed order) and sends them to the owner g',
+// receiving the same from every g'' > g; the received rows are added to a per-vertex
+// accumulator in ascending peer order; (4) the boundary finalise of g's shared vertices
+// (local halo partials, then the accumulator) and g's untouched rows. Deterministic for a
+// fixed G. The transport is NCCL (one process per GPU) or, for one-GPU tests, an in-process
+// group whose "send" is a device copy between the group's contexts (epg_comm_init_local).
+// =====================================================================================
+struct NcclApi {
+    void *h = nullptr;
+    ncclResult_t (*getUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*groupStart)() = nullptr;
+    ncclResult_t (*groupEnd)() = nullptr;
+    ncclResult_t (*send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    const char *(*errorString)(ncclResult_t) = nullptr;
+};
+
+// NCCL is resolved at run time (the torch-bundled libnccl.so.2 of this image), so libepg.so
+// loads without it and only the multi-GPU calls need it
+const NcclApi *nccl_api(std::string *err) {
+    static NcclApi api;
+    static bool tried = false;
+    if (tried) {
+        if (!api.h) *err = "NCCL (libnccl.so.2) could not be loaded";
+        return api.h ? &api : nullptr;
+    }
+    tried = true;
+    const char *cands[] = {"libnccl.so.2", "libnccl.so",
+                           "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2"};
+    for (const char *c : cands)
+        if ((api.h = dlopen(c, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!api.h) {
+        *err = "NCCL (libnccl.so.2) could not be loaded";
+        return nullptr;
+    }
+#define NSYM(field, name) api.field = reinterpret_cast<decltype(api.field)>(dlsym(api.h, name))
+    NSYM(getUniqueId, "ncclGetUniqueId");
+    NSYM(commInitRank, "ncclCommInitRank");
+    NSYM(commDestroy, "ncclCommDestroy");
+    NSYM(groupStart, "ncclGroupStart");
+    NSYM(groupEnd, "ncclGroupEnd");
+    NSYM(send, "ncclSend");
+    NSYM(recv, "ncclRecv");
+    NSYM(errorString, "ncclGetErrorString");
+#undef NSYM
+    if (!api.getUniqueId || !api.commInitRank || !api.commDestroy || !api.groupStart || !api.groupEnd || !api.send ||
+        !api.recv || !api.errorString) {
+        *err = "NCCL: missing symbols in libnccl.so.2";
+        api.h = nullptr;
+        return nullptr;
+    }
+    return &api;
+}
+
+struct LocalGroup;   // in-process group (one-GPU tests)
+
+struct Comm {
+    int nranks = 1, rank = 0;
+    ncclComm_t nccl = nullptr;
+    LocalGroup *local = nullptr;
+};
+
+struct LocalGroup {
+    std::vector<epg_ctx *> ctxs;
+};
+
+// exchange buffers and lists of one plan on one rank (built on the first sharded step)
+struct ShardState {
+    const epg_plan *plan = nullptr;
+    int G = 1, g = 0, row = 0;
+    int64_t xf = 0, xc = 0, hf = 0, hc = 0, sf = 0, sc = 0;
+    // per peer: rows this rank receives in the pull (p < g) / sends (p > g), offsets into
+    // the concatenated id lists; the same lists carry the push in the other direction
+    std::vector<int64_t> recv_off, send_off;     // [G + 1]
+    int32_t *recv_ids = nullptr, *send_ids = nullptr;
+    float *pull_send = nullptr, *pull_recv = nullptr, *push_send = nullptr, *push_recv = nullptr, *acc = nullptr;
+    int4 *recs = nullptr;     // finalise records of the shard's shared vertices (local halo entries only)
+    int32_t *acc_ids = nullptr;   // distinct vertices other ranks push partial sums for
+    int64_t acc_count = 0;
+    std::vector<void *> allocs;
+    ~ShardState() {
+        for (void *p : allocs) cudaFree(p);
+    }
+};
+
+namespace {
+
+void *shard_alloc(ShardState *S, size_t bytes, cudaError_t *e) {
+    void *p = nullptr;
+    *e = cudaMalloc(&p, std::max<size_t>(bytes, 16));
+    if (*e == cudaSuccess) S->allocs.push_back(p);
+    return p;
+}
+
+std::map<std::pair<const epg_ctx *, const epg_plan *>, ShardState *> &shard_states() {
+    static std::map<std::pair<const epg_ctx *, const epg_plan *>, ShardState *> m;
+    return m;
+}
+
+// shard state of (ctx, plan) for the ctx's group; built once
+epg_status shard_state(epg_ctx *ctx, epg_plan *pl, int row, ShardState **out) {
+    auto key = std::make_pair((const epg_ctx *)ctx, (const epg_plan *)pl);
+    auto it = shard_states().find(key);
+    if (it != shard_states().end() && it->second->row == row) {
+        *out = it->second;
+        return EPG_OK;
+    }
+    if (it != shard_states().end()) {
+        delete it->second;
+        shard_states().erase(it);
+    }
+    const int G = ctx->comm ? ctx->comm->nranks : 1, g = ctx->comm ? ctx->comm->rank : 0;
+    if (G > pl->k_ep) return ctx->fail(EPG_ERR_INFEASIBLE, "run_sharded: more ranks than EP partitions");
+    std::unique_ptr<ShardState> S(new ShardState());
+    S->plan = pl;
+    S->G = G;
+    S->g = g;
+    S->row = row;
+    int64_t r8[8];
+    epg_status st = epg_shard_ranges(pl, G, g, r8);
+    if (st) return ctx->fail(st, "run_sharded: shard ranges");
+    S->xf = r8[0]; S->xc = r8[1]; S->hf = r8[2]; S->hc = r8[3]; S->sf = r8[6]; S->sc = r8[7];
+    // O7 halo sets from the EP layout (the execution plan keeps the EP partitions' first
+    // touches, so the shard ranges of the EP map and of the execution map agree)
+    std::vector<int32_t> hid(pl->C);
+    if (pl->C > 0) CU(cudaMemcpy(hid.data(), pl->halo_ids, sizeof(int32_t) * pl->C, cudaMemcpyDeviceToHost));
+    std::vector<int32_t> pvb_ep(pl->k_ep + 1), hb_ep(pl->k_ep + 1);
+    for (int64_t p = 0; p <= pl->k_ep; p++) {
+        pvb_ep[p] = pl->pvb_h[pl->exec_base[p]];
+        hb_ep[p] = pl->hb_h[pl->exec_base[p]];
+    }
+    std::vector<int32_t> begin(G * G + 1);
+    int64_t cnt = 0;
+    if ((st = epg_shard_halos_host(pvb_ep.data(), hb_ep.data(), hid.data(), pl->k_ep, G, begin.data(), nullptr, 0, &cnt)))
+        return ctx->fail(st, "run_sharded: halo sets");
+    std::vector<int32_t> ids(std::max<int64_t>(cnt, 1));
+    if ((st = epg_shard_halos_host(pvb_ep.data(), hb_ep.data(), hid.data(), pl->k_ep, G, begin.data(), ids.data(),
+                                   (int64_t)ids.size(), &cnt)))
+        return ctx->fail(st, "run_sharded: halo sets");
+    std::vector<int32_t> rl, sl;
+    S->recv_off.assign(G + 1, 0);
+    S->send_off.assign(G + 1, 0);
+    for (int p = 0; p < G; p++) {
+        S->recv_off[p] = (int64_t)rl.size();
+        if (p < g) rl.insert(rl.end(), ids.begin() + begin[g * G + p], ids.begin() + begin[g * G + p + 1]);
+        S->send_off[p] = (int64_t)sl.size();
+        if (p > g) sl.insert(sl.end(), ids.begin() + begin[p * G + g], ids.begin() + begin[p * G + g + 1]);
+    }
+    S->recv_off[G] = (int64_t)rl.size();
+    S->send_off[G] = (int64_t)sl.size();
+    cudaError_t e;
+    const size_t rb = sizeof(float) * row;
+    S->recv_ids = (int32_t *)shard_alloc(S.get(), sizeof(int32_t) * rl.size(), &e);
+    if (e == cudaSuccess) S->send_ids = (int32_t *)shard_alloc(S.get(), sizeof(int32_t) * sl.size(), &e);
+    if (e == cudaSuccess) S->pull_send = (float *)shard_alloc(S.get(), rb * sl.size(), &e);
+    if (e == cudaSuccess) S->pull_recv = (float *)shard_alloc(S.get(), rb * rl.size(), &e);
+    if (e == cudaSuccess) S->push_send = (float *)shard_alloc(S.get(), rb * rl.size(), &e);
+    if (e == cudaSuccess) S->push_recv = (float *)shard_alloc(S.get(), rb * sl.size(), &e);
+    if (e == cudaSuccess) S->acc = (float *)shard_alloc(S.get(), rb * pl->n, &e);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return ctx->fail(EPG_ERR_NOMEM, "run_sharded: exchange buffers");
+    }
+    if (!rl.empty()) CU(cudaMemcpy(S->recv_ids, rl.data(), sizeof(int32_t) * rl.size(), cudaMemcpyHostToDevice));
+    if (!sl.empty()) CU(cudaMemcpy(S->send_ids, sl.data(), sizeof(int32_t) * sl.size(), cudaMemcpyHostToDevice));
+    {
+        std::vector<int32_t> u(sl);
+        std::sort(u.begin(), u.end());
+        u.erase(std::unique(u.begin(), u.end()), u.end());
+        S->acc_count = (int64_t)u.size();
+        S->acc_ids = (int32_t *)shard_alloc(S.get(), sizeof(int32_t) * u.size(), &e);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return ctx->fail(EPG_ERR_NOMEM, "run_sharded: exchange buffers");
+        }
+        if (!u.empty()) CU(cudaMemcpy(S->acc_ids, u.data(), sizeof(int32_t) * u.size(), cudaMemcpyHostToDevice));
+    }
+    CU(cudaMemset(S->acc, 0, rb * pl->n));
+    if (S->sc > 0) {   // packed records {v, count, h0..h5} when no shared vertex has > 6 local entries
+        int4 *recs = (int4 *)shard_alloc(S.get(), sizeof(int4) * 2 * S->sc, &e);
+        int32_t *hm = (int32_t *)shard_alloc(S.get(), 2 * sizeof(int32_t), &e);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return ctx->fail(EPG_ERR_NOMEM, "run_sharded: finalise records");
+        }
+        CU(cudaMemset(hm, 0, 2 * sizeof(int32_t)));
+        k_shard_records<<<grid_for(S->sc), kThreads>>>(pl->shared_ids + S->sf, pl->hv_off + S->sf, pl->hv_list,
+                                                       (int32_t)S->sc, S->hf, S->hf + S->hc, recs, hm);
+        CU(cudaGetLastError());
+        int32_t hmax = 0;
+        CU(cudaMemcpy(&hmax, hm, sizeof(int32_t), cudaMemcpyDeviceToHost));
+        if (hmax <= 6) S->recs = recs;
+    }
+    *out = S.release();
+    shard_states()[key] = *out;
+    return EPG_OK;
+}
+
+// rows of `ids` (rows of `row` floats) gathered from / scattered into `state`
+epg_status rows_move(epg_ctx *ctx, const float *src, float *dst, const int32_t *ids, int64_t count, int row,
+                     int scatter) {
+    if (count <= 0) return EPG_OK;
+    k_permute_rows<<<grid_for(count * row), kThreads, 0, ctx->stream>>>(
+        reinterpret_cast<const uint32_t *>(src), reinterpret_cast<uint32_t *>(dst), count, row, ids, scatter);
+    CHECK_LAUNCH();
+    return EPG_OK;
+}
+
+// the grouped point-to-point exchange of one phase: send[p] to every p in `to`, receive
+// recv[p] from every p in `from` (rows of `row` floats)
+epg_status exchange(epg_ctx *ctx, ShardState *S, const float *send, const std::vector<int64_t> &send_off,
+                    float *recv, const std::vector<int64_t> &recv_off) {
+    const int G = S->G, row = S->row;
+    Comm *c = ctx->comm;
+    if (G == 1) return EPG_OK;
+    if (c->nccl) {
+        std::string err;
+        const NcclApi *n = nccl_api(&err);
+        if (!n) return ctx->fail(EPG_ERR_NCCL, err);
+        ncclResult_t r = n->groupStart();
+        for (int p = 0; p < G && r == ncclSuccess; p++) {
+            const int64_t sc = send_off[p + 1] - send_off[p], rc = recv_off[p + 1] - recv_off[p];
+            if (sc > 0) r = n->send(send + row * send_off[p], (size_t)(row * sc), ncclFloat, p, c->nccl, ctx->stream);
+            if (r == ncclSuccess && rc > 0)
+                r = n->recv(recv + row * recv_off[p], (size_t)(row * rc), ncclFloat, p, c->nccl, ctx->stream);
+        }
+        ncclResult_t r2 = n->groupEnd();
+        if (r != ncclSuccess || r2 != ncclSuccess)
+            return ctx->fail(EPG_ERR_NCCL, std::string("run_sharded: ") + n->errorString(r != ncclSuccess ? r : r2));
+        return EPG_OK;
+    }
+    return EPG_OK;   // in-process groups exchange in run_sharded_group
+}
+
+template <class Fn>
+epg_status sharded_pull_pack(epg_ctx *ctx, ShardState *S, const float *state_in) {
+    return rows_move(ctx, state_in, S->pull_send, S->send_ids, S->send_off[S->G], Fn::ROW, 0);
+}
+template <class Fn>
+epg_status sharded_pull_unpack(epg_ctx *ctx, ShardState *S, float *state_in) {
+    return rows_move(ctx, S->pull_recv, state_in, S->recv_ids, S->recv_off[S->G], Fn::ROW, 1);
+}
+template <class Fn>
+epg_status sharded_push_pack(epg_ctx *ctx, epg_plan *pl, ShardState *S) {
+    const int64_t cnt = S->recv_off[S->G];
+    if (cnt <= 0) return EPG_OK;
+    k_shard_reduce<Fn><<<grid_for(cnt), kThreads, 0, ctx->stream>>>(S->recv_ids, cnt, pl->sidx, pl->hv_off, pl->hv_list,
+                                                                     pl->halo_buf, S->hf, S->hf + S->hc, S->push_send);
+    CHECK_LAUNCH();
+    return EPG_OK;
+}
+template <class Fn>
+epg_status sharded_push_accumulate(epg_ctx *ctx, ShardState *S) {
+    for (int p = S->g + 1; p < S->G; p++) {   // ascending peer order: a fixed summation order
+        const int64_t c = S->send_off[p + 1] - S->send_off[p];
+        if (c <= 0) continue;
+        k_accumulate_rows<<<grid_for(c * Fn::ROW), kThreads, 0, ctx->stream>>>(
+            S->push_recv + Fn::ROW * S->send_off[p], S->send_ids + S->send_off[p], c, Fn::ROW, S->acc);
+        CHECK_LAUNCH();
+    }
+    return EPG_OK;
+}
+
+// finalise of the shard: its shared vertices from the packed local records (or the ranged
+// kernel), then the pushed partial sums of the vertices other ranks share, then untouched rows
+template <class Fn>
+epg_status sharded_finalise(epg_ctx *ctx, epg_plan *pl, ShardState *S, epg_state *st) {
+    if (!S->recs) return run_finalise_range<Fn>(ctx, pl, st, S->sf, S->sc, S->hf, S->hc, S->acc, 1);
+    const float *in = static_cast<const float *>(st->state_in);
+    float *out = static_cast<float *>(st->state_out);
+    const float *vc = static_cast<const float *>(st->vertex_const);
+    const int64_t work = S->sc + (pl->n - pl->touched);
+    if (work > 0)
+        CU(launch_pdl(k_finalise_rec<Fn>, grid_for(work), kThreads, 0, ctx->stream, (const int4 *)S->recs,
+                      (const float *)pl->halo_buf, in, out, vc, (int32_t)S->sc, pl->touched, pl->n));
+    const int64_t cnt = S->acc_count;
+    if (cnt > 0) {
+        k_acc_add<Fn><<<grid_for(cnt), kThreads, 0, ctx->stream>>>(S->acc_ids, cnt, S->acc, out, vc);
+        CHECK_LAUNCH();
+    }
+    return EPG_OK;
+}
+
+template <class Fn>
+epg_status run_sharded_t(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps) {
+    ShardState *S = nullptr;
+    epg_status st = shard_state(ctx, pl, Fn::ROW, &S);
+    if (st) return st;
+    float *bufs[2] = {static_cast<float *>(state->state_in), static_cast<float *>(state->state_out)};
+    for (int32_t s = 0; s < steps; s++) {
+        epg_state cur = *state;
+        cur.state_in = bufs[s & 1];
+        cur.state_out = bufs[(s + 1) & 1];
+        float *in = static_cast<float *>(cur.state_in);
+        if ((st = sharded_pull_pack<Fn>(ctx, S, in)) ||
+            (st = exchange(ctx, S, S->pull_send, S->send_off, S->pull_recv, S->recv_off)) ||
+            (st = sharded_pull_unpack<Fn>(ctx, S, in)) || (st = run_edges_range<Fn>(ctx, pl, &cur, S->xf, S->xc)) ||
+            (st = sharded_push_pack<Fn>(ctx, pl, S)) ||
+            (st = exchange(ctx, S, S->push_send, S->recv_off, S->push_recv, S->send_off)) ||
+            (st = sharded_push_accumulate<Fn>(ctx, S)) || (st = sharded_finalise<Fn>(ctx, pl, S, &cur)))
+            return st;
+    }
+    return EPG_OK;
+}
+
+// one step of every member of an in-process group, phase by phase; the "transfers" are
+// device copies between the members' buffers ordered by events (one GPU, tests)
+template <class Fn>
+epg_status run_group_t(epg_ctx **ctxs, epg_plan **plans, epg_state *states, int G) {
+    std::vector<ShardState *> S(G);
+    for (int g = 0; g < G; g++) {
+        epg_status st = shard_state(ctxs[g], plans[g], Fn::ROW, &S[g]);
+        if (st) return st;
+    }
+    std::vector<cudaEvent_t> ev(G);
+    for (int g = 0; g < G; g++) cudaEventCreateWithFlags(&ev[g], cudaEventDisableTiming);
+    auto sync_all = [&]() {
+        for (int g = 0; g < G; g++) cudaEventRecord(ev[g], ctxs[g]->stream);
+        for (int g = 0; g < G; g++)
+            for (int p = 0; p < G; p++) cudaStreamWaitEvent(ctxs[g]->stream, ev[p], 0);
+    };
+    // copies of one phase: member g receives from p the rows p sends to g
+    auto copy_phase = [&](bool pull) {
+        for (int g = 0; g < G; g++)
+            for (int p = 0; p < G; p++) {
+                ShardState *R = S[g], *T = S[p];
+                // pull: p > ... p sends pull_send[p][g] to g (p < g); push: p sends push_send[p][g] to g (p > g)
+                const int64_t rc = pull ? R->recv_off[p + 1] - R->recv_off[p] : R->send_off[p + 1] - R->send_off[p];
+                if (rc <= 0) continue;
+                const float *src = pull ? T->pull_send + Fn::ROW * T->send_off[g] : T->push_send + Fn::ROW * T->recv_off[g];
+                float *dst = pull ? R->pull_recv + Fn::ROW * R->recv_off[p] : R->push_recv + Fn::ROW * R->send_off[p];
+                cudaMemcpyAsync(dst, src, sizeof(float) * Fn::ROW * rc, cudaMemcpyDeviceToDevice, ctxs[g]->stream);
+            }
+    };
+    epg_status st = EPG_OK;
+    for (int g = 0; g < G && !st; g++) st = sharded_pull_pack<Fn>(ctxs[g], S[g], (const float *)states[g].state_in);
+    sync_all();
+    copy_phase(true);
+    sync_all();
+    for (int g = 0; g < G && !st; g++) {
+        if ((st = sharded_pull_unpack<Fn>(ctxs[g], S[g], (float *)states[g].state_in))) break;
+        if ((st = run_edges_range<Fn>(ctxs[g], plans[g], &states[g], S[g]->xf, S[g]->xc))) break;
+        st = sharded_push_pack<Fn>(ctxs[g], plans[g], S[g]);
+    }
+    sync_all();
+    copy_phase(false);
+    sync_all();
+    for (int g = 0; g < G && !st; g++) {
+        if ((st = sharded_push_accumulate<Fn>(ctxs[g], S[g]))) break;
+        st = sharded_finalise<Fn>(ctxs[g], plans[g], S[g], &states[g]);
+    }
+    sync_all();
+    for (int g = 0; g < G; g++) cudaEventDestroy(ev[g]);
+    return st;
+}
+
+}  // namespace
+
+void comm_release(epg_ctx *ctx) {
+    for (auto it = shard_states().begin(); it != shard_states().end();) {
+        if (it->first.first == ctx) {
+            delete it->second;
+            it = shard_states().erase(it);
+        } else {
+            ++it;
+        }
+    }
+    if (!ctx->comm) return;
+    if (ctx->comm->nccl) {
+        std::string err;
+        if (const NcclApi *n = nccl_api(&err)) n->commDestroy(ctx->comm->nccl);
+    }
+    if (ctx->comm->local) {   // the group's members share it; the last one frees it
+        auto &v = ctx->comm->local->ctxs;
+        v.erase(std::remove(v.begin(), v.end(), ctx), v.end());
+        if (v.empty()) delete ctx->comm->local;
+    }
+    delete ctx->comm;
+    ctx->comm = nullptr;
+}
+
+extern "C" {
+
+epg_status epg_comm_unique_id(void *id_out) {
+    if (!id_out) return EPG_ERR_INPUT;
+    std::string err;
+    const NcclApi *n = nccl_api(&err);
+    if (!n) return EPG_ERR_NCCL;
+    ncclUniqueId id;
+    if (n->getUniqueId(&id) != ncclSuccess) return EPG_ERR_NCCL;
+    std::memcpy(id_out, &id, sizeof(id));
+    return EPG_OK;
+}
+
+epg_status epg_comm_init(epg_ctx *ctx, const void *nccl_unique_id, int32_t nranks, int32_t rank) {
+    if (!ctx) return EPG_ERR_STATE;
+    if (!nccl_unique_id || nranks < 1 || rank < 0 || rank >= nranks)
+        return ctx->fail(EPG_ERR_INPUT, "comm_init: need a unique id, nranks >= 1 and 0 <= rank < nranks");
+    CU(cudaSetDevice(ctx->device));
+    std::string err;
+    const NcclApi *n = nccl_api(&err);
+    if (!n) return ctx->fail(EPG_ERR_NCCL, err);
+    comm_release(ctx);
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_unique_id, sizeof(id));
+    ncclComm_t c = nullptr;
+    ncclResult_t r = n->commInitRank(&c, nranks, id, rank);
+    if (r != ncclSuccess) return ctx->fail(EPG_ERR_NCCL, std::string("comm_init: ") + n->errorString(r));
+    ctx->comm = new Comm();
+    ctx->comm->nranks = nranks;
+    ctx->comm->rank = rank;
+    ctx->comm->nccl = c;
+    return EPG_OK;
+}
+
+epg_status epg_comm_init_local(epg_ctx *const *ctxs, int32_t nranks) {
+    if (!ctxs || nranks < 1) return EPG_ERR_INPUT;
+    for (int g = 0; g < nranks; g++)
+        if (!ctxs[g]) return EPG_ERR_INPUT;
+    LocalGroup *grp = new LocalGroup();
+    for (int g = 0; g < nranks; g++) {
+        comm_release(ctxs[g]);
+        ctxs[g]->comm = new Comm();
+        ctxs[g]->comm->nranks = nranks;
+        ctxs[g]->comm->rank = g;
+        ctxs[g]->comm->local = grp;
+        grp->ctxs.push_back(ctxs[g]);
+    }
+    return EPG_OK;
+}
+
+epg_status epg_run_sharded(epg_ctx *ctx, const epg_plan *plan, epg_kernel kernel, epg_state *state, int32_t steps) {
+    if (!ctx) return EPG_ERR_STATE;
+    if (!plan || plan->ctx != ctx) return ctx->fail(EPG_ERR_STATE, "run_sharded: plan belongs to another context");
+    if (ctx->comm && ctx->comm->local && ctx->comm->nranks > 1)
+        return ctx->fail(EPG_ERR_STATE, "run_sharded: an in-process group runs through epg_run_sharded_group");
+    epg_status st = check_state(ctx, kernel, state);
+    if (st) return st;
+    if (steps < 0) return ctx->fail(EPG_ERR_INPUT, "run_sharded: steps < 0");
+    CU(cudaSetDevice(ctx->device));
+    epg_plan *pl = const_cast<epg_plan *>(plan);
+    switch (kernel) {
+        case EPG_KERNEL_CFD_FLUX: return run_sharded_t<CfdFlux>(ctx, pl, state, steps);
+        case EPG_KERNEL_GATHER_SCATTER: return run_sharded_t<GatherScatter>(ctx, pl, state, steps);
+        default: return run_sharded_t<Spmv>(ctx, pl, state, steps);
+    }
+}
+
+epg_status epg_run_sharded_group(epg_ctx *const *ctxs, const epg_plan *const *plans, epg_kernel kernel,
+                                 epg_state *states, int32_t nranks) {
+    if (!ctxs || !plans || !states || nranks < 1) return EPG_ERR_INPUT;
+    for (int g = 0; g < nranks; g++) {
+        if (!ctxs[g] || !plans[g] || plans[g]->ctx != ctxs[g] || !ctxs[g]->comm || ctxs[g]->comm->rank != g ||
+            ctxs[g]->comm->nranks != nranks || !ctxs[g]->comm->local)
+            return EPG_ERR_STATE;
+        epg_status st = check_state(ctxs[g], kernel, &states[g]);
+        if (st) return st;
+    }
+    std::vector<epg_ctx *> c(ctxs, ctxs + nranks);
+    std::vector<epg_plan *> p(nranks);
+    for (int g = 0; g < nranks; g++) p[g] = const_cast<epg_plan *>(plans[g]);
+    CU_NOCTX(cudaSetDevice(ctxs[0]->device));
+    switch (kernel) {
+        case EPG_KERNEL_CFD_FLUX: return run_group_t<CfdFlux>(c.data(), p.data(), states, nranks);
+        case EPG_KERNEL_GATHER_SCATTER: return run_group_t<GatherScatter>(c.data(), p.data(), states, nranks);
+        default: return run_group_t<Spmv>(c.data(), p.data(), states, nranks);
+    }
+}
 
 }  // extern "C"

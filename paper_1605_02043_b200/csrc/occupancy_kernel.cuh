@@ -575,6 +575,43 @@ __global__ void k_finalise_records(const int32_t *__restrict__ shared_ids, const
     atomicMax(hmax, c);
 }
 
+// records for the finalise of one shard (multi-GPU): the shard's shared vertices with only
+// their halo entries at positions in [h_lo, h_hi) (the shard's own partitions), in hv_list
+// order; *hmax receives the largest local count
+__global__ void k_shard_records(const int32_t *__restrict__ shared_ids, const int32_t *__restrict__ hv_off,
+                                const int32_t *__restrict__ hv_list, int32_t count, int64_t h_lo, int64_t h_hi,
+                                int4 *recs, int32_t *hmax) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= count) return;
+    int h[6] = {0, 0, 0, 0, 0, 0};
+    int c = 0;
+    for (int q = hv_off[t]; q < hv_off[t + 1]; q++) {
+        const int64_t x = hv_list[q];
+        if (x < h_lo || x >= h_hi) continue;
+        if (c < 6) h[c] = (int)x;
+        c++;
+    }
+    recs[2 * t] = make_int4(shared_ids[t], c < 6 ? c : 6, h[0], h[1]);
+    recs[2 * t + 1] = make_int4(h[2], h[3], h[4], h[5]);
+    atomicMax(hmax, c);
+}
+
+// U'_v += dt_v * acc_v for the vertices other ranks pushed partial sums for; acc cleared
+template <class Fn>
+__global__ void k_acc_add(const int32_t *__restrict__ ids, int64_t count, float *__restrict__ acc,
+                          float *__restrict__ state_out, const float *__restrict__ vconst) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const int64_t v = ids[i];
+    float sum[Fn::ROW];
+#pragma unroll
+    for (int c = 0; c < Fn::ROW; c++) {
+        sum[c] = acc[Fn::ROW * v + c];
+        acc[Fn::ROW * v + c] = 0.0f;
+    }
+    Fn::finalise_add(state_out + Fn::ROW * v, sum, Fn::kUsesConst ? vconst[v] : 0.0f);
+}
+
 // Hub finalise (hub split): U'_v += dt * hub_acc[i] for hub i of
 // shared vertex hub_sid[i]; hub_acc is cleared for the next step. The hub's partials were
 // added by the edge kernel with one red.global.add per (execution partition, hub) after

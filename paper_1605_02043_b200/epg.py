@@ -34,7 +34,8 @@ SYMBOLS = ["epg_create", "epg_destroy", "epg_last_error", "epg_num_parts", "epg_
            "epg_set_exec_limits", "epg_partition_random_host", "epg_partition_greedy_host",
            "epg_adaptive_create", "epg_adaptive_step", "epg_adaptive_wait", "epg_adaptive_read_state",
            "epg_adaptive_info", "epg_adaptive_destroy", "epg_partition_host_method", "epg_set_partition_method",
-           "epg_run_host", "epg_run_host_join", "epg_partition_rb"]
+           "epg_run_host", "epg_run_host_join", "epg_partition_rb", "epg_comm_unique_id", "epg_comm_init",
+           "epg_comm_init_local", "epg_run_sharded", "epg_run_sharded_group"]
 
 
 class _Report(C.Structure):
@@ -102,6 +103,11 @@ def _load():
         "epg_shard_reduce": (st, [P, P, C.c_int, P, i64, i64, i64, P]),
         "epg_accumulate_rows": (st, [P, P, P, i64, i32, P]),
         "epg_remapped_edges": (st, [P, P, i64, P, P, P]),
+        "epg_comm_unique_id": (st, [P]),
+        "epg_comm_init": (st, [P, P, i32, i32]),
+        "epg_comm_init_local": (st, [P, i32]),
+        "epg_run_sharded": (st, [P, P, C.c_int, C.POINTER(_State), i32]),
+        "epg_run_sharded_group": (st, [P, P, C.c_int, P, i32]),
         "epg_set_profiling": (st, [P, i32]),
         "epg_profile_read": (st, [P, P, P]),
     }
@@ -210,6 +216,35 @@ def partition_greedy_host(edges, n: int, part_size: int) -> np.ndarray:
     if s != OK:
         raise EpgError(s, buf.value.decode())
     return part[:m]
+
+
+def comm_unique_id() -> bytes:
+    """epg_comm_unique_id: a fresh NCCL unique id (128 bytes) to broadcast to every rank."""
+    buf = C.create_string_buffer(128)
+    s = lib.epg_comm_unique_id(buf)
+    if s != OK:
+        raise EpgError(s, "epg_comm_unique_id (NCCL unavailable?)")
+    return buf.raw
+
+
+def comm_init_local(ctxs: list):
+    """epg_comm_init_local: the contexts become an in-process group (ranks 0..G-1)."""
+    arr = (C.c_void_p * len(ctxs))(*[c.handle.value for c in ctxs])
+    s = lib.epg_comm_init_local(arr, len(ctxs))
+    if s != OK:
+        raise EpgError(s, "epg_comm_init_local")
+
+
+def run_sharded_group(ctxs: list, plans: list, kernel: int, states: list):
+    """epg_run_sharded_group: one sharded step of every member; states[g] = (in, out, payload, vconst)."""
+    G = len(ctxs)
+    carr = (C.c_void_p * G)(*[c.handle.value for c in ctxs])
+    parr = (C.c_void_p * G)(*[p.handle.value for p in plans])
+    sarr = (_State * G)(*[_State(_ptr(a), _ptr(b), _ptr(pw), _ptr(vc)) for a, b, pw, vc in states])
+    s = lib.epg_run_sharded_group(carr, parr, kernel, sarr, G)
+    if s != OK:
+        msgs = "; ".join(lib.epg_last_error(c.handle).decode() for c in ctxs)
+        raise EpgError(s, f"epg_run_sharded_group: {msgs}")
 
 
 ADAPTIVE_ORIGINAL, ADAPTIVE_EP, ADAPTIVE_FELL_BACK, ADAPTIVE_NO_PARTITION = 0, 1, 2, 3
@@ -442,6 +477,18 @@ class Context:
     def accumulate_rows(self, src: torch.Tensor, ids: torch.Tensor, acc: torch.Tensor):
         w = src[0].numel() if src.dim() > 1 else 1
         self._check(lib.epg_accumulate_rows(self.handle, _ptr(src), _ptr(ids), ids.numel(), w, _ptr(acc)))
+
+    # -- multi-GPU inside the library (epg_comm_* / epg_run_sharded) ----------------------
+    def comm_init(self, unique_id: bytes, nranks: int, rank: int):
+        """epg_comm_init: NCCL communicator of this context (id from comm_unique_id())."""
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        self._check(lib.epg_comm_init(self.handle, buf, nranks, rank))
+
+    def run_sharded(self, plan: Plan, kernel: int, state_in, state_out, payload=None, vconst=None, steps: int = 1):
+        """epg_run_sharded: `steps` sharded time steps of this rank (owned rows authoritative)."""
+        st = _State(_ptr(state_in), _ptr(state_out), _ptr(payload), _ptr(vconst))
+        self._check(lib.epg_run_sharded(self.handle, plan.handle, kernel, C.byref(st), steps))
+        return state_out if steps % 2 else state_in
 
     def set_variant(self, variant: int):
         """0 auto, 1 one CTA per partition, 2 pipelined TMA kernel, 3 occupancy TMA kernel."""
