@@ -750,6 +750,7 @@ epg_status launch_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t step
     for (int32_t s = 0; s < steps; s++) {
         a.state_in = bufs[s & 1];
         a.state_out = bufs[(s + 1) & 1];
+        a.state_end = a.state_in + (int64_t)Fn::ROW * pl->n;
         cudaEvent_t t0 = ctx->prof_begin();
         CU(launch_pdl(kern, (unsigned)pl->k, kOccThreads, smem, ctx->stream, a));
         ctx->prof_end(0, t0);
@@ -853,7 +854,9 @@ epg_status run_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, 
     OccArgs a{};
     a.off_recs = up16i(pl->blob3_max);
     const int recs_bytes = up16i(4 * Fn::REC * pl->Lcap + 64);
-    a.rows_land = up16i(recs_bytes - (4 * Fn::ROW * pl->Lcap + 16) - 16);
+    // landing area of the staged rows inside the record array (derived in place): owned rows
+    // then, for 5-float rows, one 32-byte slot per halo row (<= 32 L + 48 bytes in all)
+    a.rows_land = Fn::ROW == 5 ? 16 : up16i(recs_bytes - (4 * Fn::ROW * pl->Lcap + 16) - 16);
     a.off_phi = a.off_recs + recs_bytes;
     a.sentinel = pl->Scap;
     const size_t smem = (size_t)a.off_phi + occ_phi_bytes<Fn>(pl, &a);
@@ -866,6 +869,7 @@ epg_status run_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, 
     a.vconst = static_cast<const float *>(state->vertex_const);
     a.halo_buf = pl->halo_buf;
     a.first = 0;
+    a.state_end = nullptr;   // set per launch (the buffers alternate)
     a.hw = pl->hub_words;
     a.hub_acc = pl->n_hub > 0 ? pl->hub_acc : nullptr;
     return occ_dispatch<Fn>(pl, [&](auto kern, int, int) {
@@ -881,7 +885,9 @@ epg_status run_edges_range(epg_ctx *ctx, epg_plan *pl, epg_state *state, int64_t
     OccArgs a{};
     a.off_recs = up16i(pl->blob3_max);
     const int recs_bytes = up16i(4 * Fn::REC * pl->Lcap + 64);
-    a.rows_land = up16i(recs_bytes - (4 * Fn::ROW * pl->Lcap + 16) - 16);
+    // landing area of the staged rows inside the record array (derived in place): owned rows
+    // then, for 5-float rows, one 32-byte slot per halo row (<= 32 L + 48 bytes in all)
+    a.rows_land = Fn::ROW == 5 ? 16 : up16i(recs_bytes - (4 * Fn::ROW * pl->Lcap + 16) - 16);
     a.off_phi = a.off_recs + recs_bytes;
     a.sentinel = pl->Scap;
     const size_t smem = (size_t)a.off_phi + occ_phi_bytes<Fn>(pl, &a);
@@ -890,6 +896,7 @@ epg_status run_edges_range(epg_ctx *ctx, epg_plan *pl, epg_state *state, int64_t
     a.slots = pl->slots;
     a.state_in = static_cast<const float *>(state->state_in);
     a.state_out = static_cast<float *>(state->state_out);
+    a.state_end = a.state_in + (int64_t)Fn::ROW * pl->n;
     a.payload = static_cast<const float *>(state->edge_payload);
     a.vconst = static_cast<const float *>(state->vertex_const);
     a.halo_buf = pl->halo_buf;

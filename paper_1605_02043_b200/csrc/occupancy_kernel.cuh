@@ -59,6 +59,7 @@ struct OccArgs {
     // the partition's endpoint slots, edge payload and dt are bulk-copied into the Phi space
     // (dead until the edge phase) at these byte offsets from off_phi
     int st_slots, st_pay, st_vc;
+    const float *state_end;    // one past the last row of state_in (bound of the 32-byte halo reads)
 };
 
 // L2 prefetch of the aligned body of [g, g + bytes)
@@ -123,6 +124,12 @@ __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
     // map) gather after the copies instead: their halo rows are mostly other partitions'
     // owned rows that those CTAs' bulk copies are bringing into L2 at the same time.
     const bool early_halo = d.nH <= d.nO;
+    // 5-float rows: every halo row lands as the aligned 32 bytes that contain it (two 16-byte
+    // cp.async, L1 bypassed) in a slot of its own after the owned rows; the row sits at byte
+    // 4 (h mod 4) of the slot (20 h mod 16). One-float rows are gathered word by word.
+    constexpr bool kChunked = ROW == 5;
+    unsigned char *halo_slots = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(rows + ROW * d.nO) + 15) & ~uintptr_t(15));
     auto gather_halo = [&](const int32_t *hid, bool global_ids) {
         float *hr = rows + ROW * d.nO;
         int32_t h[VPT];                                 // all ids first: one round trip, not VPT
@@ -136,8 +143,21 @@ __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
             const int j = tid + r * BLOCK;
             if (j < d.nH) {
                 const float *src = a.state_in + (int64_t)ROW * h[r];
+                if constexpr (kChunked) {
+                    const float *base = reinterpret_cast<const float *>(reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15));
+                    unsigned char *dst = halo_slots + 32 * j;
+                    if (base + 8 <= a.state_end) {
+                        ptx::cp_async16(dst, base);
+                        ptx::cp_async16(dst + 16, base + 4);
+                    } else {                            // the array's last row: no read past its end
+                        float *d4 = reinterpret_cast<float *>(dst) + (src - base);
 #pragma unroll
-                for (int c = 0; c < ROW; c++) ptx::cp_async4(hr + ROW * j + c, src + c);
+                        for (int c = 0; c < ROW; c++) ptx::cp_async4(d4 + c, src + c);
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < ROW; c++) ptx::cp_async4(hr + ROW * j + c, src + c);
+                }
             }
         }
     };
@@ -196,8 +216,16 @@ __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
     for (int r = 0; r < VPT; r++) {
         const int j = tid + r * BLOCK;
         if (j < L) {
+            const float *row = rows + ROW * j;
+            if constexpr (kChunked) {
+                if (j >= d.nO) {
+                    const int jh = j - d.nO;
+                    row = reinterpret_cast<const float *>(halo_slots + 32 * jh) +
+                          (reinterpret_cast<const int32_t *>(sblob)[jh] & 3);
+                }
+            }
 #pragma unroll
-            for (int c = 0; c < ROW; c++) rv[r][c] = rows[ROW * j + c];
+            for (int c = 0; c < ROW; c++) rv[r][c] = row[c];
         }
     }
     __syncthreads();

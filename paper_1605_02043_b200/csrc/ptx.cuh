@@ -63,6 +63,12 @@ __device__ __forceinline__ void cp_async4(void *dst_smem, const void *src_gmem) 
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst_smem)), "l"(src_gmem) : "memory");
 }
 
+// 16-byte asynchronous global -> shared copy bypassing L1 (LDGSTS.128), both addresses
+// 16-byte aligned
+__device__ __forceinline__ void cp_async16(void *dst_smem, const void *src_gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst_smem)), "l"(src_gmem) : "memory");
+}
+
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 
 template <int N>

@@ -1,0 +1,32 @@
+"""C3 step timing only (bench.py's C3 sub-record): python tools/c3_step.py [--comparators]"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_1605_02043_b200 import epg  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--comparators", action="store_true")
+    ap.add_argument("--steps", type=int, default=20)
+    a = ap.parse_args()
+    args = argparse.Namespace(part_size=1024, c3_steps=a.steps, no_comparators=not a.comparators)
+    stream = torch.cuda.current_stream()
+    ctx = epg.Context(0, stream)
+    peak, _ = bench.measured_peaks()
+    out = bench.run_c3(args, torch, epg, ctx, stream, peak)
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

@@ -2,7 +2,8 @@
 
     ncu --metrics <...> -k regex:'k_edge|k_finalise|k_naive' python tools/ncu_variants.py --config c2
 
-Variants, in launch order: EP staged with the EPG-2 map ("ep"; edge kernel + finalise),
+Variants, in launch order: EP staged with the EPG-2 map ("ep"; edge kernel + finalise), the
+EPG-RB map ("rb", the bench's partitioner on C3),
 EP staged with the EPG-1 map ("ep1"), default-map staged (same kernels), naive original
 order (k_naive_edges + k_naive_update). `--reps R`
 repeats the sequence (ncu -s can skip the first). Prints the per-variant kernel order.
@@ -36,9 +37,11 @@ def main():
     Ud = torch.from_numpy(U).cuda()
     runs = []
     for v in a.variants.split(","):
-        if v in ("ep", "ep1", "default"):
+        if v in ("ep", "ep1", "default", "rb"):
             if v == "default":
                 part = ctx.default_partition(M.m, a.part_size)
+            elif v == "rb":
+                part = ctx.partition_rb(E, M.n, a.part_size)[0]
             else:
                 ctx.set_partition_method(epg.PARTITION_EPG2 if v == "ep" else epg.PARTITION_EPG1)
                 part = ctx.partition(E, M.n, a.part_size)[0]
