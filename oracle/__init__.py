@@ -50,6 +50,9 @@ def lib():
             "orc_partition_method": (C.c_int, [P, i64, i32, i32, i32, i32, P]),
             "orc_epg2": (C.c_int, [i64, P, i32, P, i64, i64, P]),
             "orc_partition_rb": (C.c_int, [P, i64, i32, i32, i32, i32, P]),
+            "orc_partition_rb_ranked": (C.c_int, [P, i64, i32, i32, i32, i32, P, P]),
+            "orc_partition_method_ranked": (C.c_int, [P, i64, i32, i32, i32, i32, P, P]),
+            "orc_remap_keyed": (C.c_int, [P, i64, i32, P, P, i64, P, P, P, P, P, P, i64, P]),
             "orc_rb_depth": (C.c_int, [i64, i32, i32]),
             "orc_remap": (C.c_int, [P, i64, i32, P, i64, P, P, P, P, P, P, i64, P]),
             "orc_shard_halos": (C.c_int, [P, i64, i32, P, i64, i32, P, P, P, P, i64]),
@@ -180,15 +183,17 @@ def epg2(edges, n: int, sizes, hub: int) -> np.ndarray:
     return part[:m]
 
 
-def partition(edges, n: int, P: int, shards: int = 1, method: int = 1) -> np.ndarray:
+def partition(edges, n: int, P: int, shards: int = 1, method: int = 1, ranked: bool = False):
     """method 1: EPG-1 on the contracted clone-and-connect graph T (O5); method 2: EPG-2,
-    growing on the EP objective of Eq. (1) directly (O5', reading Z20)."""
+    growing on the EP objective of Eq. (1) directly (O5', reading Z20). ranked: also return
+    each task's growth step within its partition (reading Z22)."""
     e, m = _edges(edges)
     part = np.zeros(max(m, 1), dtype=np.int32)
-    st = lib().orc_partition_method(_p(e), m, n, P, shards, method, _p(part))
+    rank = np.zeros(max(m, 1), dtype=np.int32)
+    st = lib().orc_partition_method_ranked(_p(e), m, n, P, shards, method, _p(part), _p(rank))
     if st:
         raise OracleError(st, "orc_partition")
-    return part[:m]
+    return (part[:m], rank[:m]) if ranked else part[:m]
 
 
 @dataclass
@@ -207,24 +212,29 @@ def rb_depth(k: int, shards: int = 1, leaf_parts: int = 256) -> int:
     return int(lib().orc_rb_depth(k, shards, leaf_parts))
 
 
-def partition_rb(edges, n: int, P: int, shards: int = 1, leaf_parts: int = 256) -> np.ndarray:
-    """EPG-RB (O5''): recursive graph-growing bisection, EPG-2 in every leaf."""
+def partition_rb(edges, n: int, P: int, shards: int = 1, leaf_parts: int = 256, ranked: bool = False):
+    """EPG-RB (O5''): recursive graph-growing bisection, EPG-2 in every leaf (ranked: also
+    the growth step of every task within its partition, reading Z22)."""
     e, m = _edges(edges)
     part = np.zeros(max(m, 1), np.int32)
-    st = lib().orc_partition_rb(_p(e), m, n, P, shards, leaf_parts, _p(part))
+    rank = np.zeros(max(m, 1), np.int32)
+    st = lib().orc_partition_rb_ranked(_p(e), m, n, P, shards, leaf_parts, _p(part), _p(rank))
     if st:
         raise OracleError(st, "orc_partition_rb")
-    return part[:m]
+    return (part[:m], rank[:m]) if ranked else part[:m]
 
 
-def remap(edges, n: int, part, k: int) -> Layout:
+def remap(edges, n: int, part, k: int, key=None) -> Layout:
+    """O6; key (optional, reading Z22): tasks of a partition ordered by (key, id)."""
     e, m = _edges(edges)
     part = np.ascontiguousarray(part, dtype=np.int32)
+    kk = None if key is None else np.ascontiguousarray(key, dtype=np.int32)
     out = Layout(np.zeros(m, np.int32), np.zeros(k + 1, np.int32), np.zeros(n, np.int32),
                  np.zeros(k + 1, np.int32), np.zeros(k + 1, np.int32), np.zeros(2 * m, np.int32),
                  np.zeros((m, 2), np.uint16))
-    st = lib().orc_remap(_p(e), m, n, _p(part), k, _p(out.edge_perm), _p(out.part_edge_begin), _p(out.vertex_perm),
-                         _p(out.part_vertex_begin), _p(out.halo_begin), _p(out.halo_ids), 2 * m, _p(out.slots))
+    st = lib().orc_remap_keyed(_p(e), m, n, _p(part), _p(kk) if kk is not None else None, k, _p(out.edge_perm),
+                               _p(out.part_edge_begin), _p(out.vertex_perm), _p(out.part_vertex_begin),
+                               _p(out.halo_begin), _p(out.halo_ids), 2 * m, _p(out.slots))
     if st:
         raise OracleError(st, "orc_remap")
     out.halo_ids = out.halo_ids[: int(out.halo_begin[k])].copy()

@@ -185,8 +185,10 @@ int orc_build_T(const int32_t *edges, int64_t m, int32_t n, int64_t *t_ptr, int3
 /* The pick is a plain linear scan over the tasks stamped in this partition */
 /* ("finite lst" = stamped since the reset).                                */
 /* ------------------------------------------------------------------------- */
-int orc_epg1(int64_t ntask, const int64_t *t_ptr, const int32_t *t_adj, const int32_t *t_w,
-             const int64_t *sizes, int64_t nparts, int32_t *part) {
+/* rank (may be NULL): rank[t] = the step r of 3. at which task t joined its partition (the */
+/* growth order; reading Z22 orders a partition's tasks by it in the remap).                  */
+int orc_epg1_ranked(int64_t ntask, const int64_t *t_ptr, const int32_t *t_adj, const int32_t *t_w,
+                    const int64_t *sizes, int64_t nparts, int32_t *part, int32_t *rank) {
     int64_t total = 0;
     for (int64_t i = 0; i < nparts; i++) total += sizes[i];
     if (total != ntask) return ORC_ERR_INPUT;
@@ -227,6 +229,7 @@ int orc_epg1(int64_t ntask, const int64_t *t_ptr, const int32_t *t_adj, const in
                 lst[best] = c++; stamped[nst++] = best;
             }
             part[best] = (int32_t)i;
+            if (rank) rank[best] = (int32_t)r;
             for (int64_t q = t_ptr[best]; q < t_ptr[best + 1]; q++) {
                 int64_t nb = t_adj[q];
                 if (part[nb] != -1) continue;
@@ -238,6 +241,11 @@ int orc_epg1(int64_t ntask, const int64_t *t_ptr, const int32_t *t_adj, const in
     }
     free(gst); free(lst); free(g); free(gst_order); free(stamped);
     return ORC_OK;
+}
+
+int orc_epg1(int64_t ntask, const int64_t *t_ptr, const int32_t *t_adj, const int32_t *t_w,
+             const int64_t *sizes, int64_t nparts, int32_t *part) {
+    return orc_epg1_ranked(ntask, t_ptr, t_adj, t_w, sizes, nparts, part, NULL);
 }
 
 /* ------------------------------------------------------------------------- */
@@ -267,8 +275,8 @@ int orc_epg1(int64_t ntask, const int64_t *t_ptr, const int32_t *t_adj, const in
 /* reaches it. No vertex of a mesh (degree <= 4) is a hub.                   */
 /* The pick is a plain linear scan over the tasks stamped in this partition. */
 /* ------------------------------------------------------------------------- */
-int orc_epg2(int64_t ntask, const int32_t *edges, int32_t n, const int64_t *sizes, int64_t nparts, int64_t hub,
-             int32_t *part) {
+int orc_epg2_ranked(int64_t ntask, const int32_t *edges, int32_t n, const int64_t *sizes, int64_t nparts,
+                    int64_t hub, int32_t *part, int32_t *rank) {
     int64_t total = 0;
     for (int64_t i = 0; i < nparts; i++) total += sizes[i];
     if (total != ntask) return ORC_ERR_INPUT;
@@ -328,6 +336,7 @@ int orc_epg2(int64_t ntask, const int32_t *edges, int32_t n, const int64_t *size
                 lst[best] = c++; stamped[nst++] = best;
             }
             part[best] = (int32_t)i;
+            if (rank) rank[best] = (int32_t)r;
             for (int side = 0; side < 2; side++) {
                 int32_t u = edges[2 * best + side];
                 if (side == 1 && u == edges[2 * best]) continue;   /* distinct endpoints */
@@ -348,6 +357,11 @@ int orc_epg2(int64_t ntask, const int32_t *edges, int32_t n, const int64_t *size
     return ORC_OK;
 }
 
+int orc_epg2(int64_t ntask, const int32_t *edges, int32_t n, const int64_t *sizes, int64_t nparts, int64_t hub,
+             int32_t *part) {
+    return orc_epg2_ranked(ntask, edges, n, sizes, nparts, hub, part, NULL);
+}
+
 /* Flat (shards = 1) or hierarchical (shards = G > 1) EPG-1 (O5):
  *  shard g receives partitions [floor(gk/G), floor((g+1)k/G)) and target size the
  *  sum of their s_i; EPG-1 on T with those G sizes gives shard[t]; then, for g
@@ -358,9 +372,9 @@ int orc_epg2(int64_t ntask, const int32_t *edges, int32_t n, const int64_t *size
 /* ascending id) with their original endpoints.                                       */
 static int grow_method(int method, int64_t ntask, const int64_t *tp, const int32_t *ta, const int32_t *tw,
                        const int32_t *edges, int32_t n, const int64_t *sizes, int64_t nparts, int32_t P,
-                       int32_t *part) {
-    if (method == 2) return orc_epg2(ntask, edges, n, sizes, nparts, 4 * (int64_t)P, part);
-    return orc_epg1(ntask, tp, ta, tw, sizes, nparts, part);
+                       int32_t *part, int32_t *rank) {
+    if (method == 2) return orc_epg2_ranked(ntask, edges, n, sizes, nparts, 4 * (int64_t)P, part, rank);
+    return orc_epg1_ranked(ntask, tp, ta, tw, sizes, nparts, part, rank);
 }
 
 int orc_partition_method(const int32_t *edges, int64_t m, int32_t n, int32_t P, int32_t shards, int32_t method,
@@ -370,8 +384,17 @@ int orc_partition(const int32_t *edges, int64_t m, int32_t n, int32_t P, int32_t
     return orc_partition_method(edges, m, n, P, shards, 1, part);
 }
 
+int orc_partition_method_ranked(const int32_t *edges, int64_t m, int32_t n, int32_t P, int32_t shards,
+                                int32_t method, int32_t *part, int32_t *rank);
+
 int orc_partition_method(const int32_t *edges, int64_t m, int32_t n, int32_t P, int32_t shards, int32_t method,
                          int32_t *part) {
+    return orc_partition_method_ranked(edges, m, n, P, shards, method, part, NULL);
+}
+
+/* rank (may be NULL): each task's growth step within its final partition */
+int orc_partition_method_ranked(const int32_t *edges, int64_t m, int32_t n, int32_t P, int32_t shards,
+                                int32_t method, int32_t *part, int32_t *rank) {
     if (m <= 0 || n <= 0) return ORC_ERR_INPUT;
     if (method != 1 && method != 2) return ORC_ERR_INPUT;
     if (orc_first_bad_edge(edges, m, n) >= 0) return ORC_ERR_INPUT;
@@ -389,7 +412,7 @@ int orc_partition_method(const int32_t *edges, int64_t m, int32_t n, int32_t P, 
     orc_part_sizes(m, k, s);
 
     if (shards == 1) {
-        st = grow_method(method, m, t_ptr, t_adj, t_w, edges, n, s, k, P, part);
+        st = grow_method(method, m, t_ptr, t_adj, t_w, edges, n, s, k, P, part, rank);
     } else {
         int64_t Gs = shards;
         int64_t *ssize = (int64_t *)calloc(Gs, sizeof(int64_t));
@@ -397,13 +420,14 @@ int orc_partition_method(const int32_t *edges, int64_t m, int32_t n, int32_t P, 
             for (int64_t i = gi * k / Gs; i < (gi + 1) * k / Gs; i++) ssize[gi] += s[i];
         int32_t *shard = (int32_t *)malloc(sizeof(int32_t) * m);
         int32_t *sedges = (int32_t *)malloc(sizeof(int32_t) * 2 * m);    /* shard's edge list */
-        st = grow_method(method, m, t_ptr, t_adj, t_w, edges, n, ssize, Gs, P, shard);
+        st = grow_method(method, m, t_ptr, t_adj, t_w, edges, n, ssize, Gs, P, shard, NULL);
         int64_t *loc = (int64_t *)malloc(sizeof(int64_t) * m);   /* task -> id inside its shard */
         int64_t *glob = (int64_t *)malloc(sizeof(int64_t) * m);  /* local id -> task           */
         int64_t *sp = (int64_t *)malloc(sizeof(int64_t) * (m + 1));
         int32_t *sa = (int32_t *)malloc(sizeof(int32_t) * (nnz > 0 ? nnz : 1));
         int32_t *sw = (int32_t *)malloc(sizeof(int32_t) * (nnz > 0 ? nnz : 1));
         int32_t *sub = (int32_t *)malloc(sizeof(int32_t) * m);
+        int32_t *subr = (int32_t *)malloc(sizeof(int32_t) * m);
         for (int64_t gi = 0; gi < Gs && st == ORC_OK; gi++) {
             int64_t mg = 0;
             for (int64_t t = 0; t < m; t++) if (shard[t] == gi) { loc[t] = mg; glob[mg] = t; mg++; }
@@ -418,10 +442,14 @@ int orc_partition_method(const int32_t *edges, int64_t m, int32_t n, int32_t P, 
             }
             for (int64_t j = 0; j < mg; j++) { sedges[2 * j] = edges[2 * glob[j]]; sedges[2 * j + 1] = edges[2 * glob[j] + 1]; }
             int64_t p0 = gi * k / Gs, p1 = (gi + 1) * k / Gs;
-            st = grow_method(method, mg, sp, sa, sw, sedges, n, s + p0, p1 - p0, P, sub);
-            for (int64_t j = 0; j < mg; j++) part[glob[j]] = (int32_t)(sub[j] + p0);
+            st = grow_method(method, mg, sp, sa, sw, sedges, n, s + p0, p1 - p0, P, sub, subr);
+            for (int64_t j = 0; j < mg; j++) {
+                part[glob[j]] = (int32_t)(sub[j] + p0);
+                if (rank) rank[glob[j]] = subr[j];
+            }
         }
         free(ssize); free(shard); free(sedges); free(loc); free(glob); free(sp); free(sa); free(sw); free(sub);
+        free(subr);
     }
     free(t_ptr); free(t_adj); free(t_w); free(s);
     return st;
@@ -493,8 +521,17 @@ static int cmp_dist_id(const void *x, const void *y) {
     return (a > b) - (a < b);
 }
 
+int orc_partition_rb_ranked(const int32_t *edges, int64_t m, int32_t n, int32_t P, int32_t shards,
+                            int32_t leaf_parts, int32_t *part, int32_t *rank);
+
 int orc_partition_rb(const int32_t *edges, int64_t m, int32_t n, int32_t P, int32_t shards, int32_t leaf_parts,
                      int32_t *part) {
+    return orc_partition_rb_ranked(edges, m, n, P, shards, leaf_parts, part, NULL);
+}
+
+/* rank (may be NULL): each task's growth step within its partition (the leaf's EPG-2) */
+int orc_partition_rb_ranked(const int32_t *edges, int64_t m, int32_t n, int32_t P, int32_t shards,
+                            int32_t leaf_parts, int32_t *part, int32_t *rank) {
     if (m <= 0 || n <= 0 || leaf_parts < 1) return ORC_ERR_INPUT;
     if (orc_first_bad_edge(edges, m, n) >= 0) return ORC_ERR_INPUT;
     if (P < 1 || P > ORC_MAX_PART) return ORC_ERR_INFEASIBLE;
@@ -557,6 +594,7 @@ int orc_partition_rb(const int32_t *edges, int64_t m, int32_t n, int32_t P, int3
     const int64_t leaves = (int64_t)1 << d;
     int32_t *sedges = (int32_t *)malloc(sizeof(int32_t) * 2 * m);
     int32_t *sub = (int32_t *)malloc(sizeof(int32_t) * m);
+    int32_t *subr = (int32_t *)malloc(sizeof(int32_t) * m);
     int st = ORC_OK;
     for (int64_t j = 0; j < leaves && st == ORC_OK; j++) {
         int64_t nt = 0;
@@ -564,9 +602,13 @@ int orc_partition_rb(const int32_t *edges, int64_t m, int32_t n, int32_t P, int3
             if (node[t] == j) { tasks[nt] = t; sedges[2 * nt] = edges[2 * t]; sedges[2 * nt + 1] = edges[2 * t + 1]; nt++; }
         const int64_t p0 = j * k / leaves, p1 = (j + 1) * k / leaves;
         if (nt == 0) continue;
-        st = orc_epg2(nt, sedges, n, s + p0, p1 - p0, hub, sub);
-        for (int64_t q = 0; q < nt; q++) part[tasks[q]] = (int32_t)(sub[q] + p0);
+        st = orc_epg2_ranked(nt, sedges, n, s + p0, p1 - p0, hub, sub, subr);
+        for (int64_t q = 0; q < nt; q++) {
+            part[tasks[q]] = (int32_t)(sub[q] + p0);
+            if (rank) rank[tasks[q]] = subr[q];
+        }
     }
+    free(subr);
     free(s); free(S); free(ip); free(inc); free(node); free(next); free(dist); free(queue); free(tasks); free(vis);
     free(sedges); free(sub);
     return st;
@@ -590,17 +632,39 @@ static int cmp_i64(const void *x, const void *y) {
     return a < b ? -1 : (a > b ? 1 : 0);
 }
 
+typedef struct { int64_t a, b, c; } trip64;
+static int cmp_trip64(const void *x, const void *y) {
+    const trip64 *p = (const trip64 *)x, *q = (const trip64 *)y;
+    if (p->a != q->a) return p->a < q->a ? -1 : 1;
+    if (p->b != q->b) return p->b < q->b ? -1 : 1;
+    if (p->c != q->c) return p->c < q->c ? -1 : 1;
+    return 0;
+}
+
+int orc_remap_keyed(const int32_t *edges, int64_t m, int32_t n, const int32_t *part, const int32_t *key_in, int64_t k,
+                    int32_t *edge_perm, int32_t *part_edge_begin, int32_t *vertex_perm, int32_t *part_vertex_begin,
+                    int32_t *halo_begin, int32_t *halo_ids, int64_t halo_cap, uint16_t *slots);
+
 int orc_remap(const int32_t *edges, int64_t m, int32_t n, const int32_t *part, int64_t k,
               int32_t *edge_perm, int32_t *part_edge_begin, int32_t *vertex_perm, int32_t *part_vertex_begin,
               int32_t *halo_begin, int32_t *halo_ids, int64_t halo_cap, uint16_t *slots) {
+    return orc_remap_keyed(edges, m, n, part, NULL, k, edge_perm, part_edge_begin, vertex_perm, part_vertex_begin,
+                           halo_begin, halo_ids, halo_cap, slots);
+}
+
+/* key_in (may be NULL = the task id): reading Z22 orders the tasks of a partition by the   */
+/* partitioner's growth rank, then id -- step 1 sorts by (part, key, id).                    */
+int orc_remap_keyed(const int32_t *edges, int64_t m, int32_t n, const int32_t *part, const int32_t *key_in, int64_t k,
+                    int32_t *edge_perm, int32_t *part_edge_begin, int32_t *vertex_perm, int32_t *part_vertex_begin,
+                    int32_t *halo_begin, int32_t *halo_ids, int64_t halo_cap, uint16_t *slots) {
     if (m <= 0 || n <= 0 || k <= 0) return ORC_ERR_INPUT;
     if (orc_first_bad_edge(edges, m, n) >= 0) return ORC_ERR_INPUT;
     for (int64_t e = 0; e < m; e++) if (part[e] < 0 || part[e] >= k) return ORC_ERR_INPUT;
-    /* 1. sort by (part, id) */
-    pair64 *pe = (pair64 *)malloc(sizeof(pair64) * m);
-    for (int64_t e = 0; e < m; e++) { pe[e].a = part[e]; pe[e].b = e; }
-    qsort(pe, m, sizeof(pair64), cmp_pair64);
-    for (int64_t i = 0; i < m; i++) edge_perm[i] = (int32_t)pe[i].b;
+    /* 1. sort by (part, key, id) */
+    trip64 *pe = (trip64 *)malloc(sizeof(trip64) * m);
+    for (int64_t e = 0; e < m; e++) { pe[e].a = part[e]; pe[e].b = key_in ? key_in[e] : e; pe[e].c = e; }
+    qsort(pe, m, sizeof(trip64), cmp_trip64);
+    for (int64_t i = 0; i < m; i++) edge_perm[i] = (int32_t)pe[i].c;
     for (int64_t p = 0; p <= k; p++) part_edge_begin[p] = 0;
     for (int64_t e = 0; e < m; e++) part_edge_begin[part[e] + 1]++;
     for (int64_t p = 0; p < k; p++) part_edge_begin[p + 1] += part_edge_begin[p];

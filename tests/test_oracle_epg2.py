@@ -21,9 +21,11 @@ from bruteforce import loads_and_cut, optimum
 from conftest import golden
 
 
-def epg2_python(edges, n, sizes, hub):
-    """O5' transcribed literally (pure Python, small inputs only)."""
+def epg2_python(edges, n, sizes, hub, with_rank=False):
+    """O5' transcribed literally (pure Python, small inputs only); with_rank: also the step at
+    which each task joined its partition (reading Z22)."""
     m = len(edges)
+    rank = [-1] * m
     INF = float("inf")
     inc = [[] for _ in range(n)]
     for t, (u, v) in enumerate(edges):
@@ -41,7 +43,7 @@ def epg2_python(edges, n, sizes, hub):
             continue
         lst[seed] = c
         c += 1
-        for _ in range(size):
+        for step in range(size):
             front = [t for t in range(m) if part[t] == -1 and lst[t] != INF]
             if not front:
                 best = min(t for t in range(m) if part[t] == -1)
@@ -50,6 +52,7 @@ def epg2_python(edges, n, sizes, hub):
             else:
                 best = max(front, key=lambda t: (g[t], -lst[t]))
             part[best] = i
+            rank[best] = step
             u, v = edges[best]
             for w in ([u] if u == v else [u, v]):
                 if w in inV:
@@ -67,7 +70,7 @@ def epg2_python(edges, n, sizes, hub):
                     if gst[t2] == INF:
                         gst[t2] = G
                         G += 1
-    return part
+    return (part, rank) if with_rank else part
 
 
 def test_epg2_fig_mot():
@@ -107,7 +110,13 @@ def test_epg2_invariants_and_transcription(seed):
     part = O.partition(e, n, P, method=2)
     assert np.bincount(part, minlength=k).tolist() == O.part_sizes(m, k).tolist()   # exact +-1 (Z2)
     assert np.array_equal(part, O.partition(e, n, P, method=2))                      # deterministic
-    assert part.tolist() == epg2_python(e.tolist(), n, O.part_sizes(m, k).tolist(), 4 * P)
+    rp, rr = epg2_python(e.tolist(), n, O.part_sizes(m, k).tolist(), 4 * P, with_rank=True)
+    assert part.tolist() == rp
+    part2, rank = O.partition(e, n, P, method=2, ranked=True)
+    assert part2.tolist() == rp and rank.tolist() == rr
+    # the ranks of every partition are its growth steps 0 .. s_i - 1
+    for p in range(k):
+        assert sorted(rank[part == p].tolist()) == list(range(int((part == p).sum())))
 
 
 def test_epg2_vs_bruteforce():
@@ -200,7 +209,7 @@ def test_epg2_quality_on_cfd_mesh(mesh_c1):
 
 # ------------------------------------------------------------------------------------
 # EPG-RB (O5'', reading Z21): recursive graph-growing bisection, EPG-2 in every leaf.
-def rb_python(edges, n, P, shards=1, leaf_parts=256):
+def rb_python(edges, n, P, shards=1, leaf_parts=256, with_rank=False):
     """O5'' transcribed literally (pure Python, small inputs only)."""
     from collections import deque
     m = len(edges)
@@ -253,17 +262,18 @@ def rb_python(edges, n, P, shards=1, leaf_parts=256):
             for j, t in enumerate(sorted(tasks, key=lambda t: (d2[t], t))):
                 nxt[t] = 2 * a + (0 if j < N0 else 1)
         node = nxt
-    part = [-1] * m
+    part, rank = [-1] * m, [-1] * m
     leaves = 1 << d
     for j in range(leaves):
         tasks = [t for t in range(m) if node[t] == j]
         p0, p1 = j * k // leaves, (j + 1) * k // leaves
         if not tasks:
             continue
-        sub = epg2_python([edges[t] for t in tasks], n, s[p0:p1], hub)
-        for t, x in zip(tasks, sub):
+        sub, subr = epg2_python([edges[t] for t in tasks], n, s[p0:p1], hub, with_rank=True)
+        for t, x, r in zip(tasks, sub, subr):
             part[t] = x + p0
-    return part
+            rank[t] = r
+    return (part, rank) if with_rank else part
 
 
 def test_rb_fig_mot():
@@ -302,7 +312,9 @@ def test_rb_literal_transcription(seed):
         if shards > k:
             continue
         for lp in (1, 2, 1000):
-            assert O.partition_rb(e, n, P, shards, lp).tolist() == rb_python(el, n, P, shards, lp)
+            part, rank = O.partition_rb(e, n, P, shards, lp, ranked=True)
+            rp, rr = rb_python(el, n, P, shards, lp, with_rank=True)
+            assert part.tolist() == rp and rank.tolist() == rr
 
 
 def test_rb_invariants_and_shards(small_mesh):

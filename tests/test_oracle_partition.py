@@ -222,8 +222,8 @@ def T_python(edges, n):
     return [sorted(d.items()) for d in nbrs]      # (nb, w), ascending nb
 
 
-def epg1_python(nbrs, sizes):
-    """O5 flat mode, step by step."""
+def epg1_python(nbrs, sizes, rank=None):
+    """O5 flat mode, step by step (rank: optional list receiving each task's growth step)."""
     m = len(nbrs)
     INF = float("inf")
     part, gst, G = [-1] * m, [INF] * m, 0
@@ -235,7 +235,7 @@ def epg1_python(nbrs, sizes):
             continue
         lst[seed] = c
         c += 1
-        for _ in range(size):
+        for step in range(size):
             front = [t for t in range(m) if part[t] == -1 and lst[t] != INF]
             if not front:
                 t = min(t for t in range(m) if part[t] == -1)
@@ -244,6 +244,8 @@ def epg1_python(nbrs, sizes):
             else:
                 t = max(front, key=lambda t: (g[t], -lst[t]))
             part[t] = i
+            if rank is not None:
+                rank[t] = step
             for nb, w in nbrs[t]:
                 if part[nb] != -1:
                     continue
@@ -257,7 +259,7 @@ def epg1_python(nbrs, sizes):
     return part
 
 
-def partition_python(edges, n, P, shards=1):
+def partition_python(edges, n, P, shards=1, rank=None):
     """O1 sizes + O5 (flat, or hierarchical: shard-level EPG-1, then EPG-1 on T restricted to
     each shard with tasks renumbered by ascending id, partition ids offset by floor(gk/G))."""
     m = len(edges)
@@ -265,7 +267,7 @@ def partition_python(edges, n, P, shards=1):
     s = [m // k + (1 if i < m % k else 0) for i in range(k)]
     nbrs = T_python(edges, n)
     if shards == 1:
-        return epg1_python(nbrs, s)
+        return epg1_python(nbrs, s, rank)
     G = shards
     ssize = [sum(s[g * k // G:(g + 1) * k // G]) for g in range(G)]
     shard = epg1_python(nbrs, ssize)
@@ -274,9 +276,12 @@ def partition_python(edges, n, P, shards=1):
         mem = [t for t in range(m) if shard[t] == g]
         loc = {t: j for j, t in enumerate(mem)}
         sub = [[(loc[nb], w) for nb, w in nbrs[t] if shard[nb] == g] for t in mem]
-        res = epg1_python(sub, s[g * k // G:(g + 1) * k // G])
+        rk = [-1] * len(mem)
+        res = epg1_python(sub, s[g * k // G:(g + 1) * k // G], rk)
         for j, t in enumerate(mem):
             part[t] = res[j] + g * k // G
+            if rank is not None:
+                rank[t] = rk[j]
     return part
 
 
@@ -289,6 +294,10 @@ def test_epg1_literal_transcription(seed):
     n, e = S.random_multigraph(500 + seed, m, n0)
     P = int(rng.integers(2, 12))
     el = [tuple(map(int, x)) for x in e]
-    assert O.partition(e, n, P).tolist() == partition_python(el, n, P)
+    rk = [-1] * m
+    part, rank = O.partition(e, n, P, ranked=True)
+    assert part.tolist() == partition_python(el, n, P, rank=rk) and rank.tolist() == rk
     if O.num_parts(m, P) >= 2:
-        assert O.partition(e, n, P, shards=2).tolist() == partition_python(el, n, P, shards=2)
+        rk = [-1] * m
+        part, rank = O.partition(e, n, P, shards=2, ranked=True)
+        assert part.tolist() == partition_python(el, n, P, shards=2, rank=rk) and rank.tolist() == rk

@@ -8,16 +8,20 @@ import synth as S
 from conftest import golden
 
 
-def cpack_sequential(edges, n, part, k):
+def cpack_sequential(edges, n, part, k, key=None):
     """cpack as the sequential first-touch walk of SPEC S:381 (a different formulation
-    from the oracle's key sort): clusters ascending, tasks ascending, endpoints (u, v);
-    each object gets the next free position on first touch; untouched appended by id."""
+    from the oracle's key sort): clusters ascending, tasks ascending (by (key, id) with a
+    key, reading Z22), endpoints (u, v); each object gets the next free position on first
+    touch; untouched appended by id."""
     new = -np.ones(n, np.int64)
     nxt = 0
     block_begin = []
     for p in range(k):
         block_begin.append(nxt)
-        for e in np.nonzero(part == p)[0]:
+        tasks = np.nonzero(part == p)[0]
+        if key is not None:
+            tasks = sorted(tasks.tolist(), key=lambda e: (key[e], e))
+        for e in tasks:
             for v in edges[e]:
                 if new[v] < 0:
                     new[v] = nxt
@@ -30,13 +34,14 @@ def cpack_sequential(edges, n, part, k):
     return new, np.array(block_begin)
 
 
-def check_layout(edges, n, part, k, lay):
+def check_layout(edges, n, part, k, lay, key=None):
     m = edges.shape[0]
-    # 1. edge order by (part, id)
-    assert np.array_equal(lay.edge_perm, np.lexsort((np.arange(m), part)))
+    # 1. edge order by (part, id), or (part, key, id) (reading Z22)
+    order = np.lexsort((np.arange(m), part)) if key is None else np.lexsort((np.arange(m), key, part))
+    assert np.array_equal(lay.edge_perm, order)
     assert np.array_equal(lay.part_edge_begin, np.concatenate([[0], np.cumsum(np.bincount(part, minlength=k))]))
     # 2-4. cpack vs the sequential walk
-    new, bb = cpack_sequential(edges, n, part, k)
+    new, bb = cpack_sequential(edges, n, part, k, key)
     assert np.array_equal(lay.vertex_perm, new)
     assert np.array_equal(lay.part_vertex_begin, bb)
     assert sorted(lay.vertex_perm.tolist()) == list(range(n))            # bijection
@@ -95,6 +100,40 @@ def test_mesh_layout(small_mesh):
         k = O.num_parts(M.m, P)
         for part in (O.partition(M.edges, M.n, P), O.default_partition(M.m, P)):
             check_layout(M.edges, M.n, part, k, O.remap(M.edges, M.n, part, k))
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_layouts_keyed(seed):
+    """Reading Z22: with an order key (the partitioner's growth rank) the tasks of a
+    partition are ordered by (key, id); every other step of O6 is unchanged."""
+    rng = np.random.default_rng(900 + seed)
+    m, n = int(rng.integers(1, 120)), int(rng.integers(1, 60))
+    n, e = S.random_multigraph(70 + seed, m, n)
+    k = int(rng.integers(1, 9))
+    part = rng.integers(0, k, m).astype(np.int32)
+    key = rng.integers(0, 5, m).astype(np.int32)          # ties broken by id
+    check_layout(e, n, part, k, O.remap(e, n, part, k, key), key)
+
+
+def test_mesh_layout_growth_order(small_mesh):
+    """The growth-ranked remap of an EPG map keeps every invariant (L, C, bijection) and
+    gives consecutive tasks of a partition shared or near vertices: the mean jump of the
+    smaller local slot between consecutive tasks drops to less than half of the id order's
+    (the staged kernel's threads then read nearby records)."""
+    M = small_mesh
+    P = 256
+    k = O.num_parts(M.m, P)
+    part, rank = O.partition(M.edges, M.n, P, method=2, ranked=True)
+    lay_r = O.remap(M.edges, M.n, part, k, rank)
+    check_layout(M.edges, M.n, part, k, lay_r, rank)
+    lay_i = O.remap(M.edges, M.n, part, k)
+    def jump(lay):
+        d = []
+        for p in range(k):
+            sl = lay.slots[lay.part_edge_begin[p]:lay.part_edge_begin[p + 1]].astype(np.int64).min(axis=1)
+            d.extend(np.abs(np.diff(sl)).tolist())
+        return float(np.mean(d))
+    assert jump(lay_r) < 0.5 * jump(lay_i)
 
 
 def test_shard_halos(small_mesh):
