@@ -71,6 +71,7 @@ class Workload:
             self.state, self.payload, self.vconst = S.int_vector(1608, self.n, 0, 7), None, None
             self.per_edge, self.per_vertex = 8, 8       # 8 B ids; 4 B x read, 4 B y write
             self.exec_rows = 1024                       # one-float rows (profiles/r01_c4_exec_sweep.txt)
+            self.leaf_parts = 4096                      # EPG-RB: R 17.1 in 24 s (512: R 18.5 in 14 s)
         elif config == "c5":
             self.n, self.edges, w = S.stencil2d_spmv(3536)
             self.m = self.edges.shape[0]
@@ -83,6 +84,8 @@ class Workload:
         else:
             raise ValueError(config)
         self.gen_s = time.perf_counter() - t0
+        if not hasattr(self, "leaf_parts"):
+            self.leaf_parts = 512
 
     def alg_bytes(self, touched: int) -> int:
         """SURVEY §8(d) compulsory bytes of one step."""
@@ -118,6 +121,13 @@ def parse():
                          "Eq. (1)'s objective) or rb (GPU recursive bisection + EPG-2 leaves on all host cores; "
                          "SURVEY 8(f) rank 2); on C2 (k = 448 < 512) rb has depth 0 and equals epg2")
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 (bandwidth-regime) sub-record")
+    ap.add_argument("--hub-l2", type=int, default=0,
+                    help="persisting L2 window over hub rows (epg_set_hub_l2; measured slower on C4, off)")
+    ap.add_argument("--order", choices=["growth", "id"], default="growth",
+                    help="task order inside a partition for the remap: the partitioner's growth steps "
+                         "(epg_remap_keyed, reading Z22) or the task id (epg_remap)")
+    ap.add_argument("--leaf-parts", type=int, default=0,
+                    help="EPG-RB leaf size (0: the config's default -- 512, or 4096 on R-MAT)")
     ap.add_argument("--c3-steps", type=int, default=20)
     ap.add_argument("--exec-rows", type=int, default=0,
                     help="execution-split row cap (epg_set_exec_limits; 0 = the config's default)")
@@ -158,7 +168,8 @@ def ncu_evidence(config: str):
     if vs:
         with open(vs[-1]) as f:
             d = json.load(f)
-        variants = {k: {kk: v[kk] for kk in ("dram_bytes_per_edge", "l2_sm_bytes_per_edge") if kk in v}
+        variants = {k: {kk: v[kk] for kk in ("dram_bytes_per_edge", "l2_sm_bytes_per_edge", "dram_reduction_vs_default",
+                                             "l2_reduction_vs_default") if kk in v}
                     for k, v in d["schedules"].items()}
         variants["source"] = os.path.relpath(vs[-1], ROOT) + " (ncu, cold L2 per kernel)"
     return traffic, src, variants
@@ -405,13 +416,15 @@ def run_sharded(args, rank, local_rank, world):
     ctx.comm_init(bytes(uid.numpy().tobytes()), world, rank)
     t0 = time.perf_counter()
     part = torch.empty(M.m, dtype=torch.int32, device=dev)
+    grank = torch.empty(M.m, dtype=torch.int32, device=dev)
     if rank == 0:
-        part, rep0 = ctx.partition_rb(E, M.n, P, shards=world)
+        part, grank, rep0 = ctx.partition_rb(E, M.n, P, shards=world, leaf_parts=M.leaf_parts, ranked=True)
     if world > 1:
         dist.broadcast(part, 0)
+        dist.broadcast(grank, 0)
     rep = ctx.load_count(E, M.n, part, k)
     t_part = time.perf_counter() - t0
-    L, plan = ctx.remap(E, M.n, part, k, halo_cap=rep.cut_cost)
+    L, plan = ctx.remap(E, M.n, part, k, halo_cap=rep.cut_cost, order_key=grank if args.order == "growth" else None)
     Ud = torch.from_numpy(M.state).to(dev)
     nrm = None if M.payload is None else ctx.permute_rows(torch.from_numpy(M.payload).to(dev), L.edge_perm,
                                                           epg.PERM_GATHER)
@@ -504,8 +517,8 @@ class Replica:
     """One independent copy of a workload's per-step inputs in the plan layout: its own plan
     (remapped from the same map), state ping-pong buffers, payload and constants."""
 
-    def __init__(self, ctx, epg, M, E, part, k, halo_cap, pay0, vc0, Ud):
-        self.L, self.plan = ctx.remap(E, M.n, part, k, halo_cap=halo_cap)
+    def __init__(self, ctx, epg, M, E, part, k, halo_cap, pay0, vc0, Ud, key=None):
+        self.L, self.plan = ctx.remap(E, M.n, part, k, halo_cap=halo_cap, order_key=key)
         self.nrm = None if pay0 is None else ctx.permute_rows(pay0, self.L.edge_perm, epg.PERM_GATHER)
         self.dt = None if vc0 is None else ctx.permute_rows(vc0, self.L.vertex_perm, epg.PERM_SCATTER)
         self.bufs = [ctx.permute_rows(Ud, self.L.vertex_perm, epg.PERM_SCATTER), None]
@@ -548,14 +561,15 @@ def run_c3(args, torch, epg, ctx, stream, peak):
     ctx.set_exec_limits(704, 1024)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    part, rep = ctx.partition_rb(E, M.n, P)
+    part, rank, rep = ctx.partition_rb(E, M.n, P, ranked=True)
     t_part = time.perf_counter() - t0
+    key = rank if getattr(args, "order", "growth") == "growth" else None
     pay0 = torch.from_numpy(M.normals).to(dev)
     vc0 = torch.from_numpy(S.cfd_dt(M.volume)).to(dev)
     Ud = torch.from_numpy(S.cfd_state(M.n)).to(dev)
     del M
     t0 = time.perf_counter()
-    R = Replica(ctx, epg, _MeshN(Ud.shape[0]), E, part, k, rep.cut_cost, pay0, vc0, Ud)
+    R = Replica(ctx, epg, _MeshN(Ud.shape[0]), E, part, k, rep.cut_cost, pay0, vc0, Ud, key)
     torch.cuda.synchronize()
     t_remap = time.perf_counter() - t0
     K = args.c3_steps
@@ -631,18 +645,23 @@ def run_ours(args, rank, local_rank, world):
         M.exec_rows = args.exec_rows
     ctx.set_exec_limits(M.exec_rows, args.exec_edges or (1280 if P > 1024 else 1024))
     ctx.set_variant(args.variant)
+    ctx.set_hub_l2(bool(args.hub_l2))
     E = torch.from_numpy(M.edges).to(dev)
     k = epg.num_parts(M.m, P)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    ctx.set_partition_method(PARTITIONERS[args.partitioner])
-    part, rep = ctx.partition(E, M.n, P)                      # EP partition + GPU cost kernel
+    if args.partitioner == "rb":                              # GPU bisection + host EPG-2 leaves
+        part, rank, rep = ctx.partition_rb(E, M.n, P, 1, args.leaf_parts or M.leaf_parts, ranked=True)
+    else:
+        ctx.set_partition_method(PARTITIONERS[args.partitioner])
+        part, rank, rep = ctx.partition_ranked(E, M.n, P)    # host EPG + GPU cost kernel
+    key = rank if args.order == "growth" else None
     t_part = time.perf_counter() - t0
     Ud = torch.from_numpy(M.state).to(dev)
     pay0 = None if M.payload is None else torch.from_numpy(M.payload).to(dev)
     vc0 = None if M.vconst is None else torch.from_numpy(M.vconst).to(dev)
     t0 = time.perf_counter()
-    reps = [Replica(ctx, epg, M, E, part, k, rep.cut_cost, pay0, vc0, Ud)]
+    reps = [Replica(ctx, epg, M, E, part, k, rep.cut_cost, pay0, vc0, Ud, key)]
     torch.cuda.synchronize()
     t_remap = time.perf_counter() - t0
     plan, L = reps[0].plan, reps[0].L
@@ -650,7 +669,7 @@ def run_ours(args, rank, local_rank, world):
     l2 = l2_bytes(torch, dev)
     nrep = int(min(64, max(2, -(-3 * l2 // max(1, reps[0].footprint())))))
     while len(reps) < nrep:
-        reps.append(Replica(ctx, epg, M, E, part, k, rep.cut_cost, pay0, vc0, Ud))
+        reps.append(Replica(ctx, epg, M, E, part, k, rep.cut_cost, pay0, vc0, Ud, key))
     flushbuf = torch.empty(args.flush_mib * (1 << 20) // 4, dtype=torch.float32, device=dev)
 
     def flush():
@@ -749,8 +768,8 @@ def run_ours(args, rank, local_rank, world):
         for other in ("epg1", "epg2"):
             if other == args.partitioner or (other == "epg2" and KER == epg.KERNEL_GATHER_SCATTER):
                 continue                                  # EPG-2 flat is too slow on R-MAT hubs
-            baselines.append((f"ep_{other}", lambda o=other: epg.partition_host(M.edges, M.n, P,
-                                                                                method=PARTITIONERS[o])))
+            baselines.append((f"ep_{other}", lambda o=other: epg.partition_host_ranked(M.edges, M.n, P, 1,
+                                                                                       PARTITIONERS[o])))
         baselines.append(("powergraph_random", lambda: epg.partition_random_host(M.m, P, 1605)))
         if KER != epg.KERNEL_GATHER_SCATTER:
             baselines.append(("powergraph_greedy", lambda: epg.partition_greedy_host(M.edges, M.n, P)))
@@ -759,9 +778,13 @@ def run_ours(args, rank, local_rank, world):
             t0 = time.perf_counter()
             bpart_h = make()
             t_b = time.perf_counter() - t0
+            bkey = None
+            if isinstance(bpart_h, tuple):                    # an EPG map with its growth ranks
+                bpart_h, bkey_h = bpart_h
+                bkey = torch.from_numpy(bkey_h).to(dev) if args.order == "growth" else None
             bpart = torch.from_numpy(bpart_h).to(dev)
             brep = ctx.load_count(E, M.n, bpart, k)
-            BL, bplan = ctx.remap(E, M.n, bpart, k, halo_cap=brep.cut_cost)
+            BL, bplan = ctx.remap(E, M.n, bpart, k, halo_cap=brep.cut_cost, order_key=bkey)
             bn = None if pay0 is None else ctx.permute_rows(pay0, BL.edge_perm, epg.PERM_GATHER)
             bd = None if vc0 is None else ctx.permute_rows(vc0, BL.vertex_perm, epg.PERM_SCATTER)
             bb = [ctx.permute_rows(Ud, BL.vertex_perm, epg.PERM_SCATTER), torch.empty_like(Ud)]
@@ -842,7 +865,7 @@ def run_ours(args, rank, local_rank, world):
                         "calls incl. the per-step L2 flush, / K"},
         "gpu_launches": launches,
         "clocks": clk,
-        "partition": {"method": args.partitioner, "k": k, "k_exec": plan.k_exec,
+        "partition": {"method": args.partitioner, "order_in_partition": args.order, "k": k, "k_exec": plan.k_exec,
                       "load_count": rep.load_count, "touched": rep.touched, "cut_cost": rep.cut_cost,
                       "replication": rep.replication, "redundant_fraction": rep.redundant_fraction,
                       "max_size": rep.max_size, "min_size": rep.min_size, "shared_vertices": plan.shared,

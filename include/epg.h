@@ -181,6 +181,10 @@ epg_status epg_partition_host(const int32_t *edges, int64_t m, int32_t n_vertice
  * epg_partition_rb), so epg_partition_host_method rejects it. */
 #define EPG_PARTITION_RB 3
 /* epg_partition_host with a method (EPG_ERR_INPUT for any other value). */
+epg_status epg_partition_host_ranked(const int32_t *edges, int64_t m, int32_t n_vertices, int32_t part_size,
+                                     int32_t shards, int32_t method, int32_t *part_of_edge, int32_t *rank_of_edge,
+                                     char *errbuf, int64_t errbuf_len);
+/* (the same, without ranks; rank_of_edge [m] HOST out of the one above: each task's growth step) */
 epg_status epg_partition_host_method(const int32_t *edges, int64_t m, int32_t n_vertices, int32_t part_size,
                                      int32_t shards, int32_t method, int32_t *part_of_edge, char *errbuf,
                                      int64_t errbuf_len);
@@ -214,9 +218,15 @@ epg_status epg_partition(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t 
 /* epg_partition with EPG_PARTITION_RB and an explicit leaf size (epg_partition uses 512, or
  * the EPG_RB_LEAF_PARTS environment variable). EPG_ERR_INPUT for leaf_parts < 1 or m >= 2^30;
  * EPG_ERR_INFEASIBLE as for epg_partition_host, or if a BFS is deeper than 2^22 - 2 levels.
- *   edges [m][2] host or device; part_of_edge [m] host or device out; out report. */
+ *   edges [m][2] host or device; part_of_edge [m] host or device out; rank_of_edge [m] host or
+ *   device out, or NULL: the step at which each task joined its partition (EPG-2's growth in
+ *   its leaf; reading Z22, for epg_remap_keyed); out report. */
 epg_status epg_partition_rb(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n_vertices, int32_t part_size,
-                            int32_t shards, int32_t leaf_parts, int32_t *part_of_edge, epg_report *out);
+                            int32_t shards, int32_t leaf_parts, int32_t *part_of_edge, int32_t *rank_of_edge,
+                            epg_report *out);
+/* epg_partition that also returns the growth ranks (as epg_partition_rb; any method). */
+epg_status epg_partition_ranked(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n_vertices, int32_t part_size,
+                                int32_t shards, int32_t *part_of_edge, int32_t *rank_of_edge, epg_report *out);
 
 /* Default task schedule (O3; "default task scheduling" P:75): task e goes to
  * the i-th contiguous chunk of sizes s_i.  part_of_edge [m] DEVICE out. */
@@ -236,6 +246,14 @@ epg_status epg_load_count(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t
  *   edges [m][2] DEVICE (original task order); part_of_edge [m] DEVICE. */
 epg_status epg_remap(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n_vertices,
                      const int32_t *part_of_edge, int64_t k, epg_layout *layout, epg_plan **plan);
+/* epg_remap with the tasks of each partition ordered by (order_key, task id) instead of the
+ * task id (reading Z22: the paper's reorganisation, leaves the order inside a
+ * thread block open). With the growth ranks of epg_partition_ranked / epg_partition_rb,
+ * consecutive tasks of a block share or neighbour their vertices, so the cpack numbering and
+ * the local slots follow the growth and the staged kernel's threads read nearby records.
+ * order_key [m] DEVICE, values in [0, 2^31), or NULL (= epg_remap). */
+epg_status epg_remap_keyed(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n_vertices, const int32_t *part_of_edge,
+                           const int32_t *order_key, int64_t k, epg_layout *layout, epg_plan **plan);
 void epg_plan_destroy(epg_plan *plan);
 /* Sizes of a plan: out[0..7] = m, n, k, touched, cut_cost (= |halo_ids| of the layout),
  * shared vertex count of the execution plan, k_exec, cut cost of the execution plan.
@@ -405,6 +423,14 @@ epg_status epg_set_exec_limits(epg_ctx *ctx, int32_t max_rows, int32_t max_edges
  * degree <= 4 (cfd) never have hubs at the default. -1 restores the default; values
  * below -1 return EPG_ERR_INPUT. */
 epg_status epg_set_hub_split(epg_ctx *ctx, int32_t min_halo_entries);
+/* Hub read side ("for the vertices with large degree ... we use hardware
+ * cache instead", the hub paragraph of P:642-683): with enable != 0 (the default) the edge
+ * kernel of a plan with hubs is launched with a persisting L2 access-policy window over the
+ * prefix of state_in that holds the hubs' rows (cpack numbers vertices by first touch and
+ * hubs are touched by the first partitions, so they sit at the front), so their rows stay
+ * L2-resident while each partition gathers them; it raises the device's persisting-L2 limit
+ * (cudaLimitPersistingL2CacheSize) to its maximum on first use. 0 launches without it. */
+epg_status epg_set_hub_l2(epg_ctx *ctx, int32_t enable);
 /* Hub count of a plan (-1 for NULL); *min_halo_entries (may be NULL) receives the
  * threshold it was built with (0 = off). */
 int64_t epg_plan_hubs(const epg_plan *plan, int32_t *min_halo_entries);

@@ -52,6 +52,7 @@ struct epg_ctx {
     int partition_method = EPG_PARTITION_EPG1;
     int variant = 0;  // 0 auto, 1 one CTA per partition, 2 pipelined TMA, 3 occupancy TMA
     int hub_min = -1; // hub split: shared vertices with >= hub_min halo entries (0 off, -1 default)
+    int hub_l2 = 1;   // hub read side: persisting L2 access-policy window over the hubs' state rows
     int exec_rows = -1, exec_edges = -1;   // execution-split caps for later remaps (-1 default)
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_used;
@@ -116,6 +117,8 @@ struct epg_plan {
     int64_t n_hub = 0;
     int32_t *hub_sid = nullptr;   // [n_hub] shared index of hub i
     float *hub_acc = nullptr;     // [n_hub][5] partial sums, zero between steps
+    int64_t hub_rows = 0;         // 1 + largest hub id: hubs are first touched early, so cpack
+                                  // gives them a prefix of the vertex order (the L2 window)
     int finalise_skip = 8;        // k_finalise3 leaves vertices with more halo entries
     int hub_words = 1;            // blob3 words per halo row (2 with hub indices)
     // the EP map the plan executes (k, C of the paper's partitions; the plan itself may
@@ -248,19 +251,44 @@ epg_status validate(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, co
 }
 
 // stable sort of task ids by partition -> edge_perm (new -> old), part_edge_begin
+// (partition, order key) of task e; order key in [0, 2^31)
+__global__ void k_part_key(const int32_t *__restrict__ part, const int32_t *__restrict__ key, int64_t m,
+                           unsigned long long *out) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e < m) out[e] = ((unsigned long long)(uint32_t)part[e] << 32) | (uint32_t)key[e];
+}
+__global__ void k_key_part(const unsigned long long *__restrict__ in, int64_t m, int32_t *out) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e < m) out[e] = (int32_t)(in[e] >> 32);
+}
+
+// stable sort of task ids by partition (then by `key`, if given: reading Z22) -> edge_perm
+// (new -> old), part_edge_begin
 epg_status group_by_part(epg_ctx *ctx, const int32_t *part, int64_t m, int64_t k, int32_t *edge_perm, int32_t *peb,
-                         std::vector<int32_t> *peb_host) {
-    Tmp iota(ctx), keys_out(ctx), temp(ctx);
+                         std::vector<int32_t> *peb_host, const int32_t *key = nullptr) {
+    Tmp iota(ctx), keys_out(ctx), temp(ctx), k64(ctx), k64o(ctx);
     CU(iota.alloc(sizeof(int32_t) * m));
     CU(keys_out.alloc(sizeof(int32_t) * m));
     k_iota<<<grid_for(m), kThreads, 0, ctx->stream>>>(iota.as<int32_t>(), m);
     size_t tb = 0;
     const int kb = bits_for(k);
-    CU(cub::DeviceRadixSort::SortPairs(nullptr, tb, part, keys_out.as<int32_t>(), iota.as<int32_t>(), edge_perm,
-                                       (int)m, 0, kb, ctx->stream));
-    CU(temp.alloc(tb));
-    CU(cub::DeviceRadixSort::SortPairs(temp.p, tb, part, keys_out.as<int32_t>(), iota.as<int32_t>(), edge_perm,
-                                       (int)m, 0, kb, ctx->stream));
+    if (key) {   // (part, key) composite, stable: ties keep the task id order
+        CU(k64.alloc(sizeof(unsigned long long) * m));
+        CU(k64o.alloc(sizeof(unsigned long long) * m));
+        k_part_key<<<grid_for(m), kThreads, 0, ctx->stream>>>(part, key, m, k64.as<unsigned long long>());
+        CU(cub::DeviceRadixSort::SortPairs(nullptr, tb, k64.as<unsigned long long>(), k64o.as<unsigned long long>(),
+                                           iota.as<int32_t>(), edge_perm, (int)m, 0, 32 + kb, ctx->stream));
+        CU(temp.alloc(tb));
+        CU(cub::DeviceRadixSort::SortPairs(temp.p, tb, k64.as<unsigned long long>(), k64o.as<unsigned long long>(),
+                                           iota.as<int32_t>(), edge_perm, (int)m, 0, 32 + kb, ctx->stream));
+        k_key_part<<<grid_for(m), kThreads, 0, ctx->stream>>>(k64o.as<unsigned long long>(), m, keys_out.as<int32_t>());
+    } else {
+        CU(cub::DeviceRadixSort::SortPairs(nullptr, tb, part, keys_out.as<int32_t>(), iota.as<int32_t>(), edge_perm,
+                                           (int)m, 0, kb, ctx->stream));
+        CU(temp.alloc(tb));
+        CU(cub::DeviceRadixSort::SortPairs(temp.p, tb, part, keys_out.as<int32_t>(), iota.as<int32_t>(), edge_perm,
+                                           (int)m, 0, kb, ctx->stream));
+    }
     k_part_begin<<<grid_for(k + 1), kThreads, 0, ctx->stream>>>(keys_out.as<int32_t>(), m, k, peb);
     CHECK_LAUNCH();
     peb_host->resize(k + 1);
@@ -489,6 +517,9 @@ epg_status build_pipeline_blob(epg_ctx *ctx, epg_plan *pl) {
                 if (pl->n_medium)
                     CU(cudaMemcpy(pl->medium, md.data(), sizeof(int32_t) * pl->n_medium, cudaMemcpyHostToDevice));
                 if (pl->n_hub) {
+                    int32_t last = 0;
+                    CU(cudaMemcpy(&last, pl->shared_ids + hubs.back(), sizeof(int32_t), cudaMemcpyDeviceToHost));
+                    pl->hub_rows = (int64_t)last + 1;
                     CU(cudaMemcpy(pl->hub_sid, hubs.data(), sizeof(int32_t) * pl->n_hub, cudaMemcpyHostToDevice));
                     CU(cudaMemset(pl->hub_acc, 0, sizeof(float) * 5 * pl->n_hub));
                     Tmp hos(ctx);
@@ -712,18 +743,58 @@ int exec_max_rows(const epg_ctx *ctx) {
 // launch with programmatic stream serialization (the kernel calls griddepcontrol.wait
 // before touching what the previous kernel in the stream writes)
 template <class K, class... Args>
-cudaError_t launch_pdl(K kern, unsigned grid, unsigned block, size_t smem, cudaStream_t stream, Args... args) {
+cudaError_t launch_pdl_w(K kern, unsigned grid, unsigned block, size_t smem, cudaStream_t stream,
+                         const cudaAccessPolicyWindow *window, Args... args) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(block);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    if (window) {   // L2 access-policy window of this launch (the hub read side)
+        attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[1].val.accessPolicyWindow = *window;
+        cfg.numAttrs = 2;
+    }
     return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+template <class K, class... Args>
+cudaError_t launch_pdl(K kern, unsigned grid, unsigned block, size_t smem, cudaStream_t stream, Args... args) {
+    return launch_pdl_w(kern, grid, block, smem, stream, nullptr, args...);
+}
+
+// Hub read side ("for the vertices with large degree ... we use
+// hardware cache instead", the hub paragraph of P:642-683): the state rows of a plan's hubs
+// (a prefix of the cpack order) are marked persisting in L2 for the edge kernel's launch, so
+// the many partitions that gather a hub's row hit L2 while the edge records stream through.
+// Sets the device's persisting-L2 carve-out once (cudaLimitPersistingL2CacheSize).
+bool hub_window(epg_ctx *ctx, const epg_plan *pl, const void *state_in, int row_bytes, cudaAccessPolicyWindow *w) {
+    if (!ctx->hub_l2 || pl->n_hub <= 0 || pl->hub_rows <= 0) return false;
+    static int max_window = -1, max_persist = -1;
+    if (max_window < 0) {
+        if (cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device) != cudaSuccess ||
+            cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, ctx->device) != cudaSuccess) {
+            cudaGetLastError();
+            max_window = max_persist = 0;
+        }
+    }
+    if (max_window <= 0 || max_persist <= 0) return false;
+    const size_t bytes = std::min<size_t>((size_t)pl->hub_rows * row_bytes, (size_t)max_window);
+    size_t limit = 0;
+    if (cudaDeviceGetLimit(&limit, cudaLimitPersistingL2CacheSize) == cudaSuccess && limit < (size_t)max_persist)
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist);
+    cudaGetLastError();
+    w->base_ptr = const_cast<void *>(state_in);
+    w->num_bytes = bytes;
+    w->hitRatio = std::min(1.0f, (float)max_persist / (float)std::max<size_t>(bytes, 1));
+    w->hitProp = cudaAccessPropertyPersisting;
+    w->missProp = cudaAccessPropertyStreaming;
+    return true;
 }
 
 template <class Fn>
@@ -751,8 +822,10 @@ epg_status launch_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t step
         a.state_in = bufs[s & 1];
         a.state_out = bufs[(s + 1) & 1];
         a.state_end = a.state_in + (int64_t)Fn::ROW * pl->n;
+        cudaAccessPolicyWindow win{};
+        const bool use_win = hub_window(ctx, pl, a.state_in, 4 * Fn::ROW, &win);
         cudaEvent_t t0 = ctx->prof_begin();
-        CU(launch_pdl(kern, (unsigned)pl->k, kOccThreads, smem, ctx->stream, a));
+        CU(launch_pdl_w(kern, (unsigned)pl->k, kOccThreads, smem, ctx->stream, use_win ? &win : nullptr, a));
         ctx->prof_end(0, t0);
         if (fin_work > 0) {
             cudaEvent_t t1 = ctx->prof_begin();
@@ -1266,7 +1339,7 @@ epg_status rb_bisect(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, i
 // EPG-RB end to end on the device edges: bisection levels (GPU), leaf grouping and leaf-local
 // vertex ids (GPU), EPG-2 per leaf (host threads), scatter of the map (GPU) into part_d.
 epg_status rb_partition(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, int32_t P, int32_t shards,
-                        int32_t leaf_parts, int32_t *part_d, std::string *err) {
+                        int32_t leaf_parts, int32_t *part_d, int32_t *rank_d, std::string *err) {
     const bool trace = std::getenv("EPG_RB_TRACE") != nullptr;
     double t0 = rb_now();
     auto mark = [&](const char *what) {
@@ -1352,7 +1425,8 @@ epg_status rb_partition(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n
     mark("leaf grouping + local ids");
     // the grouped edges stream to the host in leaf order (a copy thread, chunk by chunk)
     // while the leaf workers start on the chunks that have arrived
-    std::unique_ptr<int32_t[]> ge(new int32_t[len]), part_local(new int32_t[m]);
+    std::unique_ptr<int32_t[]> ge(new int32_t[len]), part_local(new int32_t[m]),
+        rank_local(rank_d ? new int32_t[m] : nullptr);
     std::atomic<int32_t> ready{0};
     cudaError_t copy_err = cudaSuccess;
     std::thread copier([&]() {
@@ -1367,7 +1441,7 @@ epg_status rb_partition(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n
             ready.store(copy_err == cudaSuccess ? j1 : leaves, std::memory_order_release);
         }
     });
-    st = epg::rb_leaves(ge.get(), m, nl.data(), leaves, P, part_local.get(), err, 0, &ready);
+    st = epg::rb_leaves(ge.get(), m, nl.data(), leaves, P, part_local.get(), err, 0, &ready, rank_local.get());
     copier.join();
     if (copy_err != cudaSuccess) return ctx->fail(EPG_ERR_CUDA, std::string("partition (RB): ") +
                                                                 cudaGetErrorString(copy_err));
@@ -1377,6 +1451,12 @@ epg_status rb_partition(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n
     CU(cudaMemcpyAsync(pl.p, part_local.get(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx->stream));
     k_rb_scatter<<<grid_for(m), kThreads, 0, ctx->stream>>>(order.as<int32_t>(), pl.as<int32_t>(), m, part_d);
     CHECK_LAUNCH();
+    if (rank_d) {   // growth ranks, same grouped order
+        CU(cudaStreamSynchronize(ctx->stream));
+        CU(cudaMemcpyAsync(pl.p, rank_local.get(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx->stream));
+        k_rb_scatter<<<grid_for(m), kThreads, 0, ctx->stream>>>(order.as<int32_t>(), pl.as<int32_t>(), m, rank_d);
+        CHECK_LAUNCH();
+    }
     CU(cudaStreamSynchronize(ctx->stream));   // part_local is a host vector
     mark("scatter");
     return EPG_OK;
@@ -1437,7 +1517,8 @@ namespace {
 // epg_partition / epg_partition_rb: host partitioner (or, for EPG-RB, GPU bisection levels +
 // host leaves), then the GPU cost function on the map
 epg_status partition_impl(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, int32_t part_size, int32_t shards,
-                          int32_t method, int32_t leaf_parts, int32_t *part_of_edge, epg_report *out) {
+                          int32_t method, int32_t leaf_parts, int32_t *part_of_edge, int32_t *rank_of_edge,
+                          epg_report *out) {
     if (!edges || !part_of_edge || !out || m <= 0 || n <= 0)
         return ctx->fail(EPG_ERR_INPUT, "partition: need m > 0, n > 0 and non-NULL arrays");
     if (m >= kMaxEdges) return ctx->fail(EPG_ERR_INPUT, "partition: m must be below 2^30");
@@ -1455,6 +1536,13 @@ epg_status partition_impl(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t
         CU(pd.alloc(sizeof(int32_t) * m));
         part_d = pd.as<int32_t>();
     }
+    const bool rank_dev = rank_of_edge && is_device_ptr(rank_of_edge);
+    Tmp rd(ctx);
+    int32_t *rank_d = rank_of_edge;
+    if (rank_of_edge && !rank_dev) {
+        CU(rd.alloc(sizeof(int32_t) * m));
+        rank_d = rd.as<int32_t>();
+    }
     std::string err;
     epg_status st;
     if (method == EPG_PARTITION_RB) {
@@ -1465,12 +1553,12 @@ epg_status partition_impl(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t
         const int64_t k = epg_num_parts(m, part_size);
         if (!(shards == 1 || shards == 2 || shards == 4 || shards == 8) || shards > k)
             return ctx->fail(EPG_ERR_INFEASIBLE, "partition: shards must be 1, 2, 4 or 8 and at most k");
-        if ((st = rb_partition(ctx, edges_d, m, n, part_size, shards, leaf_parts, part_d, &err)))
+        if ((st = rb_partition(ctx, edges_d, m, n, part_size, shards, leaf_parts, part_d, rank_d, &err)))
             return err.empty() ? st : ctx->fail(st, err);
-        if (!part_dev) {
-            CU(cudaMemcpyAsync(part_of_edge, part_d, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, ctx->stream));
-            CU(cudaStreamSynchronize(ctx->stream));
-        }
+        if (!part_dev) CU(cudaMemcpyAsync(part_of_edge, part_d, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, ctx->stream));
+        if (rank_of_edge && !rank_dev)
+            CU(cudaMemcpyAsync(rank_of_edge, rank_d, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
     } else {
         std::vector<int32_t> eh, ph(m);
         const int32_t *edges_h = edges;
@@ -1480,11 +1568,19 @@ epg_status partition_impl(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t
             CU(cudaStreamSynchronize(ctx->stream));
             edges_h = eh.data();
         }
-        st = epg::host_partition(edges_h, m, n, part_size, shards, ph.data(), &err, nullptr, method);
+        std::vector<int32_t> rh(rank_of_edge ? m : 0);
+        st = epg::host_partition(edges_h, m, n, part_size, shards, ph.data(), &err, nullptr, method,
+                                 rank_of_edge ? rh.data() : nullptr);
         if (st) return ctx->fail(st, err);
         if (!part_dev) std::memcpy(part_of_edge, ph.data(), sizeof(int32_t) * m);
         CU(cudaMemcpyAsync(part_d, ph.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx->stream));
-        CU(cudaStreamSynchronize(ctx->stream));   // ph is a host vector
+        if (rank_of_edge) {
+            if (rank_dev)
+                CU(cudaMemcpyAsync(rank_of_edge, rh.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx->stream));
+            else
+                std::memcpy(rank_of_edge, rh.data(), sizeof(int32_t) * m);
+        }
+        CU(cudaStreamSynchronize(ctx->stream));   // ph / rh are host vectors
     }
     return load_count_dev(ctx, edges_d, m, n, part_d, epg_num_parts(m, part_size), nullptr, out);
 }
@@ -1501,13 +1597,22 @@ epg_status epg_partition(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t 
                          int32_t shards, int32_t *part_of_edge, epg_report *out) {
     if (!ctx) return EPG_ERR_STATE;
     return partition_impl(ctx, edges, m, n, part_size, shards, ctx->partition_method, rb_leaf_parts_default(),
-                          part_of_edge, out);
+                          part_of_edge, nullptr, out);
+}
+
+epg_status epg_partition_ranked(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, int32_t part_size,
+                                int32_t shards, int32_t *part_of_edge, int32_t *rank_of_edge, epg_report *out) {
+    if (!ctx) return EPG_ERR_STATE;
+    return partition_impl(ctx, edges, m, n, part_size, shards, ctx->partition_method, rb_leaf_parts_default(),
+                          part_of_edge, rank_of_edge, out);
 }
 
 epg_status epg_partition_rb(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, int32_t part_size,
-                            int32_t shards, int32_t leaf_parts, int32_t *part_of_edge, epg_report *out) {
+                            int32_t shards, int32_t leaf_parts, int32_t *part_of_edge, int32_t *rank_of_edge,
+                            epg_report *out) {
     if (!ctx) return EPG_ERR_STATE;
-    return partition_impl(ctx, edges, m, n, part_size, shards, EPG_PARTITION_RB, leaf_parts, part_of_edge, out);
+    return partition_impl(ctx, edges, m, n, part_size, shards, EPG_PARTITION_RB, leaf_parts, part_of_edge,
+                          rank_of_edge, out);
 }
 
 epg_status epg_default_partition(epg_ctx *ctx, int64_t m, int32_t part_size, int32_t *part_of_edge) {
@@ -1535,7 +1640,7 @@ epg_status epg_load_count(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t
 namespace {
 // Remap of one partition map (O6) + the execution plan built on it.
 epg_status remap_impl(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, const int32_t *part, int64_t k,
-                      epg_layout *L, epg_plan **plan_out) {
+                      epg_layout *L, epg_plan **plan_out, const int32_t *order_key = nullptr) {
     if (!edges || !part || !L || !plan_out || m <= 0 || n <= 0 || k <= 0)
         return ctx->fail(EPG_ERR_INPUT, "remap: need m > 0, n > 0, k > 0 and non-NULL arrays");
     if (m >= kMaxEdges)   // first-touch keys 2e' + s and the scan / sort sizes are int32
@@ -1549,7 +1654,7 @@ epg_status remap_impl(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, 
     if (st) return st;
     // 1. task reorganisation: stable sort by partition
     std::vector<int32_t> peb_h;
-    if ((st = group_by_part(ctx, part, m, k, L->edge_perm, L->part_edge_begin, &peb_h))) return st;
+    if ((st = group_by_part(ctx, part, m, k, L->edge_perm, L->part_edge_begin, &peb_h, order_key))) return st;
     int64_t smax = 0;
     for (int64_t p = 0; p < k; p++) smax = std::max<int64_t>(smax, peb_h[p + 1] - peb_h[p]);
     if (smax > EPG_MAX_PART_SIZE)
@@ -1700,11 +1805,16 @@ extern "C" {
 // execution plan shares the public edge_perm / vertex_perm exactly.
 epg_status epg_remap(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, const int32_t *part, int64_t k,
                      epg_layout *L, epg_plan **plan_out) {
+    return epg_remap_keyed(ctx, edges, m, n, part, nullptr, k, L, plan_out);
+}
+
+epg_status epg_remap_keyed(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, const int32_t *part,
+                           const int32_t *order_key, int64_t k, epg_layout *L, epg_plan **plan_out) {
     if (!ctx) return EPG_ERR_STATE;
     if (!plan_out) return ctx->fail(EPG_ERR_INPUT, "remap: plan output is NULL");
     *plan_out = nullptr;
     epg_plan *ep = nullptr;
-    epg_status st = remap_impl(ctx, edges, m, n, part, k, L, &ep);
+    epg_status st = remap_impl(ctx, edges, m, n, part, k, L, &ep, order_key);
     if (st) return st;
     const int kExecMaxEdges = exec_max_edges(ctx), kExecMaxRows = exec_max_rows(ctx);
     std::vector<int32_t> cuts(k, 1);
@@ -1741,7 +1851,9 @@ epg_status epg_remap(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n, c
         epg_layout X{t_ep.as<int32_t>(), peb_x.as<int32_t>(), t_vp.as<int32_t>(), pvb_x.as<int32_t>(),
                      hb_x.as<int32_t>(), t_hid.as<int32_t>(), 2 * m, t_sl.as<uint16_t>()};
         epg_plan *xp = nullptr;
-        if ((st = remap_impl(ctx, edges, m, n, pe.as<int32_t>(), kx, &X, &xp))) return fail_ep(st);
+        // the pieces are contiguous ranges of the (partition, key, id) order, so sorting by
+        // (piece, key, id) reproduces that order: same first touches, same vertex_perm
+        if ((st = remap_impl(ctx, edges, m, n, pe.as<int32_t>(), kx, &X, &xp, order_key))) return fail_ep(st);
         bool again = false;
         for (int64_t p = 0, e = 0; p < k; p++)
             for (int c = 0; c < cuts[p]; c++, e++)
@@ -2074,6 +2186,12 @@ epg_status epg_set_exec_limits(epg_ctx *ctx, int32_t max_rows, int32_t max_edges
         return ctx->fail(EPG_ERR_INPUT, "set_exec_limits: max_rows in [64, 2048], max_edges in [32, 1280], or -1");
     ctx->exec_rows = max_rows;
     ctx->exec_edges = max_edges;
+    return EPG_OK;
+}
+
+epg_status epg_set_hub_l2(epg_ctx *ctx, int32_t enable) {
+    if (!ctx) return EPG_ERR_STATE;
+    ctx->hub_l2 = enable != 0;
     return EPG_OK;
 }
 

@@ -12,9 +12,10 @@ namespace epg {
 
 // Host EPG-1 / EPG-2 (partition.cpp; method EPG_PARTITION_*). A non-zero *cancel (polled
 // once per partition) stops it with EPG_ERR_STATE ("partition: cancelled").
+// rank (may be NULL): each task's growth step within its partition (reading Z22).
 epg_status host_partition(const int32_t *edges, int64_t m, int32_t n, int32_t part_size, int32_t shards,
                           int32_t *part, std::string *err, const std::atomic<int> *cancel = nullptr,
-                          int32_t method = EPG_PARTITION_EPG1);
+                          int32_t method = EPG_PARTITION_EPG1, int32_t *rank = nullptr);
 
 // EPG-RB leaves (O5'', reading Z21): EPG-2 (hub = 4 x part_size) on every leaf's tasks.
 // local_edges [m][2] HOST: the tasks grouped by leaf (leaf j holds the tasks of its
@@ -26,7 +27,7 @@ epg_status host_partition(const int32_t *edges, int64_t m, int32_t n, int32_t pa
 // *ready > j (the caller streams local_edges in leaf order).
 epg_status rb_leaves(const int32_t *local_edges, int64_t m, const int32_t *n_local, int32_t leaves,
                      int32_t part_size, int32_t *part_local, std::string *err, int threads = 0,
-                     const std::atomic<int32_t> *ready = nullptr);
+                     const std::atomic<int32_t> *ready = nullptr, int32_t *rank_local = nullptr);
 // number of CPUs this process may run on (affinity mask)
 int host_cpus();
 

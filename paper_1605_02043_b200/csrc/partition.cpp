@@ -115,7 +115,9 @@ struct Frontier {
 };
 
 // returns false if *cancel became non-zero (checked once per partition)
-bool grow(const TaskGraph &T, const int64_t *sizes, int64_t nparts, int32_t *part, const std::atomic<int> *cancel) {
+// rank (may be NULL): the step at which each task joined its partition (reading Z22)
+bool grow(const TaskGraph &T, const int64_t *sizes, int64_t nparts, int32_t *part, const std::atomic<int> *cancel,
+          int32_t *rank = nullptr) {
     const int64_t ntask = T.ntask;
     std::vector<TaskState> st(ntask, TaskState{-1, kNoStamp, kNoStamp, 0});
     std::vector<int32_t> by_gst;
@@ -150,6 +152,7 @@ bool grow(const TaskGraph &T, const int64_t *sizes, int64_t nparts, int32_t *par
             }
             st[t].part = static_cast<int32_t>(i);
             part[t] = static_cast<int32_t>(i);
+            if (rank) rank[t] = static_cast<int32_t>(r);
             const int32_t *nb = &T.nb[4 * static_cast<int64_t>(t)];
             for (int c = 0; c < 4 && nb[c] >= 0; c++) __builtin_prefetch(&st[nb[c]]);
             for (int c = 0; c < 4 && nb[c] >= 0; c++) {
@@ -199,7 +202,7 @@ Incidence build_incidence(const int32_t *edges, int64_t m, int32_t n) {
 // A vertex with more than `hub` incident tasks (4 x part_size: it is cut into many clusters
 // whatever happens) attracts no tasks -- the hub discussion of P:642-683, reading Z20.
 bool grow_direct(const int32_t *edges, int64_t ntask, int32_t n, const int64_t *sizes, int64_t nparts, int64_t hub,
-                 int32_t *part, const std::atomic<int> *cancel) {
+                 int32_t *part, const std::atomic<int> *cancel, int32_t *rank = nullptr) {
     Incidence I = build_incidence(edges, ntask, n);
     std::vector<int64_t> live_end(I.beg.begin() + 1, I.beg.end());   // end of v's live (unassigned) tasks
     std::vector<TaskState> st(ntask, TaskState{-1, kNoStamp, kNoStamp, 0});
@@ -236,6 +239,7 @@ bool grow_direct(const int32_t *edges, int64_t ntask, int32_t n, const int64_t *
             }
             st[t].part = static_cast<int32_t>(i);
             part[t] = static_cast<int32_t>(i);
+            if (rank) rank[t] = static_cast<int32_t>(r);
             const int32_t ends[2] = {edges[2 * static_cast<int64_t>(t)], edges[2 * static_cast<int64_t>(t) + 1]};
             for (int side = 0; side < 2; side++) {
                 const int32_t v = ends[side];
@@ -277,7 +281,7 @@ int host_cpus() {
 
 epg_status rb_leaves(const int32_t *local_edges, int64_t m, const int32_t *n_local, int32_t leaves,
                      int32_t part_size, int32_t *part_local, std::string *err, int threads,
-                     const std::atomic<int32_t> *ready) {
+                     const std::atomic<int32_t> *ready, int32_t *rank_local) {
     const int64_t k = (m + part_size - 1) / part_size;
     std::vector<int64_t> s(k), S(k + 1, 0);
     for (int64_t i = 0; i < k; i++) {
@@ -295,7 +299,8 @@ epg_status rb_leaves(const int32_t *local_edges, int64_t m, const int32_t *n_loc
             if (nt == 0) continue;
             if (ready)   // the leaf's edges are still being copied in
                 while (ready->load(std::memory_order_acquire) <= j) std::this_thread::yield();
-            grow_direct(local_edges + 2 * b, nt, n_local[j], s.data() + p0, p1 - p0, hub, part_local + b, nullptr);
+            grow_direct(local_edges + 2 * b, nt, n_local[j], s.data() + p0, p1 - p0, hub, part_local + b, nullptr,
+                        rank_local ? rank_local + b : nullptr);
             for (int64_t q = 0; q < nt; q++) part_local[b + q] += static_cast<int32_t>(p0);
         }
     };
@@ -309,7 +314,8 @@ epg_status rb_leaves(const int32_t *local_edges, int64_t m, const int32_t *n_loc
 }
 
 epg_status host_partition(const int32_t *edges, int64_t m, int32_t n, int32_t part_size, int32_t shards,
-                          int32_t *part, std::string *err, const std::atomic<int> *cancel, int32_t method) {
+                          int32_t *part, std::string *err, const std::atomic<int> *cancel, int32_t method,
+                          int32_t *rank) {
     if (method == EPG_PARTITION_RB) {
         *err = "partition: EPG-RB bisects on the GPU -- use epg_partition / epg_partition_rb";
         return EPG_ERR_INPUT;
@@ -350,7 +356,7 @@ epg_status host_partition(const int32_t *edges, int64_t m, int32_t n, int32_t pa
     };
     if (method == EPG_PARTITION_EPG2) {
         const int64_t hub = 4 * static_cast<int64_t>(part_size);
-        if (shards == 1) return grow_direct(edges, m, n, s.data(), k, hub, part, cancel) ? EPG_OK : cancelled();
+        if (shards == 1) return grow_direct(edges, m, n, s.data(), k, hub, part, cancel, rank) ? EPG_OK : cancelled();
         // hierarchical: shard-level growing, then growing on each shard's own edge list
         std::vector<int64_t> ssize(shards, 0);
         for (int g = 0; g < shards; g++)
@@ -366,16 +372,19 @@ epg_status host_partition(const int32_t *edges, int64_t m, int32_t n, int32_t pa
                     sub_edges.push_back(edges[2 * t + 1]);
                 }
             const int64_t p0 = g * k / shards, p1 = (g + 1) * k / shards;
-            std::vector<int32_t> sub(mem.size());
+            std::vector<int32_t> sub(mem.size()), subr(mem.size());
             if (!grow_direct(sub_edges.data(), static_cast<int64_t>(mem.size()), n, s.data() + p0, p1 - p0, hub,
-                             sub.data(), cancel))
+                             sub.data(), cancel, subr.data()))
                 return cancelled();
-            for (size_t j = 0; j < mem.size(); j++) part[mem[j]] = static_cast<int32_t>(sub[j] + p0);
+            for (size_t j = 0; j < mem.size(); j++) {
+                part[mem[j]] = static_cast<int32_t>(sub[j] + p0);
+                if (rank) rank[mem[j]] = subr[j];
+            }
         }
         return EPG_OK;
     }
     TaskGraph T = build_task_graph(edges, m, n);
-    if (shards == 1) return grow(T, s.data(), k, part, cancel) ? EPG_OK : cancelled();
+    if (shards == 1) return grow(T, s.data(), k, part, cancel, rank) ? EPG_OK : cancelled();
     // hierarchical: shard-level growing, then growing inside each shard
     std::vector<int64_t> ssize(shards, 0);
     for (int g = 0; g < shards; g++)
@@ -403,9 +412,12 @@ epg_status host_partition(const int32_t *edges, int64_t m, int32_t n, int32_t pa
             }
         }
         const int64_t p0 = g * k / shards, p1 = (g + 1) * k / shards;
-        std::vector<int32_t> sub(mem.size());
-        if (!grow(Tg, s.data() + p0, p1 - p0, sub.data(), cancel)) return cancelled();
-        for (size_t j = 0; j < mem.size(); j++) part[mem[j]] = static_cast<int32_t>(sub[j] + p0);
+        std::vector<int32_t> sub(mem.size()), subr(mem.size());
+        if (!grow(Tg, s.data() + p0, p1 - p0, sub.data(), cancel, subr.data())) return cancelled();
+        for (size_t j = 0; j < mem.size(); j++) {
+            part[mem[j]] = static_cast<int32_t>(sub[j] + p0);
+            if (rank) rank[mem[j]] = subr[j];
+        }
     }
     return EPG_OK;
 }
@@ -421,8 +433,16 @@ extern "C" epg_status epg_partition_host(const int32_t *edges, int64_t m, int32_
 extern "C" epg_status epg_partition_host_method(const int32_t *edges, int64_t m, int32_t n_vertices, int32_t part_size,
                                                 int32_t shards, int32_t method, int32_t *part_of_edge, char *errbuf,
                                                 int64_t errbuf_len) {
+    return epg_partition_host_ranked(edges, m, n_vertices, part_size, shards, method, part_of_edge, nullptr, errbuf,
+                                     errbuf_len);
+}
+
+extern "C" epg_status epg_partition_host_ranked(const int32_t *edges, int64_t m, int32_t n_vertices, int32_t part_size,
+                                                int32_t shards, int32_t method, int32_t *part_of_edge,
+                                                int32_t *rank_of_edge, char *errbuf, int64_t errbuf_len) {
     std::string err;
-    epg_status st = epg::host_partition(edges, m, n_vertices, part_size, shards, part_of_edge, &err, nullptr, method);
+    epg_status st = epg::host_partition(edges, m, n_vertices, part_size, shards, part_of_edge, &err, nullptr, method,
+                                        rank_of_edge);
     if (st != EPG_OK && errbuf && errbuf_len > 0) {
         std::strncpy(errbuf, err.c_str(), static_cast<size_t>(errbuf_len - 1));
         errbuf[errbuf_len - 1] = '\0';

@@ -35,7 +35,8 @@ SYMBOLS = ["epg_create", "epg_destroy", "epg_last_error", "epg_num_parts", "epg_
            "epg_adaptive_create", "epg_adaptive_step", "epg_adaptive_wait", "epg_adaptive_read_state",
            "epg_adaptive_info", "epg_adaptive_destroy", "epg_partition_host_method", "epg_set_partition_method",
            "epg_run_host", "epg_run_host_join", "epg_partition_rb", "epg_comm_unique_id", "epg_comm_init",
-           "epg_comm_init_local", "epg_run_sharded", "epg_run_sharded_group"]
+           "epg_comm_init_local", "epg_run_sharded", "epg_run_sharded_group", "epg_set_hub_l2", "epg_remap_keyed",
+           "epg_partition_ranked", "epg_partition_host_ranked"]
 
 
 class _Report(C.Structure):
@@ -73,7 +74,10 @@ def _load():
         "epg_partition_host_method": (st, [P, i64, i32, i32, i32, i32, P, C.c_char_p, i64]),
         "epg_set_partition_method": (st, [P, i32]),
         "epg_partition": (st, [P, P, i64, i32, i32, i32, P, C.POINTER(_Report)]),
-        "epg_partition_rb": (st, [P, P, i64, i32, i32, i32, i32, P, C.POINTER(_Report)]),
+        "epg_partition_rb": (st, [P, P, i64, i32, i32, i32, i32, P, P, C.POINTER(_Report)]),
+        "epg_partition_ranked": (st, [P, P, i64, i32, i32, i32, P, P, C.POINTER(_Report)]),
+        "epg_partition_host_ranked": (st, [P, i64, i32, i32, i32, i32, P, P, C.c_char_p, i64]),
+        "epg_remap_keyed": (st, [P, P, i64, i32, P, P, i64, C.POINTER(_Layout), C.POINTER(P)]),
         "epg_default_partition": (st, [P, i64, i32, P]),
         "epg_load_count": (st, [P, P, i64, i32, P, i64, P, C.POINTER(_Report)]),
         "epg_remap": (st, [P, P, i64, i32, P, i64, C.POINTER(_Layout), C.POINTER(P)]),
@@ -86,6 +90,7 @@ def _load():
         "epg_run_naive": (st, [P, C.c_int, P, i64, i32, C.POINTER(_State), i32]),
         "epg_set_variant": (st, [P, i32]),
         "epg_set_hub_split": (st, [P, i32]),
+        "epg_set_hub_l2": (st, [P, i32]),
         "epg_set_exec_limits": (st, [P, i32, i32]),
         "epg_partition_random_host": (st, [i64, i32, C.c_uint64, P, C.c_char_p, i64]),
         "epg_partition_greedy_host": (st, [P, i64, i32, i32, P, C.c_char_p, i64]),
@@ -194,6 +199,20 @@ def partition_host(edges, n: int, part_size: int, shards: int = 1, method: int =
     if s != OK:
         raise EpgError(s, buf.value.decode())
     return part[:m]
+
+
+def partition_host_ranked(edges, n: int, part_size: int, shards: int = 1, method: int = PARTITION_EPG1):
+    """epg_partition_host_ranked -> (part, rank) (HOST numpy)."""
+    e = np.ascontiguousarray(edges.cpu().numpy() if isinstance(edges, torch.Tensor) else edges, dtype=np.int32)
+    m = e.shape[0]
+    part = np.zeros(max(m, 1), np.int32)
+    rank = np.zeros(max(m, 1), np.int32)
+    buf = C.create_string_buffer(512)
+    s = lib.epg_partition_host_ranked(e.ctypes.data if m else None, m, n, part_size, shards, method,
+                                      part.ctypes.data, rank.ctypes.data, buf, 512)
+    if s != OK:
+        raise EpgError(s, buf.value.decode())
+    return part[:m], rank[:m]
 
 
 def partition_random_host(m: int, part_size: int, seed: int = 1605) -> np.ndarray:
@@ -369,16 +388,28 @@ class Context:
         self._check(lib.epg_partition(self.handle, _ptr(edges), m, n, part_size, shards, _ptr(out), C.byref(r)))
         return out, _rep(r)
 
-    def partition_rb(self, edges: torch.Tensor, n: int, part_size: int, shards: int = 1, leaf_parts: int = 256,
-                     out: torch.Tensor | None = None):
-        """EPG-RB (epg_partition_rb): GPU bisection levels + EPG-2 leaves on the host cores."""
+    def partition_rb(self, edges: torch.Tensor, n: int, part_size: int, shards: int = 1, leaf_parts: int = 512,
+                     out: torch.Tensor | None = None, ranked: bool = False):
+        """EPG-RB (epg_partition_rb): GPU bisection levels + EPG-2 leaves on the host cores.
+        -> (part, report), or (part, rank, report) with ranked=True (growth steps, reading Z22)."""
         m = edges.shape[0]
         if out is None:
             out = torch.empty(m, dtype=torch.int32, device=edges.device)
+        rank = torch.empty(m, dtype=torch.int32, device=edges.device) if ranked else None
         r = _Report()
         self._check(lib.epg_partition_rb(self.handle, _ptr(edges), m, n, part_size, shards, leaf_parts, _ptr(out),
-                                         C.byref(r)))
-        return out, _rep(r)
+                                         _ptr(rank), C.byref(r)))
+        return (out, rank, _rep(r)) if ranked else (out, _rep(r))
+
+    def partition_ranked(self, edges: torch.Tensor, n: int, part_size: int, shards: int = 1):
+        """epg_partition_ranked (ctx's method) -> (part, rank, report)."""
+        m = edges.shape[0]
+        out = torch.empty(m, dtype=torch.int32, device=edges.device)
+        rank = torch.empty(m, dtype=torch.int32, device=edges.device)
+        r = _Report()
+        self._check(lib.epg_partition_ranked(self.handle, _ptr(edges), m, n, part_size, shards, _ptr(out), _ptr(rank),
+                                             C.byref(r)))
+        return out, rank, _rep(r)
 
     def default_partition(self, m: int, part_size: int) -> torch.Tensor:
         out = torch.empty(m, dtype=torch.int32, device=self.device)
@@ -392,7 +423,8 @@ class Context:
         return (_rep(r), pp) if per_part else _rep(r)
 
     # -- remap ---------------------------------------------------------------------
-    def remap(self, edges: torch.Tensor, n: int, part: torch.Tensor, k: int, halo_cap: int | None = None):
+    def remap(self, edges: torch.Tensor, n: int, part: torch.Tensor, k: int, halo_cap: int | None = None,
+              order_key: torch.Tensor | None = None):
         m = edges.shape[0]
         if halo_cap is None:
             halo_cap = self.load_count(edges, n, part, k).cut_cost
@@ -405,7 +437,8 @@ class Context:
         cl = _Layout(_ptr(L.edge_perm), _ptr(L.part_edge_begin), _ptr(L.vertex_perm), _ptr(L.part_vertex_begin),
                      _ptr(L.halo_begin), _ptr(L.halo_ids), halo_cap, _ptr(L.slots))
         h = C.c_void_p()
-        self._check(lib.epg_remap(self.handle, _ptr(edges), m, n, _ptr(part), k, C.byref(cl), C.byref(h)))
+        self._check(lib.epg_remap_keyed(self.handle, _ptr(edges), m, n, _ptr(part), _ptr(order_key), k, C.byref(cl),
+                                        C.byref(h)))
         plan = Plan(h, self)
         L.halo_ids = L.halo_ids[: plan.cut_cost]
         return L, plan
@@ -505,6 +538,10 @@ class Context:
     def set_hub_split(self, min_halo_entries: int):
         """Hub split for plans remapped after this call (0 off; default 7, see include/epg.h)."""
         self._check(lib.epg_set_hub_split(self.handle, min_halo_entries))
+
+    def set_hub_l2(self, enable: bool):
+        """Persisting L2 window over the hubs' rows for the edge kernel (default on)."""
+        self._check(lib.epg_set_hub_l2(self.handle, 1 if enable else 0))
 
     def set_profiling(self, enable: bool):
         self._check(lib.epg_set_profiling(self.handle, 1 if enable else 0))

@@ -16,7 +16,7 @@ from conftest import ROOT, golden
 def _declared_symbols():
     with open(os.path.join(ROOT, "include", "epg.h")) as f:
         src = re.sub(r"/\*.*?\*/", "", f.read(), flags=re.S)
-    return sorted(set(re.findall(r"\b(epg_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(epg_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_library_exports_every_declared_symbol():
@@ -179,3 +179,24 @@ def test_host_partition_method_errors():
     with pytest.raises(epg.EpgError) as ex:
         epg.partition_host(np.array([[0, 1]], np.int32), 2, 1, method=3)
     assert ex.value.status == epg.ERR_INPUT
+
+
+@pytest.mark.parametrize("method", [1, 2])
+def test_host_ranked_matches_oracle(method, mesh_c1):
+    """epg_partition_host_ranked: the growth step of every task (reading Z22) equals the
+    oracle's, flat and hierarchical, on random multigraphs and the C1 mesh."""
+    from paper_1605_02043_b200 import epg
+    for seed in range(8):
+        rng = np.random.default_rng(4400 + seed)
+        m, n0 = int(rng.integers(5, 400)), int(rng.integers(3, 120))
+        n, e = S.random_multigraph(4500 + seed, m, n0)
+        P = int(rng.integers(2, 40))
+        for shards in (1, 2):
+            if shards > O.num_parts(m, P):
+                continue
+            part, rank = epg.partition_host_ranked(e, n, P, shards, method)
+            rp, rr = O.partition(e, n, P, shards, method=method, ranked=True)
+            assert np.array_equal(part, rp) and np.array_equal(rank, rr)
+    part, rank = epg.partition_host_ranked(mesh_c1.edges, mesh_c1.n, 1024, 1, method)
+    rp, rr = O.partition(mesh_c1.edges, mesh_c1.n, 1024, method=method, ranked=True)
+    assert np.array_equal(part, rp) and np.array_equal(rank, rr)

@@ -95,9 +95,9 @@ def test_partition_host_and_device_edges(ctx, mesh_c1):
 
 
 # ---------------------------------------------------------------------------- remap (a4)
-def _check_remap(ctx, edges, n, part, k):
-    L, plan = ctx.remap(dev(edges), n, dev(part), k)
-    ref = O.remap(edges, n, part, k)
+def _check_remap(ctx, edges, n, part, k, key=None):
+    L, plan = ctx.remap(dev(edges), n, dev(part), k, order_key=None if key is None else dev(key))
+    ref = O.remap(edges, n, part, k, key)
     for name in ("edge_perm", "part_edge_begin", "vertex_perm", "part_vertex_begin", "halo_begin", "halo_ids"):
         got = getattr(L, name).cpu().numpy()
         assert np.array_equal(got, getattr(ref, name)), name
@@ -134,6 +134,40 @@ def test_remap_mesh(ctx, mesh_c1, P):
     k = O.num_parts(M.m, P)
     _check_remap(ctx, M.edges, M.n, O.partition(M.edges, M.n, P), k)
     _check_remap(ctx, M.edges, M.n, O.default_partition(M.m, P), k)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_remap_keyed_random(ctx, seed):
+    """epg_remap_keyed (reading Z22): arbitrary keys with ties, bit-exact vs orc_remap_keyed."""
+    rng = np.random.default_rng(3100 + seed)
+    m, n = int(rng.integers(1, 6000)), int(rng.integers(1, 3000))
+    n, e = S.random_multigraph(40 + seed, m, n)
+    P = int(rng.choice([7, 256, 1000, 4096]))
+    k = O.num_parts(m, P)
+    part = O.default_partition(m, P) if seed % 2 else O.partition(e, n, P)
+    key = rng.integers(0, 50, m).astype(np.int32)
+    _check_remap(ctx, e, n, part, k, key)
+
+
+@pytest.mark.parametrize("P", [256, 1024, 4096])
+def test_remap_growth_order_mesh(ctx, mesh_c1, P):
+    """The growth-ranked layout of the EPG-2 map (what the bench runs), bit-exact; P = 4096
+    also exercises the execution split (pieces of a growth-ordered partition)."""
+    M = mesh_c1
+    k = O.num_parts(M.m, P)
+    part, rank = O.partition(M.edges, M.n, P, method=2, ranked=True)
+    _check_remap(ctx, M.edges, M.n, part, k, rank)
+    U, dt = _cfd_inputs(M)
+    from paper_1605_02043_b200 import epg
+    L, plan = ctx.remap(dev(M.edges), M.n, dev(part), k, order_key=dev(rank))
+    Un = ctx.permute_rows(dev(U), L.vertex_perm, epg.PERM_SCATTER)
+    nrm = ctx.permute_rows(dev(M.normals), L.edge_perm, epg.PERM_GATHER)
+    dtn = ctx.permute_rows(dev(dt), L.vertex_perm, epg.PERM_SCATTER)
+    out = torch.empty_like(Un)
+    ctx.run(plan, epg.KERNEL_CFD_FLUX, Un, out, nrm, dtn, 1)
+    got = ctx.permute_rows(out, L.vertex_perm, epg.PERM_GATHER).cpu().numpy()
+    ref, _ = O.cfd_step(M.edges, M.n, M.normals, U, dt)
+    assert normwise_err(got, ref).max() <= TOL
 
 
 def test_remap_rejects_oversized_partition(ctx):

@@ -21,9 +21,10 @@ def _check(ctx, e, n, P, shards, lp, host_edges=False):
     k = O.num_parts(len(e), P)
     edges = torch.from_numpy(np.ascontiguousarray(e)) if host_edges else dev(e)
     out = torch.empty(len(e), dtype=torch.int32, device=edges.device)
-    part, rep = ctx.partition_rb(edges, n, P, shards, lp, out=out)
-    ref = O.partition_rb(e, n, P, shards, lp)
+    part, rank, rep = ctx.partition_rb(edges, n, P, shards, lp, out=out, ranked=True)
+    ref, ref_rank = O.partition_rb(e, n, P, shards, lp, ranked=True)
     assert np.array_equal(part.cpu().numpy(), ref)
+    assert np.array_equal(rank.cpu().numpy(), ref_rank)          # growth steps (reading Z22)
     r = O.cost(e, n, ref, k)
     assert (rep.load_count, rep.cut_cost, rep.touched, rep.max_size, rep.min_size) == \
         (r.load_count, r.cut_cost, r.touched, r.max_size, r.min_size)

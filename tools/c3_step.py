@@ -19,8 +19,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--comparators", action="store_true")
     ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--order", choices=["growth", "id"], default="growth")
     a = ap.parse_args()
-    args = argparse.Namespace(part_size=1024, c3_steps=a.steps, no_comparators=not a.comparators)
+    args = argparse.Namespace(part_size=1024, c3_steps=a.steps, no_comparators=not a.comparators, order=a.order)
     stream = torch.cuda.current_stream()
     ctx = epg.Context(0, stream)
     peak, _ = bench.measured_peaks()

@@ -53,8 +53,9 @@ def main():
         sys.path.insert(0, ROOT)
         import synth
         m = synth.config_mesh(a.config).m
-    # 1. launch list
-    rows = read_ncu_csv(os.path.join(g, f"launches_{a.config}.csv"))
+    # 1. launch list (optional: the bench's launch list is only taken for the headline config)
+    lpath = os.path.join(g, f"launches_{a.config}.csv")
+    rows = read_ncu_csv(lpath) if os.path.exists(lpath) else []
     per = {}
     for r in rows:
         if r.get("Metric Name") != "gpu__time_duration.sum":
@@ -66,7 +67,9 @@ def main():
     tot = sum(sum(v) for v in per.values())
     step = {k: v for k, v in per.items() if k.split("<")[0] in ("k_edge_occ", "k_finalise_rec", "k_finalise3")}
     step_tot = sum(statistics.median(v) for v in step.values()) or 1.0
-    with open(pre + "_launches.csv", "w", newline="") as f:
+    if not per:
+        per = {}
+    with open(pre + "_launches.csv", "w", newline="") if rows else open(os.devnull, "w") as f:
         w = csv.writer(f)
         w.writerow(["kernel", "launches", "mean_us", "median_us", "total_us", "share_of_all", "share_of_step"])
         for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
@@ -110,8 +113,9 @@ def main():
         d.update({"dram_bytes": dram, "dram_bytes_per_edge": dram / m, "l2_sm_bytes": l2,
                   "l2_sm_bytes_per_edge": l2 / m, "time_us_cold": t / 1000.0})
         out["schedules"][name] = d
-    if "ep" in out["schedules"]:
-        ep = out["schedules"]["ep"]
+    ep_key = "ep" if "ep" in out["schedules"] else ("rb" if "rb" in out["schedules"] else None)
+    if ep_key:
+        ep = out["schedules"][ep_key]
         for other in ("default", "naive"):
             if other in out["schedules"]:
                 o = out["schedules"][other]
@@ -156,7 +160,8 @@ def main():
                        "dram_bytes_per_launch": traffic,
                        "source": f"profiles/{a.round}_{a.config}_full.txt (ncu --set full, one cold launch)"}, f,
                       indent=1)
-    print(open(pre + "_launches.csv").read())
+    if rows:
+        print(open(pre + "_launches.csv").read())
     print(json.dumps(out, indent=1))
 
 
