@@ -38,14 +38,15 @@ def main():
     runs = []
     for v in a.variants.split(","):
         if v in ("ep", "ep1", "default", "rb"):
+            key = None
             if v == "default":
                 part = ctx.default_partition(M.m, a.part_size)
-            elif v == "rb":
-                part = ctx.partition_rb(E, M.n, a.part_size)[0]
+            elif v == "rb":       # the bench's map and layout: EPG-RB, tasks in growth order (Z22)
+                part, key, _ = ctx.partition_rb(E, M.n, a.part_size, ranked=True)
             else:
                 ctx.set_partition_method(epg.PARTITION_EPG2 if v == "ep" else epg.PARTITION_EPG1)
                 part = ctx.partition(E, M.n, a.part_size)[0]
-            L, plan = ctx.remap(E, M.n, part, k)
+            L, plan = ctx.remap(E, M.n, part, k, order_key=key)
             nrm = ctx.permute_rows(torch.from_numpy(M.normals).cuda(), L.edge_perm, epg.PERM_GATHER)
             dtn = ctx.permute_rows(torch.from_numpy(dt).cuda(), L.vertex_perm, epg.PERM_SCATTER)
             b = [ctx.permute_rows(Ud, L.vertex_perm, epg.PERM_SCATTER), torch.empty_like(Ud)]
