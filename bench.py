@@ -558,7 +558,7 @@ def run_c3(args, torch, epg, ctx, stream, peak):
     P = args.part_size
     E = torch.from_numpy(M.edges).to(dev)
     k = epg.num_parts(M.m, P)
-    ctx.set_exec_limits(704, 1024)
+    ctx.set_exec_limits(getattr(args, "exec_rows", 0) or 704, 1024)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     part, rank, rep = ctx.partition_rb(E, M.n, P, ranked=True)

@@ -952,7 +952,8 @@ epg_status run_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, 
 
 // edge kernel over execution partitions [first, first + count) only (no finalise)
 template <class Fn>
-epg_status run_edges_range(epg_ctx *ctx, epg_plan *pl, epg_state *state, int64_t first, int64_t count) {
+epg_status run_edges_range(epg_ctx *ctx, epg_plan *pl, epg_state *state, int64_t first, int64_t count,
+                           const int32_t *order = nullptr) {
     if (pl->Scap > kOccMaxEdges || pl->Lcap > occ_max_rows<Fn>())
         return ctx->fail(EPG_ERR_INFEASIBLE, "run_edges: plan exceeds the occupancy kernel limits");
     OccArgs a{};
@@ -974,6 +975,7 @@ epg_status run_edges_range(epg_ctx *ctx, epg_plan *pl, epg_state *state, int64_t
     a.vconst = static_cast<const float *>(state->vertex_const);
     a.halo_buf = pl->halo_buf;
     a.first = first;
+    a.order = order;
     a.hw = pl->hub_words;
     a.hub_acc = nullptr;   // shard ranges sum every halo partial through hv_list
     if (count <= 0) return EPG_OK;
@@ -2340,9 +2342,19 @@ struct ShardState {
     int4 *recs = nullptr;     // finalise records of the shard's shared vertices (local halo entries only)
     int32_t *acc_ids = nullptr;   // distinct vertices other ranks push partial sums for
     int64_t acc_count = 0;
+    // the shard's execution partitions, interior ones first (no halo row owned by a lower
+    // rank: they need nothing from the pull and run while it is in flight), then the boundary
+    int32_t *order = nullptr;
+    int64_t n_interior = 0;
+    // NCCL: the exchanges run on a stream of their own, ordered against the ctx stream by events
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     std::vector<void *> allocs;
     ~ShardState() {
         for (void *p : allocs) cudaFree(p);
+        for (cudaEvent_t e : ev)
+            if (e) cudaEventDestroy(e);
+        if (comm_stream) cudaStreamDestroy(comm_stream);
     }
 };
 
@@ -2454,6 +2466,35 @@ epg_status shard_state(epg_ctx *ctx, epg_plan *pl, int row, ShardState **out) {
         CU(cudaMemcpy(&hmax, hm, sizeof(int32_t), cudaMemcpyDeviceToHost));
         if (hmax <= 6) S->recs = recs;
     }
+    {   // interior / boundary split of the shard's execution partitions (ids in the plan's
+        // halo lists are cpack ids; a lower rank owns exactly the ids below the shard's first row)
+        std::vector<int32_t> xh;
+        const int64_t h0 = pl->hb_h[S->xf], h1 = pl->hb_h[S->xf + S->xc];
+        if (h1 > h0) {
+            xh.resize(h1 - h0);
+            CU(cudaMemcpy(xh.data(), pl->halo_ids + h0, sizeof(int32_t) * (h1 - h0), cudaMemcpyDeviceToHost));
+        }
+        const int32_t v_lo = pl->pvb_h[S->xf];
+        std::vector<int32_t> inner, outer;
+        for (int64_t x = S->xf; x < S->xf + S->xc; x++) {
+            bool foreign = false;
+            for (int64_t q = pl->hb_h[x]; q < pl->hb_h[x + 1] && !foreign; q++) foreign = xh[q - h0] < v_lo;
+            (foreign ? outer : inner).push_back((int32_t)x);
+        }
+        S->n_interior = (int64_t)inner.size();
+        inner.insert(inner.end(), outer.begin(), outer.end());
+        S->order = (int32_t *)shard_alloc(S.get(), sizeof(int32_t) * inner.size(), &e);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return ctx->fail(EPG_ERR_NOMEM, "run_sharded: partition order");
+        }
+        if (!inner.empty())
+            CU(cudaMemcpy(S->order, inner.data(), sizeof(int32_t) * inner.size(), cudaMemcpyHostToDevice));
+    }
+    if (ctx->comm && ctx->comm->nccl && G > 1) {
+        CU(cudaStreamCreateWithFlags(&S->comm_stream, cudaStreamNonBlocking));
+        for (cudaEvent_t &ev : S->ev) CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    }
     *out = S.release();
     shard_states()[key] = *out;
     return EPG_OK;
@@ -2472,7 +2513,7 @@ epg_status rows_move(epg_ctx *ctx, const float *src, float *dst, const int32_t *
 // the grouped point-to-point exchange of one phase: send[p] to every p in `to`, receive
 // recv[p] from every p in `from` (rows of `row` floats)
 epg_status exchange(epg_ctx *ctx, ShardState *S, const float *send, const std::vector<int64_t> &send_off,
-                    float *recv, const std::vector<int64_t> &recv_off) {
+                    float *recv, const std::vector<int64_t> &recv_off, cudaStream_t stream) {
     const int G = S->G, row = S->row;
     Comm *c = ctx->comm;
     if (G == 1) return EPG_OK;
@@ -2483,9 +2524,9 @@ epg_status exchange(epg_ctx *ctx, ShardState *S, const float *send, const std::v
         ncclResult_t r = n->groupStart();
         for (int p = 0; p < G && r == ncclSuccess; p++) {
             const int64_t sc = send_off[p + 1] - send_off[p], rc = recv_off[p + 1] - recv_off[p];
-            if (sc > 0) r = n->send(send + row * send_off[p], (size_t)(row * sc), ncclFloat, p, c->nccl, ctx->stream);
+            if (sc > 0) r = n->send(send + row * send_off[p], (size_t)(row * sc), ncclFloat, p, c->nccl, stream);
             if (r == ncclSuccess && rc > 0)
-                r = n->recv(recv + row * recv_off[p], (size_t)(row * rc), ncclFloat, p, c->nccl, ctx->stream);
+                r = n->recv(recv + row * recv_off[p], (size_t)(row * rc), ncclFloat, p, c->nccl, stream);
         }
         ncclResult_t r2 = n->groupEnd();
         if (r != ncclSuccess || r2 != ncclSuccess)
@@ -2527,8 +2568,7 @@ epg_status sharded_push_accumulate(epg_ctx *ctx, ShardState *S) {
 // finalise of the shard: its shared vertices from the packed local records (or the ranged
 // kernel), then the pushed partial sums of the vertices other ranks share, then untouched rows
 template <class Fn>
-epg_status sharded_finalise(epg_ctx *ctx, epg_plan *pl, ShardState *S, epg_state *st) {
-    if (!S->recs) return run_finalise_range<Fn>(ctx, pl, st, S->sf, S->sc, S->hf, S->hc, S->acc, 1);
+epg_status sharded_finalise_local(epg_ctx *ctx, epg_plan *pl, ShardState *S, epg_state *st) {
     const float *in = static_cast<const float *>(st->state_in);
     float *out = static_cast<float *>(st->state_out);
     const float *vc = static_cast<const float *>(st->vertex_const);
@@ -2536,12 +2576,24 @@ epg_status sharded_finalise(epg_ctx *ctx, epg_plan *pl, ShardState *S, epg_state
     if (work > 0)
         CU(launch_pdl(k_finalise_rec<Fn>, grid_for(work), kThreads, 0, ctx->stream, (const int4 *)S->recs,
                       (const float *)pl->halo_buf, in, out, vc, (int32_t)S->sc, pl->touched, pl->n));
+    return EPG_OK;
+}
+template <class Fn>
+epg_status sharded_acc_add(epg_ctx *ctx, ShardState *S, epg_state *st) {
     const int64_t cnt = S->acc_count;
     if (cnt > 0) {
-        k_acc_add<Fn><<<grid_for(cnt), kThreads, 0, ctx->stream>>>(S->acc_ids, cnt, S->acc, out, vc);
+        k_acc_add<Fn><<<grid_for(cnt), kThreads, 0, ctx->stream>>>(S->acc_ids, cnt, S->acc,
+                                                                   static_cast<float *>(st->state_out),
+                                                                   static_cast<const float *>(st->vertex_const));
         CHECK_LAUNCH();
     }
     return EPG_OK;
+}
+template <class Fn>
+epg_status sharded_finalise(epg_ctx *ctx, epg_plan *pl, ShardState *S, epg_state *st) {
+    if (!S->recs) return run_finalise_range<Fn>(ctx, pl, st, S->sf, S->sc, S->hf, S->hc, S->acc, 1);
+    epg_status e = sharded_finalise_local<Fn>(ctx, pl, S, st);
+    return e ? e : sharded_acc_add<Fn>(ctx, S, st);
 }
 
 template <class Fn>
@@ -2550,18 +2602,46 @@ epg_status run_sharded_t(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t s
     epg_status st = shard_state(ctx, pl, Fn::ROW, &S);
     if (st) return st;
     float *bufs[2] = {static_cast<float *>(state->state_in), static_cast<float *>(state->state_out)};
+    // with a comm stream the exchanges overlap the ctx stream's work:
+    //   ctx:  pack | interior edges .............. | unpack, boundary edges, push pack | local finalise ...... | accumulate
+    //   comm:       (wait ev0) pull exchange (ev1) |                        (wait ev2) push exchange (ev3) |
+    // the kernels and their order on the ctx stream are the sequential schedule's, so the result
+    // is bit-identical to it (same partitions, same summation orders)
+    cudaStream_t cs = S->comm_stream ? S->comm_stream : ctx->stream;
+    auto fork = [&](int e) -> epg_status {
+        if (!S->comm_stream) return EPG_OK;
+        CU(cudaEventRecord(S->ev[e], ctx->stream));
+        CU(cudaStreamWaitEvent(S->comm_stream, S->ev[e], 0));
+        return EPG_OK;
+    };
+    auto join = [&](int e) -> epg_status {
+        if (!S->comm_stream) return EPG_OK;
+        CU(cudaEventRecord(S->ev[e], S->comm_stream));
+        CU(cudaStreamWaitEvent(ctx->stream, S->ev[e], 0));
+        return EPG_OK;
+    };
+    const int64_t nb = S->xc - S->n_interior;
     for (int32_t s = 0; s < steps; s++) {
         epg_state cur = *state;
         cur.state_in = bufs[s & 1];
         cur.state_out = bufs[(s + 1) & 1];
         float *in = static_cast<float *>(cur.state_in);
-        if ((st = sharded_pull_pack<Fn>(ctx, S, in)) ||
-            (st = exchange(ctx, S, S->pull_send, S->send_off, S->pull_recv, S->recv_off)) ||
-            (st = sharded_pull_unpack<Fn>(ctx, S, in)) || (st = run_edges_range<Fn>(ctx, pl, &cur, S->xf, S->xc)) ||
-            (st = sharded_push_pack<Fn>(ctx, pl, S)) ||
-            (st = exchange(ctx, S, S->push_send, S->recv_off, S->push_recv, S->send_off)) ||
-            (st = sharded_push_accumulate<Fn>(ctx, S)) || (st = sharded_finalise<Fn>(ctx, pl, S, &cur)))
+        if ((st = sharded_pull_pack<Fn>(ctx, S, in)) || (st = fork(0)) ||
+            (st = exchange(ctx, S, S->pull_send, S->send_off, S->pull_recv, S->recv_off, cs)) ||
+            (st = run_edges_range<Fn>(ctx, pl, &cur, 0, S->n_interior, S->order)) || (st = join(1)) ||
+            (st = sharded_pull_unpack<Fn>(ctx, S, in)) ||
+            (st = run_edges_range<Fn>(ctx, pl, &cur, S->n_interior, nb, S->order)) ||
+            (st = sharded_push_pack<Fn>(ctx, pl, S)) || (st = fork(2)) ||
+            (st = exchange(ctx, S, S->push_send, S->recv_off, S->push_recv, S->send_off, cs)))
             return st;
+        if (S->recs) {   // the local finalise needs nothing from the push: it runs while that is in flight
+            if ((st = sharded_finalise_local<Fn>(ctx, pl, S, &cur)) || (st = join(3)) ||
+                (st = sharded_push_accumulate<Fn>(ctx, S)) || (st = sharded_acc_add<Fn>(ctx, S, &cur)))
+                return st;
+        } else if ((st = join(3)) || (st = sharded_push_accumulate<Fn>(ctx, S)) ||
+                   (st = sharded_finalise<Fn>(ctx, pl, S, &cur))) {
+            return st;
+        }
     }
     return EPG_OK;
 }
@@ -2598,11 +2678,15 @@ epg_status run_group_t(epg_ctx **ctxs, epg_plan **plans, epg_state *states, int 
     epg_status st = EPG_OK;
     for (int g = 0; g < G && !st; g++) st = sharded_pull_pack<Fn>(ctxs[g], S[g], (const float *)states[g].state_in);
     sync_all();
+    for (int g = 0; g < G && !st; g++)   // interior partitions: nothing from the pull
+        st = run_edges_range<Fn>(ctxs[g], plans[g], &states[g], 0, S[g]->n_interior, S[g]->order);
     copy_phase(true);
     sync_all();
     for (int g = 0; g < G && !st; g++) {
         if ((st = sharded_pull_unpack<Fn>(ctxs[g], S[g], (float *)states[g].state_in))) break;
-        if ((st = run_edges_range<Fn>(ctxs[g], plans[g], &states[g], S[g]->xf, S[g]->xc))) break;
+        if ((st = run_edges_range<Fn>(ctxs[g], plans[g], &states[g], S[g]->n_interior, S[g]->xc - S[g]->n_interior,
+                                      S[g]->order)))
+            break;
         st = sharded_push_pack<Fn>(ctxs[g], plans[g], S[g]);
     }
     sync_all();

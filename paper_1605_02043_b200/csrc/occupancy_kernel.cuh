@@ -60,7 +60,11 @@ struct OccArgs {
     // (dead until the edge phase) at these byte offsets from off_phi
     int st_slots, st_pay, st_vc;
     const float *state_end;    // one past the last row of state_in (bound of the 32-byte halo reads)
+    const int32_t *order;      // NULL, or the execution partitions of this launch are order[first + b]
+                               // (multi-GPU: a shard's interior partitions, then its boundary ones)
 };
+
+__device__ __forceinline__ int64_t occ_part(const OccArgs &a, int64_t x) { return a.order ? a.order[x] : x; }
 
 // L2 prefetch of the aligned body of [g, g + bytes)
 __device__ __forceinline__ void prefetch_region(const void *g, uint32_t bytes) {
@@ -69,14 +73,17 @@ __device__ __forceinline__ void prefetch_region(const void *g, uint32_t bytes) {
     if (hi > lo) ptx::bulk_prefetch_l2(reinterpret_cast<const void *>(lo), (uint32_t)(hi - lo));
 }
 
+#ifndef EPG_OCC_MINB
+#define EPG_OCC_MINB 1   // minimum resident CTAs per SM the register allocation targets (experiments)
+#endif
 template <class Fn, int BLOCK, int EPT, int VPT, int W>
-__global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
+__global__ void __launch_bounds__(BLOCK, EPG_OCC_MINB) k_edge_occ(OccArgs a) {
     extern __shared__ __align__(128) unsigned char occ_smem[];
     __shared__ __align__(8) uint64_t bar;
     constexpr int ROW = Fn::ROW, PW = Fn::PAYW;
     const int tid = threadIdx.x;
     EPG_TP(0, 0);
-    const PartDesc d = a.desc[a.first + blockIdx.x];
+    const PartDesc d = a.desc[occ_part(a, a.first + blockIdx.x)];
     const int L = d.nO + d.nH;
     unsigned char *sblob = occ_smem;
     float *recs = reinterpret_cast<float *>(occ_smem + a.off_recs);
@@ -112,37 +119,41 @@ __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
     // trips become L2 hits
     const bool ahead = a.ahead > 0 && tid == 32 && blockIdx.x + a.ahead < a.count;
     PartDesc f{};
-    if (ahead) f = a.desc[a.first + blockIdx.x + a.ahead];
+    if (ahead) f = a.desc[occ_part(a, a.first + blockIdx.x + a.ahead)];
+    // halo rows H_p. With few halos (nH <= nO, the EP maps) they are gathered right after the
+    // wait so they fly with the bulk copies -- the halo ids open the blob, so each thread reads
+    // its ids from global memory, before the wait (plan data), instead of waiting for the copy.
+    // Halo-heavy partitions (the default map) gather after the copies instead: their halo rows
+    // are mostly other partitions' owned rows that those CTAs' bulk copies are bringing into L2
+    // at the same time.
+    const bool early_halo = d.nH <= d.nO;
+    int32_t hid[VPT];                               // all ids first: one round trip, not VPT
+    if (early_halo) {
+        const int32_t *gh = reinterpret_cast<const int32_t *>(a.blob + 16 * (int64_t)d.blob16);
+#pragma unroll
+        for (int r = 0; r < VPT; r++) {
+            const int j = tid + r * BLOCK;
+            hid[r] = j < d.nH ? __ldg(gh + j) : 0;
+        }
+    }
     ptx::pdl_wait();                               // state_in is final from here on
     // single-wave grids: every CTA of this grid is resident, so the finalise may launch now
     // and load its (static) records on SMs with room while the edge partitions run
     if (a.early_pdl) ptx::pdl_launch_dependents();
     if (tid == 0) region_bulk(rows_base, g_rows, rows_bytes, &bar);
-    // halo rows H_p. With few halos (nH <= nO, the EP maps) they are gathered now so they fly
-    // with the bulk copies -- the halo ids open the blob, so each thread reads its ids from
-    // global memory instead of waiting for the copy. Halo-heavy partitions (the default
-    // map) gather after the copies instead: their halo rows are mostly other partitions'
-    // owned rows that those CTAs' bulk copies are bringing into L2 at the same time.
-    const bool early_halo = d.nH <= d.nO;
     // 5-float rows: every halo row lands as the aligned 32 bytes that contain it (two 16-byte
     // cp.async, L1 bypassed) in a slot of its own after the owned rows; the row sits at byte
     // 4 (h mod 4) of the slot (20 h mod 16). One-float rows are gathered word by word.
     constexpr bool kChunked = ROW == 5;
     unsigned char *halo_slots = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(rows + ROW * d.nO) + 15) & ~uintptr_t(15));
-    auto gather_halo = [&](const int32_t *hid, bool global_ids) {
+    auto gather_halo = [&]() {
         float *hr = rows + ROW * d.nO;
-        int32_t h[VPT];                                 // all ids first: one round trip, not VPT
-#pragma unroll
-        for (int r = 0; r < VPT; r++) {
-            const int j = tid + r * BLOCK;
-            h[r] = j < d.nH ? (global_ids ? __ldg(hid + j) : hid[j]) : 0;
-        }
 #pragma unroll
         for (int r = 0; r < VPT; r++) {                 // one halo row per thread and r
             const int j = tid + r * BLOCK;
             if (j < d.nH) {
-                const float *src = a.state_in + (int64_t)ROW * h[r];
+                const float *src = a.state_in + (int64_t)ROW * hid[r];
                 if constexpr (kChunked) {
                     const float *base = reinterpret_cast<const float *>(reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15));
                     unsigned char *dst = halo_slots + 32 * j;
@@ -161,7 +172,7 @@ __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
             }
         }
     };
-    if (early_halo) gather_halo(reinterpret_cast<const int32_t *>(a.blob + 16 * (int64_t)d.blob16), true);
+    if (early_halo) gather_halo();
     __syncthreads();                               // barrier initialisation visible
     EPG_TP(0, 1);
     ptx::mbar_wait(&bar, 0);
@@ -177,7 +188,15 @@ __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
     else if (tid < 64) region_ragged(st_sl, g_sl, sl_bytes, tid - 32);   // ... and of the staged ranges
     else if (tid < 96) { if (g_pay) region_ragged(st_pay, g_pay, pay_bytes, tid - 64); }
     else if (tid < 128) { if (g_vc) region_ragged(st_vc, g_vc, vc_bytes, tid - 96); }
-    if (!early_halo) gather_halo(reinterpret_cast<const int32_t *>(sblob), false);
+    if (!early_halo) {
+        const int32_t *sh = reinterpret_cast<const int32_t *>(sblob);
+#pragma unroll
+        for (int r = 0; r < VPT; r++) {
+            const int j = tid + r * BLOCK;
+            hid[r] = j < d.nH ? sh[j] : 0;
+        }
+        gather_halo();
+    }
     ptx::cp_async_commit();
     ptx::cp_async_wait<0>();
     __syncthreads();
@@ -232,7 +251,7 @@ __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
 #pragma unroll
     for (int r = 0; r < VPT; r++) {
         const int j = tid + r * BLOCK;
-        if (j < L) Fn::derive_rec(rv[r], recs, j);
+        if (j < L) Fn::derive_occ(rv[r], recs, j);
     }
     __syncthreads();
     // edges
@@ -280,8 +299,8 @@ __global__ void __launch_bounds__(BLOCK) k_edge_occ(OccArgs a) {
         }
         if (j < d.nO) {
             float U[ROW];
-            Fn::rec_state(recs, j, U);
-            Fn::finish_row(U, acc, dtv[r], out[r]);
+            Fn::rec_state_occ(recs, j, U);
+            Fn::finish_occ(U, acc, dtv[r], out[r]);
         } else {
 #pragma unroll
             for (int c = 0; c < ROW; c++) out[r][c] = acc[c];

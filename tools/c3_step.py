@@ -20,8 +20,11 @@ def main():
     ap.add_argument("--comparators", action="store_true")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--order", choices=["growth", "id"], default="growth")
+    ap.add_argument("--part-size", type=int, default=1024)
+    ap.add_argument("--exec-rows", type=int, default=704)
     a = ap.parse_args()
-    args = argparse.Namespace(part_size=1024, c3_steps=a.steps, no_comparators=not a.comparators, order=a.order)
+    args = argparse.Namespace(part_size=a.part_size, c3_steps=a.steps, no_comparators=not a.comparators, order=a.order,
+                              exec_rows=a.exec_rows)
     stream = torch.cuda.current_stream()
     ctx = epg.Context(0, stream)
     peak, _ = bench.measured_peaks()

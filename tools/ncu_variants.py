@@ -29,9 +29,17 @@ def main():
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--variants", default="ep,ep1,default,naive")
     a = ap.parse_args()
-    M = S.config_mesh(a.config)
-    U, dt = S.cfd_state(M.n), S.cfd_dt(M.volume)
+    if a.config in ("c4", "c5"):   # R-MAT gather-scatter / stencil SpMV: bench.py's workload
+        import bench
+        W = bench.Workload(a.config)
+        M = argparse.Namespace(n=W.n, m=W.m, edges=W.edges, normals=W.payload)
+        U, dt, KER = W.state, W.vconst, W.kernel
+    else:
+        M = S.config_mesh(a.config)
+        U, dt, KER = S.cfd_state(M.n), S.cfd_dt(M.volume), epg.KERNEL_CFD_FLUX
     ctx = epg.Context(0)
+    if a.config == "c4":
+        ctx.set_exec_limits(1024, 1024)
     E = torch.from_numpy(M.edges).cuda()
     k = epg.num_parts(M.m, a.part_size)
     Ud = torch.from_numpy(U).cuda()
@@ -42,21 +50,24 @@ def main():
             if v == "default":
                 part = ctx.default_partition(M.m, a.part_size)
             elif v == "rb":       # the bench's map and layout: EPG-RB, tasks in growth order (Z22)
-                part, key, _ = ctx.partition_rb(E, M.n, a.part_size, ranked=True)
+                part, key, _ = ctx.partition_rb(E, M.n, a.part_size, 1, 4096 if a.config == "c4" else 512, ranked=True)
             else:
                 ctx.set_partition_method(epg.PARTITION_EPG2 if v == "ep" else epg.PARTITION_EPG1)
                 part = ctx.partition(E, M.n, a.part_size)[0]
             L, plan = ctx.remap(E, M.n, part, k, order_key=key)
-            nrm = ctx.permute_rows(torch.from_numpy(M.normals).cuda(), L.edge_perm, epg.PERM_GATHER)
-            dtn = ctx.permute_rows(torch.from_numpy(dt).cuda(), L.vertex_perm, epg.PERM_SCATTER)
+            nrm = None if M.normals is None else ctx.permute_rows(torch.from_numpy(M.normals).cuda(), L.edge_perm,
+                                                                   epg.PERM_GATHER)
+            dtn = None if dt is None else ctx.permute_rows(torch.from_numpy(dt).cuda(), L.vertex_perm,
+                                                           epg.PERM_SCATTER)
             b = [ctx.permute_rows(Ud, L.vertex_perm, epg.PERM_SCATTER), torch.empty_like(Ud)]
             runs.append((v, lambda plan=plan, b=b, nrm=nrm, dtn=dtn:
-                         ctx.run(plan, epg.KERNEL_CFD_FLUX, b[0], b[1], nrm, dtn, 1), plan))
+                         ctx.run(plan, KER, b[0], b[1], nrm, dtn, 1), plan))
         else:
             b = [Ud.clone(), torch.empty_like(Ud)]
-            nrm0, dt0 = torch.from_numpy(M.normals).cuda(), torch.from_numpy(dt).cuda()
+            nrm0 = None if M.normals is None else torch.from_numpy(M.normals).cuda()
+            dt0 = None if dt is None else torch.from_numpy(dt).cuda()
             runs.append((v, lambda b=b, nrm0=nrm0, dt0=dt0:
-                         ctx.run_naive(epg.KERNEL_CFD_FLUX, E, M.n, b[0], b[1], nrm0, dt0, 1), None))
+                         ctx.run_naive(KER, E, M.n, b[0], b[1], nrm0, dt0, 1), None))
     torch.cuda.synchronize()
     for r in range(a.reps):
         for name, fn, plan in runs:

@@ -160,7 +160,7 @@ def main():
                        "dram_bytes_per_launch": traffic,
                        "source": f"profiles/{a.round}_{a.config}_full.txt (ncu --set full, one cold launch)"}, f,
                       indent=1)
-    if rows:
+    if os.path.exists(pre + "_launches.csv"):
         print(open(pre + "_launches.csv").read())
     print(json.dumps(out, indent=1))
 
