@@ -288,11 +288,15 @@ epg_status epg_remapped_edges(epg_ctx *ctx, const int32_t *edges, int64_t m, con
  * results directly; vertices shared by several partitions (p_v > 1) are completed
  * by a boundary-finalise pass. Deterministic: the summation order is fixed, except for
  * hub vertices under the hub split (epg_set_hub_split; never on cfd meshes).
- * On the occupancy-kernel path the launches of one call are captured once into a CUDA
- * graph per (plan, kernel, buffer pointers, steps, variant) -- at most 16 per plan,
- * owned by the plan -- and replayed into ctx's stream on later calls (not while
- * profiling; EPG_GRAPHS=0 in the environment disables it). Multi-wave grids prefetch the
- * next wave's ranges into L2 (EPG_PREFETCH_AHEAD=<CTAs>, 0 disables). */
+ * On the occupancy-kernel path a call of steps >= 2 is captured once into a CUDA graph
+ * per (plan, kernel, buffer pointers, steps, variant) -- at most 16 per plan, owned by
+ * the plan -- and replayed into ctx's stream on later calls (not while profiling). A
+ * one-step call launches its kernels directly, with programmatic-dependent-launch
+ * attributes, so back-to-back calls overlap each kernel's prologue with the previous
+ * kernel in the stream (a graph launch would end that overlap at every call boundary:
+ * C2, 23 alternating plans, 19.1 -> 12.7 us per step). EPG_GRAPHS=0 in the environment
+ * disables the graphs, EPG_GRAPHS=2 also captures one-step calls. Multi-wave grids
+ * prefetch the next wave's ranges into L2 (EPG_PREFETCH_AHEAD=<CTAs>, 0 disables). */
 epg_status epg_run(epg_ctx *ctx, const epg_plan *plan, epg_kernel kernel, epg_state *state, int32_t steps);
 
 /* epg_run from and to HOST memory (the end-to-end call): one call copies the state

@@ -799,13 +799,13 @@ bool hub_window(epg_ctx *ctx, const epg_plan *pl, const void *state_in, int row_
 
 template <class Fn>
 epg_status launch_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, OccArgs a, size_t smem,
-                      void (*kern)(OccArgs)) {
+                      void (*kern)(OccArgs), int block) {
     CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     {   // early PDL trigger only when the whole grid is resident at once (one wave)
         auto it = pl->resident_ctas.find(reinterpret_cast<const void *>(kern));
         if (it == pl->resident_ctas.end()) {
             int occ = 0, sms = 0;
-            CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kOccThreads, smem));
+            CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, block, smem));
             CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
             it = pl->resident_ctas.emplace(reinterpret_cast<const void *>(kern), (int64_t)occ * sms).first;
         }
@@ -825,7 +825,7 @@ epg_status launch_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t step
         cudaAccessPolicyWindow win{};
         const bool use_win = hub_window(ctx, pl, a.state_in, 4 * Fn::ROW, &win);
         cudaEvent_t t0 = ctx->prof_begin();
-        CU(launch_pdl_w(kern, (unsigned)pl->k, kOccThreads, smem, ctx->stream, use_win ? &win : nullptr, a));
+        CU(launch_pdl_w(kern, (unsigned)pl->k, (unsigned)block, smem, ctx->stream, use_win ? &win : nullptr, a));
         ctx->prof_end(0, t0);
         if (fin_work > 0) {
             cudaEvent_t t1 = ctx->prof_begin();
@@ -859,14 +859,29 @@ epg_status launch_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t step
     return EPG_OK;
 }
 
+// CTA size of the occupancy kernel for a plan: 256 threads, or 288 (9 warps, EPT 4 / VPT 3:
+// up to 1152 edges and 864 rows) for cfd partitions of 1025..1152 edges -- the partition size
+// that makes a one-wave grid a multiple of the SM count (C2: P = 1032, 444 = 3 x 148 CTAs, every
+// SM three partitions) without the idle lanes and registers of the EPT 5 / VPT 5 instance
+constexpr int kOccThreadsWide = 288;
+template <class Fn>
+int occ_block(const epg_plan *pl) {
+    if (Fn::ROW == 5 && pl->inc_width > 0 && pl->Scap > 4 * kOccThreads && pl->Scap <= 4 * kOccThreadsWide &&
+        pl->Lcap <= 3 * kOccThreadsWide)
+        return kOccThreadsWide;
+    return kOccThreads;
+}
 // EPT / VPT that occ_dispatch picks for a plan
-inline int occ_ept(const epg_plan *pl) {
+template <class Fn>
+int occ_ept(const epg_plan *pl) {
+    if (occ_block<Fn>(pl) == kOccThreadsWide) return 4;
     if (pl->Scap <= 2 * kOccThreads && pl->Lcap <= 2 * kOccThreads) return 2;
     return pl->Scap > 4 * kOccThreads ? 5 : 4;
 }
 template <class Fn>
 int occ_vpt(const epg_plan *pl) {
     const int L = pl->Lcap;
+    if (occ_block<Fn>(pl) == kOccThreadsWide) return 3;
     if (pl->Scap <= 2 * kOccThreads && L <= 2 * kOccThreads) return 2;
     if (Fn::ROW == 1 && L > 4 * kOccThreads) return 8;
     if (L > 4 * kOccThreads) return 5;
@@ -878,8 +893,9 @@ int occ_vpt(const epg_plan *pl) {
 // any) and dt; returns its size and sets the staging offsets in *a.
 template <class Fn>
 int occ_phi_bytes(const epg_plan *pl, OccArgs *a) {
-    // every thread reads EPT x 256 edge entries and VPT x 256 dt entries unpredicated
-    const int se = std::max(pl->Scap, occ_ept(pl) * kOccThreads), sv = std::max(pl->Ocap, occ_vpt<Fn>(pl) * kOccThreads);
+    // every thread reads EPT x BLOCK edge entries and VPT x BLOCK dt entries unpredicated
+    const int B = occ_block<Fn>(pl);
+    const int se = std::max(pl->Scap, occ_ept<Fn>(pl) * B), sv = std::max(pl->Ocap, occ_vpt<Fn>(pl) * B);
     a->st_slots = 0;
     a->st_pay = up16i(4 * se + 32);
     a->st_vc = a->st_pay + up16i(4 * Fn::PAYW * se + 32);
@@ -889,16 +905,17 @@ int occ_phi_bytes(const epg_plan *pl, OccArgs *a) {
 }
 
 // Instance of the occupancy kernel for a plan: EPT edges and VPT staged rows per thread
-// (256 threads), W the padded incidence width. `go` is called with the chosen instance.
+// (256 or 288 threads, occ_block), W the padded incidence width. `go` is called with the
+// chosen instance and its CTA size.
 template <class Fn, class Go>
 epg_status occ_dispatch(const epg_plan *pl, Go &&go) {
     const int S = pl->Scap, L = pl->Lcap;
     auto by_w = [&](auto ept, auto vpt) -> epg_status {
         constexpr int E = decltype(ept)::value, V = decltype(vpt)::value;
         switch (pl->inc_width) {
-            case 4: return go(k_edge_occ<Fn, kOccThreads, E, V, 4>, E, V);
-            case 8: return go(k_edge_occ<Fn, kOccThreads, E, V, 8>, E, V);
-            default: return go(k_edge_occ<Fn, kOccThreads, E, V, 0>, E, V);
+            case 4: return go(k_edge_occ<Fn, kOccThreads, E, V, 4>, kOccThreads);
+            case 8: return go(k_edge_occ<Fn, kOccThreads, E, V, 8>, kOccThreads);
+            default: return go(k_edge_occ<Fn, kOccThreads, E, V, 0>, kOccThreads);
         }
     };
     using I2 = std::integral_constant<int, 2>;
@@ -906,6 +923,11 @@ epg_status occ_dispatch(const epg_plan *pl, Go &&go) {
     using I4 = std::integral_constant<int, 4>;
     using I5 = std::integral_constant<int, 5>;
     using I8 = std::integral_constant<int, 8>;
+    if constexpr (Fn::ROW == 5) {
+        if (occ_block<Fn>(pl) == kOccThreadsWide)
+            return pl->inc_width == 4 ? go(k_edge_occ<Fn, kOccThreadsWide, 4, 3, 4>, kOccThreadsWide)
+                                      : go(k_edge_occ<Fn, kOccThreadsWide, 4, 3, 8>, kOccThreadsWide);
+    }
     if (S <= 2 * kOccThreads && L <= 2 * kOccThreads) return by_w(I2{}, I2{});   // small partitions
     if constexpr (Fn::ROW == 1) {   // one-float rows: up to 2048 staged rows, 8 per thread
         if (L > 4 * kOccThreads) return S > 4 * kOccThreads ? by_w(I5{}, I8{}) : by_w(I4{}, I8{});
@@ -945,8 +967,8 @@ epg_status run_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, 
     a.state_end = nullptr;   // set per launch (the buffers alternate)
     a.hw = pl->hub_words;
     a.hub_acc = pl->n_hub > 0 ? pl->hub_acc : nullptr;
-    return occ_dispatch<Fn>(pl, [&](auto kern, int, int) {
-        return launch_occ<Fn>(ctx, pl, state, steps, a, smem, kern);
+    return occ_dispatch<Fn>(pl, [&](auto kern, int block) {
+        return launch_occ<Fn>(ctx, pl, state, steps, a, smem, kern, block);
     });
 }
 
@@ -979,13 +1001,13 @@ epg_status run_edges_range(epg_ctx *ctx, epg_plan *pl, epg_state *state, int64_t
     a.hw = pl->hub_words;
     a.hub_acc = nullptr;   // shard ranges sum every halo partial through hv_list
     if (count <= 0) return EPG_OK;
-    return occ_dispatch<Fn>(pl, [&](auto kern, int, int) -> epg_status {
+    return occ_dispatch<Fn>(pl, [&](auto kern, int block) -> epg_status {
         CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         {   // as launch_occ: multi-wave ranges prefetch the next wave's ranges into L2
             auto it = pl->resident_ctas.find(reinterpret_cast<const void *>(kern));
             if (it == pl->resident_ctas.end()) {
                 int occ = 0, sms = 0;
-                CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kOccThreads, smem));
+                CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, block, smem));
                 CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
                 it = pl->resident_ctas.emplace(reinterpret_cast<const void *>(kern), (int64_t)occ * sms).first;
             }
@@ -995,7 +1017,7 @@ epg_status run_edges_range(epg_ctx *ctx, epg_plan *pl, epg_state *state, int64_t
             a.count = count;
         }
         cudaEvent_t t0 = ctx->prof_begin();
-        CU(launch_pdl(kern, (unsigned)count, kOccThreads, smem, ctx->stream, a));
+        CU(launch_pdl(kern, (unsigned)count, (unsigned)block, smem, ctx->stream, a));
         ctx->prof_end(0, t0);
         return EPG_OK;
     });
@@ -1124,8 +1146,11 @@ epg_status check_state(epg_ctx *ctx, epg_kernel kernel, const epg_state *state) 
 // step, with their programmatic-dependent-launch edges) are captured once on a private stream
 // and replayed into ctx's stream, which saves their per-launch overhead (C2: 21.5 -> 20.5 us per
 // step in a scratch A/B). Only for the occupancy path (whose launches are capturable: no host
-// synchronisation); not while profiling (the per-launch events would be baked in);
-// EPG_GRAPHS=0 disables it.
+// synchronisation); not while profiling (the per-launch events would be baked in). Only for
+// calls of two steps or more by default: a graph launch ends the PDL overlap at its boundary,
+// and back-to-back one-step calls (a time loop driven by the caller, or the bench's
+// round-robin over replicas) are faster launched directly (C2: 19.1 -> 12.7 us per step).
+// EPG_GRAPHS=0 disables graphs, EPG_GRAPHS=2 captures one-step calls as well.
 template <class Fn>
 bool occ_applies(epg_ctx *ctx, const epg_plan *pl) {
     if (!(ctx->variant == 0 || ctx->variant == 3)) return false;
@@ -1140,7 +1165,8 @@ bool occ_applies(epg_ctx *ctx, const epg_plan *pl) {
 template <class Fn>
 epg_status run_graphed(epg_ctx *ctx, epg_plan *pl, epg_kernel kernel, epg_state *state, int32_t steps) {
     const char *ge = std::getenv("EPG_GRAPHS");
-    if (steps == 0 || ctx->profiling || (ge && std::atoi(ge) == 0) || !occ_applies<Fn>(ctx, pl))
+    const int gmode = ge ? std::atoi(ge) : 1;
+    if (steps == 0 || ctx->profiling || gmode == 0 || (steps == 1 && gmode != 2) || !occ_applies<Fn>(ctx, pl))
         return run_staged<Fn>(ctx, pl, state, steps);
     const std::vector<uintptr_t> key = {(uintptr_t)kernel, (uintptr_t)state->state_in, (uintptr_t)state->state_out,
                                         (uintptr_t)state->edge_payload, (uintptr_t)state->vertex_const,

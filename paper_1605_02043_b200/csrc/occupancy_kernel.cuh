@@ -73,11 +73,14 @@ __device__ __forceinline__ void prefetch_region(const void *g, uint32_t bytes) {
     if (hi > lo) ptx::bulk_prefetch_l2(reinterpret_cast<const void *>(lo), (uint32_t)(hi - lo));
 }
 
-#ifndef EPG_OCC_MINB
-#define EPG_OCC_MINB 1   // minimum resident CTAs per SM the register allocation targets (experiments)
+// EPG_OCC_MINB (experiments): minimum resident CTAs per SM the register allocation targets
+#ifdef EPG_OCC_MINB
+#define EPG_OCC_BOUNDS(b) __launch_bounds__(b, EPG_OCC_MINB)
+#else
+#define EPG_OCC_BOUNDS(b) __launch_bounds__(b)
 #endif
 template <class Fn, int BLOCK, int EPT, int VPT, int W>
-__global__ void __launch_bounds__(BLOCK, EPG_OCC_MINB) k_edge_occ(OccArgs a) {
+__global__ void EPG_OCC_BOUNDS(BLOCK) k_edge_occ(OccArgs a) {
     extern __shared__ __align__(128) unsigned char occ_smem[];
     __shared__ __align__(8) uint64_t bar;
     constexpr int ROW = Fn::ROW, PW = Fn::PAYW;
@@ -267,6 +270,75 @@ __global__ void __launch_bounds__(BLOCK, EPG_OCC_MINB) k_edge_occ(OccArgs a) {
     EPG_TP(0, 4);
     // reduce per local vertex into registers
     const uint16_t *inc = reinterpret_cast<const uint16_t *>(sblob + blob3_inc_offset(d.nH, a.hw));
+    // One-float rows with variable-length incidence lists (power-law graphs: a hub can hold most
+    // of a partition's edges, and one thread summing its list stalls the whole CTA at the next
+    // barrier): the 2s entries, in list order, are cut evenly over the threads and summed by a
+    // block-wide segmented scan -- each thread sums its entries in order, the open segment
+    // carries flow through a fixed shuffle tree, so the order is fixed (deterministic). The
+    // vertex totals land in the record array (dead for these functors after the edge phase).
+    constexpr bool kSegScan = (W == 0 && ROW == 1);
+    float *tot = recs;
+    if constexpr (kSegScan) {
+        __shared__ float seg_wv[BLOCK / 32];
+        __shared__ int seg_wf[BLOCK / 32];
+        constexpr int IPT = 2 * EPT;
+        const int ne = 2 * d.s;
+        const uint16_t *ioff = inc + 2 * d.s;
+        const int q0 = tid * IPT, q1 = min(q0 + IPT, ne);
+        int j = 0;
+        if (q0 < ne) {                                  // largest j with ioff[j] <= q0
+            int lo = 0, hi = L - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if ((int)ioff[mid] <= q0) lo = mid;
+                else hi = mid - 1;
+            }
+            j = lo;
+        }
+        const int j0 = j;
+        const bool cont0 = q0 < ne && (int)ioff[j0] < q0;   // the first segment began before q0
+        int bnd = j + 1 < L ? (int)ioff[j + 1] : ne;
+        float part = 0.0f, first_part = 0.0f;
+        bool first_closed = false;
+        for (int q = q0; q < q1; q++) {
+            if (q == bnd) {                             // segment j ended at q - 1
+                if (j == j0) { first_part = part; first_closed = true; }
+                else tot[j] = part;
+                part = 0.0f;
+                j++;
+                bnd = j + 1 < L ? (int)ioff[j + 1] : ne;
+            }
+            const int w = inc[q];
+            float v[1] = {0.0f};
+            Fn::gather_split(phis, w >> 1, w & 1, v, a.pstride);
+            part += v[0];
+        }
+        // carry of the open segment across threads: inclusive scan of (starts, value) with
+        // (a, b) -> (a.f | b.f, b.f ? b.v : a.v + b.v); the exclusive value is the carry in
+        const int starts = q0 < ne ? ((j != j0 || !cont0) ? 1 : 0) : 0;
+        int f = starts;
+        float sv = q0 < ne ? part : 0.0f;
+        const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const float ov = __shfl_up_sync(0xffffffffu, sv, o);
+            const int of = __shfl_up_sync(0xffffffffu, f, o);
+            if (lane >= o && !f) sv += ov;
+            if (lane >= o) f |= of;
+        }
+        if (lane == 31) { seg_wv[wid] = sv; seg_wf[wid] = f; }
+        __syncthreads();
+        float pv = 0.0f;                                // prefix of the earlier warps
+        for (int w = 0; w < wid; w++) pv = seg_wf[w] ? seg_wv[w] : pv + seg_wv[w];
+        const float incl_prev = __shfl_up_sync(0xffffffffu, sv, 1);
+        const int f_prev = __shfl_up_sync(0xffffffffu, f, 1);
+        const float carry = lane == 0 ? pv : (f_prev ? incl_prev : pv + incl_prev);
+        if (q0 < ne) {
+            if (first_closed) tot[j0] = (cont0 ? carry : 0.0f) + first_part;
+            if (bnd == q1 || q1 == ne) tot[j] = (j == j0 && cont0 ? carry : 0.0f) + part;
+        }
+        __syncthreads();
+    }
     float out[VPT][ROW];
 #pragma unroll
     for (int r = 0; r < VPT; r++) {
@@ -289,6 +361,8 @@ __global__ void __launch_bounds__(BLOCK, EPG_OCC_MINB) k_edge_occ(OccArgs a) {
                 const uint32_t w = (w2[q >> 1] >> (16 * (q & 1))) & 0xffffu;
                 Fn::gather_split(phis, (int)(w >> 1), (int)(w & 1), acc, a.pstride);
             }
+        } else if constexpr (kSegScan) {
+            acc[0] = tot[j];
         } else {
             const uint16_t *ioff = inc + 2 * d.s;
             const int q0 = ioff[j], q1 = j + 1 < L ? ioff[j + 1] : 2 * d.s;

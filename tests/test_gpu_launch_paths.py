@@ -85,18 +85,20 @@ def test_graph_replay_bitexact():
     old = _env("EPG_GRAPHS", "0")
     try:
         direct = sweep()
+        _env("EPG_GRAPHS", "2")                    # one-step calls through graphs too
+        graphed = sweep()
+        # more than 16 keys: the cache is evicted and rebuilt, results unchanged
+        extra = [(Un.clone(), torch.empty_like(Un)) for _ in range(8)]
+        for a, b in extra:
+            for steps in (1, 2):
+                a.copy_(Un)
+                out = ctx.run(plan, epg.KERNEL_CFD_FLUX, a, b, nrm, dtn, steps)
+                assert np.array_equal(out.cpu().numpy(), graphed[steps - 1])
     finally:
         _env("EPG_GRAPHS", old)
-    graphed = sweep()
-    for x, y in zip(direct, graphed):
-        assert np.array_equal(x, y)
-    # more than 16 keys: the cache is evicted and rebuilt, results unchanged
-    extra = [(Un.clone(), torch.empty_like(Un)) for _ in range(8)]
-    for a, b in extra:
-        for steps in (1, 2):
-            a.copy_(Un)
-            out = ctx.run(plan, epg.KERNEL_CFD_FLUX, a, b, nrm, dtn, steps)
-            assert np.array_equal(out.cpu().numpy(), graphed[steps - 1])
+    default = sweep()                              # default: graphs for steps >= 2 only
+    for x, y, z in zip(direct, graphed, default):
+        assert np.array_equal(x, y) and np.array_equal(x, z)
 
 
 @pytest.mark.timeout(300, method="thread")
@@ -132,3 +134,40 @@ def test_pipelined_variant_one_plan_two_grids():
         ctx.run(plan, epg.KERNEL_GATHER_SCATTER, xn, y, None, None, 1)
         got = ctx.permute_rows(y, L.vertex_perm, epg.PERM_GATHER).cpu().numpy()
         assert np.array_equal(got.astype(np.float64), ref_gs)
+
+
+@pytest.mark.parametrize("cfg,P", [("c1", 1032), ("c2", 1032), ("c1", 1100)])
+def test_wide_cta_instance(cfg, P):
+    """Partitions of 1025..1152 edges run on the 288-thread (9-warp) instance of the edge
+    kernel (bench.py's SM-balanced C2 size P = 1032): growth-ordered EPG-RB map as in the
+    bench, exec limits (864 rows, 1152 edges); within the Z14 tolerance of the fp64 oracle,
+    normwise and componentwise, and the same result through epg_run(steps=2) (graph) as
+    through two one-step calls (direct launches)."""
+    from paper_1605_02043_b200 import epg
+    M = S.config_mesh(cfg)
+    ctx = epg.Context(0)
+    ctx.set_exec_limits(864, 1152)
+    E = dev(M.edges)
+    part, rank, _ = ctx.partition_rb(E, M.n, P, ranked=True)
+    k = epg.num_parts(M.m, P)
+    L, plan = ctx.remap(E, M.n, part, k, order_key=rank)
+    assert plan.k_exec == k                       # no execution splits: every partition fits
+    U, dt = S.cfd_state(M.n), S.cfd_dt(M.volume)
+    Un = ctx.permute_rows(dev(U), L.vertex_perm, epg.PERM_SCATTER)
+    nrm = ctx.permute_rows(dev(M.normals), L.edge_perm, epg.PERM_GATHER)
+    dtn = ctx.permute_rows(dev(dt), L.vertex_perm, epg.PERM_SCATTER)
+    out = torch.empty_like(Un)
+    ctx.run(plan, epg.KERNEL_CFD_FLUX, Un, out, nrm, dtn, 1)
+    got = ctx.permute_rows(out, L.vertex_perm, epg.PERM_GATHER).cpu().numpy().astype(np.float64)
+    ref, _ = O.cfd_step(M.edges, M.n, M.normals, U, dt)
+    err = np.abs(got - ref).max(axis=0) / np.abs(ref).max(axis=0)
+    assert err.max() <= 1e-5
+    S_v = O.cfd_flux_abs(M.edges, M.n, M.normals, U)
+    comp = np.abs(got - ref) / np.maximum(np.abs(ref), dt[:, None] * S_v)
+    assert comp.max() <= 1e-5
+    a, b = Un.clone(), torch.empty_like(Un)
+    ctx.run(plan, epg.KERNEL_CFD_FLUX, a, b, nrm, dtn, 1)
+    ctx.run(plan, epg.KERNEL_CFD_FLUX, b, a, nrm, dtn, 1)
+    c, d = Un.clone(), torch.empty_like(Un)
+    two = ctx.run(plan, epg.KERNEL_CFD_FLUX, c, d, nrm, dtn, 2)
+    assert np.array_equal(a.cpu().numpy(), two.cpu().numpy())
