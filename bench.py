@@ -111,7 +111,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=["c1", "c2", "c3", "c4", "c5"], default=None,
                     help="workload (default: c2 on one GPU, c3 with --gpus N > 1)")
-    ap.add_argument("--part-size", type=int, default=1024)
+    ap.add_argument("--part-size", type=int, default=1024,
+                    help="edges per EP partition (1025..1152: the 288-thread instance of the edge kernel)")
     ap.add_argument("--flush-mib", type=int, default=512)
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="bounded oracle sample for cpu_baseline")
     ap.add_argument("--variant", type=int, default=0,
@@ -555,7 +556,7 @@ def run_c3(args, torch, epg, ctx, stream, peak):
     M = S.config_mesh("c3")
     gen = time.perf_counter() - t0
     dev = ctx.device
-    P = args.part_size
+    P = args.part_size if getattr(args, "config", "c3") == "c3" else 1024
     E = torch.from_numpy(M.edges).to(dev)
     k = epg.num_parts(M.m, P)
     ctx.set_exec_limits(getattr(args, "exec_rows", 0) or 704, 1024)
@@ -651,6 +652,8 @@ def run_ours(args, rank, local_rank, world):
     KER = M.kernel
     if args.exec_rows:
         M.exec_rows = args.exec_rows
+    if P > 1024 and M.kernel == epg.KERNEL_CFD_FLUX and not args.exec_rows:
+        M.exec_rows = 1152                     # the 288-thread instance: up to 1152 edges and rows
     ctx.set_exec_limits(M.exec_rows, args.exec_edges or (1280 if P > 1024 else 1024))
     ctx.set_variant(args.variant)
     ctx.set_hub_l2(bool(args.hub_l2))

@@ -24,6 +24,7 @@
 #include "run_kernels.cuh"
 #include "pipelined_kernel.cuh"
 #include "occupancy_kernel.cuh"
+#include "place_kernels.cuh"
 #include "rb_kernels.cuh"
 
 // epg_run_host's pipeline (ctx-owned): copy-in and copy-out streams beside the ctx stream,
@@ -93,6 +94,7 @@ struct epg_plan {
     int32_t *peb = nullptr, *pvb = nullptr, *hb = nullptr, *halo_ids = nullptr, *sidx = nullptr;
     int32_t *shared_ids = nullptr, *hv_off = nullptr, *hv_list = nullptr;
     uint32_t *slots = nullptr;
+    uint32_t *slots_occ = nullptr;   // occupancy kernel: placed record positions + Phi position (place_kernels.cuh)
     uint16_t *inc = nullptr, *inc_off = nullptr;
     float *owner_buf = nullptr, *halo_buf = nullptr;
     // pipelined kernel: per-partition descriptors and contiguous blobs
@@ -581,6 +583,30 @@ epg_status build_pipeline_blob(epg_ctx *ctx, epg_plan *pl) {
     pl->pvb_h = pvb;
     pl->hb_h = hb;
     pl->blob_max = bmax;
+    {   // bank-conflict-aware placement of every partition's records (place_kernels.cuh, one
+        // warp per partition); EPG_PLACE=0, or variable-length incidence, keeps the identity
+        const int64_t m = peb[k], nl = (int64_t)pvb[k] + hb[k];
+        if ((st = plan_alloc_t(pl, ctx, &pl->slots_occ, std::max<int64_t>(m, 1)))) return st;
+        Tmp dv(ctx), de(ctx);
+        CU(dv.alloc(std::max<int64_t>(nl, 1)));
+        CU(de.alloc(std::max<int64_t>(m, 1)));
+        const char *pe = std::getenv("EPG_PLACE");
+        const bool place = !(pe && std::atoi(pe) == 0) && (W == 4 || W == 8);
+        if (place) {
+            const int sm = place_smem_bytes(pl->Scap, pl->Lcap, W);
+            auto kp = W == 4 ? k_place<4> : k_place<8>;
+            CU(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+            kp<<<(unsigned)k, 32, sm, ctx->stream>>>(pl->desc3, pl->slots, pl->Scap, pl->Lcap, dv.as<uint8_t>(),
+                                                      de.as<uint8_t>());
+        } else {
+            k_place_identity<<<(unsigned)k, 256, 0, ctx->stream>>>(pl->desc3, dv.as<uint8_t>(), de.as<uint8_t>());
+        }
+        CHECK_LAUNCH();
+        k_apply_place<<<(unsigned)k, 256, 0, ctx->stream>>>(pl->desc3, pl->slots, dv.as<uint8_t>(), de.as<uint8_t>(), W,
+                                                            pl->hub_words, pl->Scap, pl->blob3, pl->slots_occ);
+        CHECK_LAUNCH();
+        CU(cudaStreamSynchronize(ctx->stream));   // the temporaries die here
+    }
     return EPG_OK;
 }
 
@@ -859,15 +885,15 @@ epg_status launch_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t step
     return EPG_OK;
 }
 
-// CTA size of the occupancy kernel for a plan: 256 threads, or 288 (9 warps, EPT 4 / VPT 3:
-// up to 1152 edges and 864 rows) for cfd partitions of 1025..1152 edges -- the partition size
+// CTA size of the occupancy kernel for a plan: 256 threads, or 288 (9 warps, EPT 4 / VPT 3-4:
+// up to 1152 edges and 1152 rows) for cfd partitions of 1025..1152 edges -- the partition size
 // that makes a one-wave grid a multiple of the SM count (C2: P = 1032, 444 = 3 x 148 CTAs, every
 // SM three partitions) without the idle lanes and registers of the EPT 5 / VPT 5 instance
 constexpr int kOccThreadsWide = 288;
 template <class Fn>
 int occ_block(const epg_plan *pl) {
     if (Fn::ROW == 5 && pl->inc_width > 0 && pl->Scap > 4 * kOccThreads && pl->Scap <= 4 * kOccThreadsWide &&
-        pl->Lcap <= 3 * kOccThreadsWide)
+        pl->Lcap <= 4 * kOccThreadsWide)
         return kOccThreadsWide;
     return kOccThreads;
 }
@@ -881,7 +907,7 @@ int occ_ept(const epg_plan *pl) {
 template <class Fn>
 int occ_vpt(const epg_plan *pl) {
     const int L = pl->Lcap;
-    if (occ_block<Fn>(pl) == kOccThreadsWide) return 3;
+    if (occ_block<Fn>(pl) == kOccThreadsWide) return L > 3 * kOccThreadsWide ? 4 : 3;
     if (pl->Scap <= 2 * kOccThreads && L <= 2 * kOccThreads) return 2;
     if (Fn::ROW == 1 && L > 4 * kOccThreads) return 8;
     if (L > 4 * kOccThreads) return 5;
@@ -924,9 +950,13 @@ epg_status occ_dispatch(const epg_plan *pl, Go &&go) {
     using I5 = std::integral_constant<int, 5>;
     using I8 = std::integral_constant<int, 8>;
     if constexpr (Fn::ROW == 5) {
-        if (occ_block<Fn>(pl) == kOccThreadsWide)
+        if (occ_block<Fn>(pl) == kOccThreadsWide) {
+            if (L > 3 * kOccThreadsWide)
+                return pl->inc_width == 4 ? go(k_edge_occ<Fn, kOccThreadsWide, 4, 4, 4>, kOccThreadsWide)
+                                          : go(k_edge_occ<Fn, kOccThreadsWide, 4, 4, 8>, kOccThreadsWide);
             return pl->inc_width == 4 ? go(k_edge_occ<Fn, kOccThreadsWide, 4, 3, 4>, kOccThreadsWide)
                                       : go(k_edge_occ<Fn, kOccThreadsWide, 4, 3, 8>, kOccThreadsWide);
+        }
     }
     if (S <= 2 * kOccThreads && L <= 2 * kOccThreads) return by_w(I2{}, I2{});   // small partitions
     if constexpr (Fn::ROW == 1) {   // one-float rows: up to 2048 staged rows, 8 per thread
@@ -959,7 +989,7 @@ epg_status run_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, 
     *fits = true;
     a.desc = pl->desc3;
     a.blob = pl->blob3;
-    a.slots = pl->slots;
+    a.slots = pl->slots_occ;
     a.payload = static_cast<const float *>(state->edge_payload);
     a.vconst = static_cast<const float *>(state->vertex_const);
     a.halo_buf = pl->halo_buf;
@@ -989,7 +1019,7 @@ epg_status run_edges_range(epg_ctx *ctx, epg_plan *pl, epg_state *state, int64_t
     const size_t smem = (size_t)a.off_phi + occ_phi_bytes<Fn>(pl, &a);
     a.desc = pl->desc3;
     a.blob = pl->blob3;
-    a.slots = pl->slots;
+    a.slots = pl->slots_occ;
     a.state_in = static_cast<const float *>(state->state_in);
     a.state_out = static_cast<float *>(state->state_out);
     a.state_end = a.state_in + (int64_t)Fn::ROW * pl->n;

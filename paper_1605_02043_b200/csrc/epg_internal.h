@@ -31,6 +31,7 @@ epg_status rb_leaves(const int32_t *local_edges, int64_t m, const int32_t *n_loc
 // number of CPUs this process may run on (affinity mask)
 int host_cpus();
 
+
 // the CUDA stream a context enqueues on (api.cu)
 void *ctx_stream(epg_ctx *ctx);
 int ctx_device(epg_ctx *ctx);

@@ -29,13 +29,17 @@ namespace epg {
 
 // blob of the occupancy kernel: [halo ids nH x i32] ([hub index nH x i32] when the plan has
 // hubs: hw = 2 words per halo row) pad16 [incidence] (W as in the pipelined blob: W x L u16
-// padded lists, or W = 0: 2s u16 entries + L u16 offsets)
+// padded lists, or W = 0: 2s u16 entries + L u16 offsets) pad16 [placement: L x u8, the
+// in-group position of each local vertex's derived record, place_kernels.cuh]
 __host__ __device__ __forceinline__ int blob3_inc_offset(int nH, int hw = 1) { return (4 * hw * nH + 15) & ~15; }
+__host__ __device__ __forceinline__ int blob3_col_offset(int nH, int s, int L, int W, int hw = 1) {
+    const int inc = W > 0 ? 2 * W * L : 4 * s + 2 * L;
+    return (blob3_inc_offset(nH, hw) + inc + 15) & ~15;
+}
 // padded incidence entries point at Phi record `sentinel` (the plan's largest execution
 // partition, >= every edge index), kept zero by the kernel
 __host__ __device__ __forceinline__ int blob3_bytes_for(int nH, int s, int L, int W, int hw = 1) {
-    const int inc = W > 0 ? 2 * W * L : 4 * s + 2 * L;
-    return (blob3_inc_offset(nH, hw) + inc + 15) & ~15;
+    return (blob3_col_offset(nH, s, L, W, hw) + L + 15) & ~15;
 }
 
 struct OccArgs {
@@ -89,6 +93,7 @@ __global__ void EPG_OCC_BOUNDS(BLOCK) k_edge_occ(OccArgs a) {
     const PartDesc d = a.desc[occ_part(a, a.first + blockIdx.x)];
     const int L = d.nO + d.nH;
     unsigned char *sblob = occ_smem;
+    const uint8_t *scol = sblob + blob3_col_offset(d.nH, d.s, L, W, a.hw);   // record placement
     float *recs = reinterpret_cast<float *>(occ_smem + a.off_recs);
     float *phis = reinterpret_cast<float *>(occ_smem + a.off_phi);
     const float *g_rows = a.state_in + (int64_t)ROW * d.o0;
@@ -254,14 +259,16 @@ __global__ void EPG_OCC_BOUNDS(BLOCK) k_edge_occ(OccArgs a) {
 #pragma unroll
     for (int r = 0; r < VPT; r++) {
         const int j = tid + r * BLOCK;
-        if (j < L) Fn::derive_occ(rv[r], recs, j);
+        if (j < L) Fn::derive_occ(rv[r], recs, (j & ~7) | scol[j]);   // placed record (place_kernels.cuh)
     }
     __syncthreads();
     // edges
 #pragma unroll
     for (int r = 0; r < EPT; r++) {
         const int i = tid + r * BLOCK;
-        if (i < d.s) Fn::edge_split(recs, (int)(sl[r] & 0xffffu), (int)(sl[r] >> 16), pw[r], i, phis, a.pstride);
+        if (i < d.s)   // slots hold the placed record positions; bits 29-31 the Phi record's
+            Fn::edge_split(recs, (int)(sl[r] & 0xffffu), (int)((sl[r] >> 16) & 0x1fffu), pw[r],
+                           (i & ~7) | (int)(sl[r] >> 29), phis, a.pstride);
     }
     if constexpr (W > 0) {
         if (tid == 0) Fn::zero_split(phis, a.sentinel, a.pstride);
@@ -373,7 +380,7 @@ __global__ void EPG_OCC_BOUNDS(BLOCK) k_edge_occ(OccArgs a) {
         }
         if (j < d.nO) {
             float U[ROW];
-            Fn::rec_state_occ(recs, j, U);
+            Fn::rec_state_occ(recs, (j & ~7) | scol[j], U);
             Fn::finish_occ(U, acc, dtv[r], out[r]);
         } else {
 #pragma unroll
@@ -795,6 +802,33 @@ __global__ void k_build_blob3(const int32_t *__restrict__ peb, const int32_t *__
     }
     if (threadIdx.x == 0)
         desc[p] = PartDesc{o0, nO, e0, s, h0, nH, blob16[p], blob3_bytes_for(nH, s, L, W, hw), 0, 0, 0, 0};
+}
+
+// Apply the placement (place_kernels.cuh) to partition p of the plan: the occupancy kernel's slots
+// (record positions of both endpoints, bits 29-31 the in-group position of the edge's Phi
+// record), the blob's incidence entries (Phi positions) and its placement bytes.
+__global__ void k_apply_place(const PartDesc *__restrict__ desc, const uint32_t *__restrict__ slots,
+                              const uint8_t *__restrict__ vcol, const uint8_t *__restrict__ ecol, int W, int hw,
+                              int sentinel, unsigned char *blob, uint32_t *slots_occ) {
+    const PartDesc d = desc[blockIdx.x];
+    const int L = d.nO + d.nH;
+    const int64_t lb = (int64_t)d.o0 + d.h0;
+    const uint8_t *vc = vcol + lb, *ec = ecol + d.e0;
+    for (int i = threadIdx.x; i < d.s; i += blockDim.x) {
+        const uint32_t sl = slots[d.e0 + i];
+        const int a = (int)(sl & 0xffffu), b = (int)(sl >> 16);
+        const uint32_t pa = (uint32_t)((a & ~7) | vc[a]), pb = (uint32_t)((b & ~7) | vc[b]);
+        slots_occ[d.e0 + i] = pa | ((pb | ((uint32_t)ec[i] << 13)) << 16);
+    }
+    unsigned char *b0 = blob + 16 * (int64_t)d.blob16;
+    uint16_t *ic = reinterpret_cast<uint16_t *>(b0 + blob3_inc_offset(d.nH, hw));
+    const int ninc = W > 0 ? W * L : 2 * d.s;
+    for (int q = threadIdx.x; q < ninc; q += blockDim.x) {
+        const int e = ic[q], i = e >> 1;
+        if (i != sentinel) ic[q] = (uint16_t)((((i & ~7) | ec[i]) << 1) | (e & 1));
+    }
+    uint8_t *cb = b0 + blob3_col_offset(d.nH, d.s, L, W, hw);
+    for (int j = threadIdx.x; j < L; j += blockDim.x) cb[j] = vc[j];
 }
 
 __global__ void k_blob3_sizes(const int32_t *__restrict__ peb, const int32_t *__restrict__ pvb,

@@ -140,13 +140,13 @@ def test_pipelined_variant_one_plan_two_grids():
 def test_wide_cta_instance(cfg, P):
     """Partitions of 1025..1152 edges run on the 288-thread (9-warp) instance of the edge
     kernel (bench.py's SM-balanced C2 size P = 1032): growth-ordered EPG-RB map as in the
-    bench, exec limits (864 rows, 1152 edges); within the Z14 tolerance of the fp64 oracle,
+    bench, exec limits (1152 rows, 1152 edges); within the Z14 tolerance of the fp64 oracle,
     normwise and componentwise, and the same result through epg_run(steps=2) (graph) as
     through two one-step calls (direct launches)."""
     from paper_1605_02043_b200 import epg
     M = S.config_mesh(cfg)
     ctx = epg.Context(0)
-    ctx.set_exec_limits(864, 1152)
+    ctx.set_exec_limits(1152, 1152)
     E = dev(M.edges)
     part, rank, _ = ctx.partition_rb(E, M.n, P, ranked=True)
     k = epg.num_parts(M.m, P)

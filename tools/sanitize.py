@@ -8,6 +8,10 @@ Scenarios: the launch shapes the bench uses, at sizes the sanitizers finish in m
   default_map  C1 mesh, P = 1024, default (contiguous) map: halo-heavy partitions, late gather
   hub          R-MAT scale 14, gather-scatter, hub split on (red.global.add accumulators)
   spmv         2D 5-point stencil SpMV (bipartite graph), P = 1024
+  wide         C1 mesh, P = 1100: the 288-thread (9-warp) instance, single wave
+  sharded      C1 mesh, P = 1024, in-process group of 4: interior / boundary launches, exchange
+Every plan carries the bank-conflict placement (place.cpp) unless EPG_PLACE=0; the hub
+scenario's variable-length incidence lists take the segmented-scan reduce.
 Each checks its result against the fp64 oracle, so a run that the sanitizer perturbs
 into a wrong answer fails loudly too.
 """
@@ -35,6 +39,8 @@ def dev(a):
 def cfd(M, P, default_map=False):
     ctx = epg.Context(0)
     ctx.set_partition_method(2)
+    if P > 1024:
+        ctx.set_exec_limits(1152, 1152)
     k = epg.num_parts(M.m, P)
     E = dev(M.edges)
     part = ctx.default_partition(M.m, P) if default_map else ctx.partition(E, M.n, P)[0]
@@ -87,6 +93,40 @@ def spmv():
     assert np.array_equal(got, O.spmv(e, n, w, x))
 
 
+def sharded():
+    M = S.config_mesh("c1")
+    G, P = 4, 1024
+    ctxs = [epg.Context(0) for _ in range(G)]
+    k = epg.num_parts(M.m, P)
+    E = dev(M.edges)
+    part, rank, _ = ctxs[0].partition_rb(E, M.n, P, G, 8, ranked=True)
+    U, dt = S.cfd_state(M.n), S.cfd_dt(M.volume)
+    plans, states = [], []
+    for c in ctxs:
+        L, plan = c.remap(E, M.n, part, k, order_key=rank)
+        Un = c.permute_rows(dev(U), L.vertex_perm, epg.PERM_SCATTER)
+        nrm = c.permute_rows(dev(M.normals), L.edge_perm, epg.PERM_GATHER)
+        dtn = c.permute_rows(dev(dt), L.vertex_perm, epg.PERM_SCATTER)
+        plans.append(plan)
+        states.append((Un, torch.empty_like(Un), nrm, dtn, L))
+    epg.comm_init_local(ctxs)
+    epg.run_sharded_group(ctxs, plans, epg.KERNEL_CFD_FLUX, [s[:4] for s in states])
+    torch.cuda.synchronize()
+    ref, _ = O.cfd_step(M.edges, M.n, M.normals, U, dt)
+    vp = states[0][4].vertex_perm.cpu().numpy()
+    ref_l = np.empty_like(ref)
+    ref_l[vp] = ref                                   # the oracle's rows in the plan layout
+    err = 0.0
+    for g in range(G):   # each member's own (authoritative) rows
+        out = states[g][1]
+        r = ctxs[g].shard_ranges(plans[g], G, g)
+        lo, hi = r["vertex_first"], r["vertex_first"] + r["vertex_count"]
+        got = out[lo:hi].cpu().numpy().astype(np.float64)
+        err = max(err, (np.abs(got - ref_l[lo:hi]).max(axis=0) / np.abs(ref).max(axis=0)).max())
+    print(f"sharded G={G} k={k} err={err:.2e}")
+    assert err <= 1e-5
+
+
 def main(which):
     if which == "c1_single":
         cfd(S.config_mesh("c1"), 1024)
@@ -98,6 +138,10 @@ def main(which):
         hub()
     elif which == "spmv":
         spmv()
+    elif which == "wide":
+        cfd(S.config_mesh("c1"), 1100)
+    elif which == "sharded":
+        sharded()
     else:
         raise SystemExit(f"unknown scenario {which}")
     torch.cuda.synchronize()
