@@ -1,0 +1,23 @@
+#!/bin/bash
+# round-2 ncu evidence for the current build: C2 launch list (bench command), per-schedule
+# traffic (C2, C3), full captures of the edge kernel and finalise (C2, C3) exported to text
+mkdir -p gpurun_out
+OUT=gpurun_out
+M="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_srcunit_tex_op_read.sum,lts__t_sectors_srcunit_tex_op_write.sum,lts__t_sectors_srcunit_tex_op_atom.sum,lts__t_sectors_srcunit_tex_op_red.sum,lts__t_sectors_srcunit_tex.sum,sm__throughput.avg.pct_of_peak_sustained_elapsed,dram__throughput.avg.pct_of_peak_sustained_elapsed"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_c2.csv \
+    python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-comparators --no-c3 > $OUT/launches_c2.log 2>&1
+for CFG in c2 c3; do
+  V=rb,default,naive; [ $CFG = c3 ] && V=rb,default
+  timeout 1500 ncu --metrics $M --csv --log-file $OUT/variants_$CFG.csv -k regex:'^(k_edge_occ|k_finalise_rec|k_finalise3|k_naive_edges|k_naive_update)$' \
+      python tools/ncu_variants.py --config $CFG --reps 1 --variants $V > $OUT/variants_$CFG.log 2>&1
+  for K in edge fin; do
+    R='k_edge_occ'; [ $K = fin ] && R='^k_finalise_rec$'
+    timeout 1200 ncu --set full --clock-control none --import-source on -k regex:$R -c 1 -o $OUT/full_${K}_$CFG \
+        python tools/ncu_variants.py --config $CFG --reps 1 --variants rb > /dev/null 2>&1
+    ncu -i $OUT/full_${K}_$CFG.ncu-rep --page details > $OUT/details_${K}_$CFG.txt 2>&1
+    ncu -i $OUT/full_${K}_$CFG.ncu-rep --page raw --csv > $OUT/raw_${K}_$CFG.csv 2>&1
+    ncu -i $OUT/full_${K}_$CFG.ncu-rep --page source --csv --print-source sass > $OUT/sass_${K}_$CFG.csv 2>&1
+    gzip -f $OUT/raw_${K}_$CFG.csv $OUT/sass_${K}_$CFG.csv
+    rm -f $OUT/full_${K}_$CFG.ncu-rep
+  done
+done

@@ -36,6 +36,9 @@ def main():
     ap.add_argument("--part-size", type=int, default=1024)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--variants", default="0")
+    ap.add_argument("--rr", type=int, default=0,
+                    help="R > 0: trace the last step of 2R round-robin steps over R replicas (bench.py's "
+                         "headline mode: direct launches chained by PDL, inputs evicted) instead of one cold step")
     a = ap.parse_args()
     os.environ["EPG_LIB_PATH"] = build_trace_lib()
     sys.path.insert(0, ROOT)
@@ -54,9 +57,8 @@ def main():
     ctx = epg.Context(0)
     E = torch.from_numpy(M.edges).cuda()
     k = epg.num_parts(M.m, a.part_size)
-    ctx.set_partition_method(epg.PARTITION_EPG2)
-    part, _ = ctx.partition(E, M.n, a.part_size)
-    L, plan = ctx.remap(E, M.n, part, k)
+    part, rank, _ = ctx.partition_rb(E, M.n, a.part_size, ranked=True)   # the bench's map and order
+    L, plan = ctx.remap(E, M.n, part, k, order_key=rank)
     nrm = ctx.permute_rows(torch.from_numpy(M.normals).cuda(), L.edge_perm, epg.PERM_GATHER)
     dtn = ctx.permute_rows(torch.from_numpy(dt).cuda(), L.vertex_perm, epg.PERM_SCATTER)
     Un = ctx.permute_rows(torch.from_numpy(U).cuda(), L.vertex_perm, epg.PERM_SCATTER)
@@ -66,13 +68,32 @@ def main():
     nblk = min(plan.k_exec, 1024)
     epg.lib.epg_debug_trace_clear.restype = C.c_int
     runs = [(v, rep) for v in map(int, a.variants.split(",")) for rep in range(a.reps)]
+    reps = []
+    if a.rr:
+        for r in range(a.rr):
+            Lr, pr = ctx.remap(E, M.n, part, k, order_key=rank)
+            reps.append((pr, ctx.permute_rows(torch.from_numpy(U).cuda(), Lr.vertex_perm, epg.PERM_SCATTER),
+                         ctx.permute_rows(torch.from_numpy(M.normals).cuda(), Lr.edge_perm, epg.PERM_GATHER),
+                         ctx.permute_rows(torch.from_numpy(dt).cuda(), Lr.vertex_perm, epg.PERM_SCATTER)))
+        reps = [(pr, u, torch.empty_like(u), nr, dd) for pr, u, nr, dd in reps]
     for v, rep in runs:
         ctx.set_variant(v)
         torch.cuda.synchronize()
-        torch.cuda._sleep(2_000_000)               # keep the GPU busy while the host enqueues
-        flush.fill_(rep & 255)
-        ctx.run(plan, epg.KERNEL_CFD_FLUX, Un, out, nrm, dtn, 1)
-        torch.cuda.synchronize()
+        if a.rr:
+            for i in range(2 * a.rr):              # warm: every replica twice
+                pr, u, o, nr, dd = reps[i % a.rr]
+                ctx.run(pr, epg.KERNEL_CFD_FLUX, u, o, nr, dd, 1)
+            torch.cuda.synchronize()
+            torch.cuda._sleep(2_000_000)
+            for i in range(2 * a.rr):              # the traced stamps are those of the last launch
+                pr, u, o, nr, dd = reps[i % a.rr]
+                ctx.run(pr, epg.KERNEL_CFD_FLUX, u, o, nr, dd, 1)
+            torch.cuda.synchronize()
+        else:
+            torch.cuda._sleep(2_000_000)               # keep the GPU busy while the host enqueues
+            flush.fill_(rep & 255)
+            ctx.run(plan, epg.KERNEL_CFD_FLUX, Un, out, nrm, dtn, 1)
+            torch.cuda.synchronize()
         buf = np.zeros(1024 * niters * npts, dtype=np.uint64)
         epg.lib.epg_debug_trace(buf.ctypes.data, buf.size)
         buf = buf.astype(np.uint64)
