@@ -43,8 +43,11 @@ WORKLOADS = {
     "c4": "C4: R-MAT scale 24 (n = 16,777,216, m = 134,217,728, a = 0.57, b = c = 0.19), gather-scatter",
     "c5": "C5 per-GPU share: SpMV of a 2D 5-point Laplacian on a 3536^2 grid (12.5M rows, 62.5M nnz = 1/8 "
           "of the 500M-nnz 8-GPU config) as a bipartite COO data-affinity graph",
+    "c5full": "C5: SpMV of a 2D 5-point Laplacian on a 10,000^2 grid (1e8 rows, 499,960,000 nnz; BASELINE "
+              "configs[4]) as a bipartite COO data-affinity graph, sharded over the N GPUs",
 }
-FUNCTORS = {"c1": "cfd_flux", "c2": "cfd_flux", "c3": "cfd_flux", "c4": "gather_scatter", "c5": "spmv"}
+FUNCTORS = {"c1": "cfd_flux", "c2": "cfd_flux", "c3": "cfd_flux", "c4": "gather_scatter", "c5": "spmv",
+            "c5full": "spmv"}
 L2_MODE = ("inputs larger than L2: the timed steps cycle round-robin over R independent replicas of the "
            "workload (own plan, state, payload and constants each; R x working set >= 3 x L2), so every "
            "step's inputs were evicted by the others' traffic; per-step L2-flushed timing reported beside it")
@@ -72,8 +75,8 @@ class Workload:
             self.per_edge, self.per_vertex = 8, 8       # 8 B ids; 4 B x read, 4 B y write
             self.exec_rows = 1024                       # one-float rows (profiles/r01_c4_exec_sweep.txt)
             self.leaf_parts = 4096                      # EPG-RB: R 17.1 in 24 s (512: R 18.5 in 14 s)
-        elif config == "c5":
-            self.n, self.edges, w = S.stencil2d_spmv(3536)
+        elif config in ("c5", "c5full"):
+            self.n, self.edges, w = S.stencil2d_spmv(3536 if config == "c5" else 10000)
             self.m = self.edges.shape[0]
             N = self.n // 2
             self.kernel, self.functor = 3, "spmv"
@@ -109,7 +112,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=["c1", "c2", "c3", "c4", "c5"], default=None,
+    ap.add_argument("--config", choices=["c1", "c2", "c3", "c4", "c5", "c5full"], default=None,
                     help="workload (default: c2 on one GPU, c3 with --gpus N > 1)")
     ap.add_argument("--part-size", type=int, default=1024,
                     help="edges per EP partition (1025..1152: the 288-thread instance of the edge kernel)")
@@ -912,6 +915,8 @@ def main():
     if args.config is None:
         # N = 1: BASELINE configs[1] (C2, the headline); N > 1: configs[2] (C3 across GPUs)
         args.config = "c2" if world == 1 and args.gpus == 1 else "c3"
+    if args.config == "c5" and (world > 1 or args.gpus > 1):
+        args.config = "c5full"   # N > 1: the 500M-nnz SpMV of BASELINE configs[4] (c5 is its one-GPU share)
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

@@ -84,18 +84,25 @@ def rmat(scale: int, edge_factor: int = 8, seed: int = 1607, a=0.57, b=0.19, c=0
     return n, out
 
 
-def stencil2d_spmv(g: int):
+def stencil2d_spmv(g: int, chunk_rows: int = 1 << 22):
     """2D 5-point Laplacian on a g x g grid as the bipartite data-affinity graph of SpMV
     (P:859-861): vertices 0..N-1 are x_j (columns), N..2N-1 are y_i (rows), one edge
-    (j, N + i) per nonzero A[i, j] in row-major (CUSP) order; values 4 / -1."""
+    (j, N + i) per nonzero A[i, j] in row-major (CUSP) order; values 4 / -1.
+    Row i's nonzeros sit in columns i - g, i - 1, i, i + 1, i + g (ascending), so row-major
+    order needs no sort; built in chunks of rows (g = 10,000: 499,960,000 nonzeros)."""
     N = g * g
-    i = np.arange(N, dtype=np.int64)
-    r, c = i // g, i % g
-    cols, vals, rows = [], [], []
-    for dr, dc, val in ((-1, 0, -1.0), (0, -1, -1.0), (0, 0, 4.0), (0, 1, -1.0), (1, 0, -1.0)):
-        ok = (r + dr >= 0) & (r + dr < g) & (c + dc >= 0) & (c + dc < g)
-        rows.append(i[ok]); cols.append((i + dr * g + dc)[ok]); vals.append(np.full(int(ok.sum()), val, np.float32))
-    rows = np.concatenate(rows); cols = np.concatenate(cols); vals = np.concatenate(vals)
-    order = np.lexsort((cols, rows))
-    edges = np.stack([cols[order], N + rows[order]], axis=1).astype(np.int32)
-    return 2 * N, edges, vals[order]
+    offs = np.array([-g, -1, 0, 1, g], np.int64)
+    vals5 = np.array([-1.0, -1.0, 4.0, -1.0, -1.0], np.float32)
+    ok_r = np.array([[-1, 0], [0, -1], [0, 0], [0, 1], [1, 0]], np.int64)
+    parts_e, parts_v = [], []
+    for i0 in range(0, N, chunk_rows):
+        i = np.arange(i0, min(N, i0 + chunk_rows), dtype=np.int64)
+        r, c = i // g, i % g
+        ok = np.ones((i.size, 5), bool)
+        for q, (dr, dc) in enumerate(ok_r):
+            ok[:, q] = (r + dr >= 0) & (r + dr < g) & (c + dc >= 0) & (c + dc < g)
+        cols = (i[:, None] + offs[None, :])[ok]
+        rows = np.broadcast_to(i[:, None], (i.size, 5))[ok]
+        parts_e.append(np.stack([cols, N + rows], axis=1).astype(np.int32))
+        parts_v.append(np.broadcast_to(vals5[None, :], (i.size, 5))[ok])
+    return 2 * N, np.concatenate(parts_e), np.concatenate(parts_v)
