@@ -675,6 +675,7 @@ __global__ void k_finalise_rec(const int4 *__restrict__ recs, const float *__res
             }
         }
         Fn::finalise_add(state_out + Fn::ROW * v, acc, dt);
+        EPG_TP(14, 2);
         return;
     }
     const int64_t v = touched + (t - S);

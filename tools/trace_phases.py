@@ -109,6 +109,8 @@ def main():
             d = (col - base) / 1e3
             print(f"  pt{pt}: n={col.size:4d}  min {d.min():7.2f}  p10 {np.percentile(d, 10):7.2f}  "
                   f"p50 {np.percentile(d, 50):7.2f}  p90 {np.percentile(d, 90):7.2f}  max {d.max():7.2f} us")
+        last_edge = t[:, 6][t[:, 6] > 0].max() if (t[:, 6] > 0).any() else base
+        print(f"  last edge CTA done at {(last_edge - base) / 1e3:7.2f} us")
         fin = buf.reshape(1024, niters, npts)[:, 14, :3].astype(np.int64)
         fin = fin[fin[:, 0] > 0]
         if fin.size:
