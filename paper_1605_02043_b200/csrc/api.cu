@@ -110,6 +110,8 @@ struct epg_plan {
     unsigned char *blob3 = nullptr;
     int blob3_max = 0;
     int4 *fin_recs = nullptr;   // packed finalise records (when every vertex has <= 6 halo entries)
+    int4 *fin_rec16 = nullptr;  // ... as 16-byte records {v, count, h0, h1 or overflow index}
+    int32_t *fin_over = nullptr;   // ... and the entries h1..h5 of the vertices with > 2
     int32_t *heavy = nullptr;   // shared vertices with more than kBlockHalo halo entries
     int64_t n_heavy = 0;
     int32_t *medium = nullptr;  // shared vertices with (kHeavyHalo, kBlockHalo] halo entries
@@ -493,6 +495,26 @@ epg_status build_pipeline_blob(epg_ctx *ctx, epg_plan *pl) {
             if ((st = read_i32(ctx, hm.as<int32_t>(), &hmax)) || (st = read_i32(ctx, hm.as<int32_t>() + 1, &nhub)))
                 return st;
             if (hmax > 6) pl->fin_recs = nullptr;   // (the allocation is released with the plan)
+            const char *r16 = std::getenv("EPG_FIN_REC16");
+            if (pl->fin_recs && !(r16 && std::atoi(r16) == 0)) {   // 16-byte records, same order
+                Tmp flag(ctx), pos(ctx);
+                CU(flag.alloc(sizeof(int32_t) * (pl->S + 1)));
+                CU(pos.alloc(sizeof(int32_t) * (pl->S + 1)));
+                CU(cudaMemsetAsync(flag.p, 0, sizeof(int32_t) * (pl->S + 1), ctx->stream));
+                k_rec16_flags<<<grid_for(pl->S), kThreads, 0, ctx->stream>>>(pl->fin_recs, (int32_t)pl->S,
+                                                                            flag.as<int32_t>());
+                if ((st = exclusive_scan(ctx, flag.as<int32_t>(), pos.as<int32_t>(), pl->S + 1))) return st;
+                int32_t nov = 0;
+                if ((st = read_i32(ctx, pos.as<int32_t>() + pl->S, &nov))) return st;
+                if ((st = plan_alloc_t(pl, ctx, &pl->fin_rec16, pl->S)) ||
+                    (st = plan_alloc_t(pl, ctx, &pl->fin_over, 5 * std::max<int64_t>(nov, 1))))
+                    return st;
+                k_rec16_build<<<grid_for(pl->S), kThreads, 0, ctx->stream>>>(pl->fin_recs, (int32_t)pl->S,
+                                                                            pos.as<int32_t>(), pl->fin_rec16,
+                                                                            pl->fin_over);
+                CHECK_LAUNCH();
+                CU(cudaStreamSynchronize(ctx->stream));
+            }
             pl->finalise_skip = nhub > 0 ? std::min(kHeavyHalo, pl->hub_min - 1) : kHeavyHalo;
             if (hmax > kHeavyHalo || nhub > 0) {    // list medium / heavy vertices and hubs on the host
                 std::vector<int32_t> off(pl->S + 1), hv, md, hubs, hub_of_s;
@@ -855,7 +877,12 @@ epg_status launch_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t step
         ctx->prof_end(0, t0);
         if (fin_work > 0) {
             cudaEvent_t t1 = ctx->prof_begin();
-            if (pl->fin_recs)
+            if (pl->fin_rec16)
+                CU(launch_pdl(k_finalise_rec16<Fn>, grid_for(fin_work), kThreads, 0, ctx->stream,
+                              (const int4 *)pl->fin_rec16, (const int32_t *)pl->fin_over,
+                              (const float *)pl->halo_buf, (const float *)a.state_in, a.state_out, a.vconst,
+                              (int32_t)pl->S, pl->touched, pl->n));
+            else if (pl->fin_recs)
                 CU(launch_pdl(k_finalise_rec<Fn>, grid_for(fin_work), kThreads, 0, ctx->stream,
                               (const int4 *)pl->fin_recs, (const float *)pl->halo_buf, (const float *)a.state_in,
                               a.state_out, a.vconst, (int32_t)pl->S, pl->touched, pl->n));

@@ -28,9 +28,22 @@ struct CfdVertex {
     float rho, mx, my, mz, E, p, speed, rinv;  // speed = |u| + c, rinv = 1 / rho
 };
 
+// MUFU reciprocal square root / reciprocal, flush-to-zero forms: rsqrtf / __fdividef add a
+// denormal range check and rescale around the MUFU op (an FSETP and a predicated FMUL each);
+// the staged values are never denormal (densities, energies, squared speeds and face areas)
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_ftz(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 // sqrt(x) for x >= 0 through the MUFU reciprocal square root (no IEEE fix-up branch);
 // relative error ~1e-7, far inside the 1e-5 parity tolerance
-__device__ __forceinline__ float sqrt_nb(float x) { return x > 0.0f ? x * rsqrtf(x) : 0.0f; }
+__device__ __forceinline__ float sqrt_nb(float x) { return x > 0.0f ? x * rsqrt_ftz(x) : 0.0f; }
 
 __device__ __forceinline__ CfdVertex cfd_derive(float rho, float mx, float my, float mz, float E) {
     CfdVertex d;
@@ -192,7 +205,7 @@ struct CfdFlux {
     // (rho, m_x), (m_y, m_z), (E, p'): ~32 FP instructions per edge instead of ~47.
     __device__ __forceinline__ static void derive_occ(const float *row, float *recs, int j) {
         const float rho = row[0], mx = row[1], my = row[2], mz = row[3], E = row[4];
-        const float rinv = __fdividef(1.0f, rho);
+        const float rinv = rcp_ftz(rho);
         const float ux = mx * rinv, uy = my * rinv, uz = mz * rinv;
         const float uu = ux * ux + uy * uy + uz * uz;
         const float p = (kGamma - 1.0f) * (E - 0.5f * rho * uu);

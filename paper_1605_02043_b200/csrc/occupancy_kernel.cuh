@@ -150,11 +150,21 @@ __global__ void EPG_OCC_BOUNDS(BLOCK) k_edge_occ(OccArgs a) {
     if (a.early_pdl) ptx::pdl_launch_dependents();
     if (tid == 0) region_bulk(rows_base, g_rows, rows_bytes, &bar);
     // 5-float rows: every halo row lands as the aligned 32 bytes that contain it (two 16-byte
-    // cp.async, L1 bypassed) in a slot of its own after the owned rows; the row sits at byte
-    // 4 (h mod 4) of the slot (20 h mod 16). One-float rows are gathered word by word.
+    // cp.async, L1 bypassed) after the owned rows, the row at byte 4 (h mod 4) of the 32 (20 h
+    // mod 16). The two 16-byte halves of halo row j go to halo_lo + 16 j and halo_hi + 16 j, so
+    // a warp quarter's cp.async writes are 16-byte contiguous (a 32-byte slot per row made
+    // lanes l and l + 4 collide on one bank group). One-float rows are gathered word by word.
+    // (Per-thread 32-byte TMA bulk copies instead were measured slower: a bulk copy takes
+    // uniform operands, so a divergent per-lane issue becomes a loop -- C3 8,469 -> 10,035
+    // warp instructions per CTA, edge kernel 1.41 -> 1.61 ms.)
     constexpr bool kChunked = ROW == 5;
-    unsigned char *halo_slots = reinterpret_cast<unsigned char *>(
+    unsigned char *halo_lo = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(rows + ROW * d.nO) + 15) & ~uintptr_t(15));
+    unsigned char *halo_hi = halo_lo + 16 * d.nH;
+    // word p (0..7) of halo row j's 32-byte window
+    auto halo_word = [&](int j, int p) -> float * {
+        return reinterpret_cast<float *>((p < 4 ? halo_lo : halo_hi) + 16 * j) + (p & 3);
+    };
     auto gather_halo = [&]() {
         float *hr = rows + ROW * d.nO;
 #pragma unroll
@@ -164,14 +174,13 @@ __global__ void EPG_OCC_BOUNDS(BLOCK) k_edge_occ(OccArgs a) {
                 const float *src = a.state_in + (int64_t)ROW * hid[r];
                 if constexpr (kChunked) {
                     const float *base = reinterpret_cast<const float *>(reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15));
-                    unsigned char *dst = halo_slots + 32 * j;
                     if (base + 8 <= a.state_end) {
-                        ptx::cp_async16(dst, base);
-                        ptx::cp_async16(dst + 16, base + 4);
+                        ptx::cp_async16(halo_lo + 16 * j, base);
+                        ptx::cp_async16(halo_hi + 16 * j, base + 4);
                     } else {                            // the array's last row: no read past its end
-                        float *d4 = reinterpret_cast<float *>(dst) + (src - base);
+                        const int p0 = (int)(src - base);
 #pragma unroll
-                        for (int c = 0; c < ROW; c++) ptx::cp_async4(d4 + c, src + c);
+                        for (int c = 0; c < ROW; c++) ptx::cp_async4(halo_word(j, p0 + c), src + c);
                     }
                 } else {
 #pragma unroll
@@ -244,15 +253,14 @@ __global__ void EPG_OCC_BOUNDS(BLOCK) k_edge_occ(OccArgs a) {
         const int j = tid + r * BLOCK;
         if (j < L) {
             const float *row = rows + ROW * j;
-            if constexpr (kChunked) {
-                if (j >= d.nO) {
-                    const int jh = j - d.nO;
-                    row = reinterpret_cast<const float *>(halo_slots + 32 * jh) +
-                          (reinterpret_cast<const int32_t *>(sblob)[jh] & 3);
-                }
-            }
+            if (kChunked && j >= d.nO) {
+                const int jh = j - d.nO, p0 = reinterpret_cast<const int32_t *>(sblob)[jh] & 3;
 #pragma unroll
-            for (int c = 0; c < ROW; c++) rv[r][c] = row[c];
+                for (int c = 0; c < ROW; c++) rv[r][c] = *halo_word(jh, p0 + c);
+            } else {
+#pragma unroll
+                for (int c = 0; c < ROW; c++) rv[r][c] = row[c];
+            }
         }
     }
     __syncthreads();
@@ -680,6 +688,75 @@ __global__ void k_finalise_rec(const int4 *__restrict__ recs, const float *__res
     }
     const int64_t v = touched + (t - S);
     if (v < n) Fn::untouched(state_in + Fn::ROW * v, state_out + Fn::ROW * v);
+}
+
+// Finalise from 16-byte records {v, count, h0, x}: x = h1 when count <= 2, else the index of
+// the vertex's entries h1..h5 in `over` (5 ints each). Same vertices, order and summation as
+// k_finalise_rec, with half its record bytes (the C3 finalise is DRAM-bound and the 32-byte
+// records were ~30 % of its traffic; most shared vertices of a mesh have one or two entries).
+template <class Fn>
+__global__ void k_finalise_rec16(const int4 *__restrict__ recs, const int32_t *__restrict__ over,
+                                 const float *__restrict__ halo_buf, const float *__restrict__ state_in,
+                                 float *__restrict__ state_out, const float *__restrict__ vconst, int32_t S,
+                                 int64_t touched, int64_t n) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    // records, overflow entries and dt are plan / constant data: loaded before the wait
+    int4 r = make_int4(0, -1, 0, 0);
+    int h[6] = {0, 0, 0, 0, 0, 0};
+    float dt = 0.0f;
+    if (t < S) {
+        r = recs[t];
+        h[0] = r.z;
+        if (r.y > 2) {
+            const int32_t *o = over + 5 * (int64_t)r.w;
+#pragma unroll
+            for (int i = 1; i < 6; i++) h[i] = o[i - 1];
+        } else {
+            h[1] = r.w;
+        }
+        if (Fn::kUsesConst && r.y >= 0) dt = vconst[r.x];
+    }
+    ptx::pdl_wait();
+    ptx::pdl_launch_dependents();
+    if (t < S) {
+        const int64_t v = r.x;
+        const int c = r.y;
+        if (c < 0) return;                         // a hub: k_finalise_hub's vertex
+        float acc[Fn::ROW];
+#pragma unroll
+        for (int k = 0; k < Fn::ROW; k++) acc[k] = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 6; i++) {
+            if (i < c) {
+#pragma unroll
+                for (int k = 0; k < Fn::ROW; k++) acc[k] += halo_buf[Fn::ROW * (int64_t)h[i] + k];
+            }
+        }
+        Fn::finalise_add(state_out + Fn::ROW * v, acc, dt);
+        return;
+    }
+    const int64_t v = touched + (t - S);
+    if (v < n) Fn::untouched(state_in + Fn::ROW * v, state_out + Fn::ROW * v);
+}
+
+// 16-byte records from the 32-byte ones: over_flag[t] = count > 2 (scanned into positions)
+__global__ void k_rec16_flags(const int4 *__restrict__ recs, int32_t S, int32_t *flag) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < S) flag[t] = recs[2 * t].y > 2 ? 1 : 0;
+}
+__global__ void k_rec16_build(const int4 *__restrict__ recs, int32_t S, const int32_t *__restrict__ pos,
+                              int4 *rec16, int32_t *over) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= S) return;
+    const int4 r0 = recs[2 * t], r1 = recs[2 * t + 1];
+    if (r0.y > 2) {
+        const int32_t p = pos[t];
+        rec16[t] = make_int4(r0.x, r0.y, r0.z, p);
+        int32_t *o = over + 5 * (int64_t)p;
+        o[0] = r0.w; o[1] = r1.x; o[2] = r1.y; o[3] = r1.z; o[4] = r1.w;
+    } else {
+        rec16[t] = make_int4(r0.x, r0.y, r0.z, r0.w);
+    }
 }
 
 // records for k_finalise_rec; *hmax receives the largest halo count of a non-hub vertex

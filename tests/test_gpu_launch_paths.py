@@ -171,3 +171,40 @@ def test_wide_cta_instance(cfg, P):
     c, d = Un.clone(), torch.empty_like(Un)
     two = ctx.run(plan, epg.KERNEL_CFD_FLUX, c, d, nrm, dtn, 2)
     assert np.array_equal(a.cpu().numpy(), two.cpu().numpy())
+
+
+@pytest.mark.parametrize("cfg,P", [("c1", 1024), ("c1", 256)])
+def test_plan_options_bitexact(cfg, P):
+    """Execution-plan choices that must not change a single result bit (include/epg.h):
+    the bank-conflict-aware record placement (EPG_PLACE=0: identity positions) and the 16-byte
+    finalise records (EPG_FIN_REC16=0: the 32-byte records) -- each plan built under the option,
+    two cfd steps, compared bit for bit with the default plan; and the default within the Z14
+    tolerance of the fp64 oracle."""
+    from paper_1605_02043_b200 import epg
+    M = S.config_mesh(cfg)
+    U, dt = S.cfd_state(M.n), S.cfd_dt(M.volume)
+    E = dev(M.edges)
+    ctx = epg.Context(0)
+    part, rank, _ = ctx.partition_rb(E, M.n, P, ranked=True)
+    k = epg.num_parts(M.m, P)
+
+    def run(env):
+        olds = {kk: _env(kk, vv) for kk, vv in env.items()}
+        try:
+            L, plan = ctx.remap(E, M.n, part, k, order_key=rank)
+        finally:
+            for kk, vv in olds.items():
+                _env(kk, vv)
+        Un = ctx.permute_rows(dev(U), L.vertex_perm, epg.PERM_SCATTER)
+        nrm = ctx.permute_rows(dev(M.normals), L.edge_perm, epg.PERM_GATHER)
+        dtn = ctx.permute_rows(dev(dt), L.vertex_perm, epg.PERM_SCATTER)
+        out = ctx.run(plan, epg.KERNEL_CFD_FLUX, Un, torch.empty_like(Un), nrm, dtn, 2)
+        return ctx.permute_rows(out, L.vertex_perm, epg.PERM_GATHER).cpu().numpy()
+
+    base = run({})
+    assert np.array_equal(base, run({"EPG_PLACE": "0"}))
+    assert np.array_equal(base, run({"EPG_FIN_REC16": "0"}))
+    ref, _ = O.cfd_step(M.edges, M.n, M.normals, U, dt)
+    ref2, _ = O.cfd_step(M.edges, M.n, M.normals, ref.astype(np.float32), dt)
+    err = np.abs(base - ref2).max(axis=0) / np.abs(ref2).max(axis=0)
+    assert err.max() <= 2e-5
