@@ -243,6 +243,12 @@ epg_status epg_load_count(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t
  * see epg_layout) and creates *plan: the device descriptors of the staged kernel
  * (per-partition incidence lists, shared-vertex lists, accumulators). Requires every
  * partition to have at most EPG_MAX_PART_SIZE edges.
+ * The plan also fixes where each partition's staged records live in shared memory: a
+ * record (and an edge's Phi record) may take any position of its aligned group of 8, and a
+ * greedy pass (one warp per partition) picks the positions so that the 128-bit shared loads
+ * of a warp quarter hit distinct bank groups; EPG_PLACE=0 keeps the identity. The boundary
+ * finalise reads 16-byte records {v, count, h0, h1 | overflow index} (EPG_FIN_REC16=0: the
+ * 32-byte records). Neither changes a result bit (same values, same summation orders).
  *   edges [m][2] DEVICE (original task order); part_of_edge [m] DEVICE. */
 epg_status epg_remap(epg_ctx *ctx, const int32_t *edges, int64_t m, int32_t n_vertices,
                      const int32_t *part_of_edge, int64_t k, epg_layout *layout, epg_plan **plan);

@@ -1,5 +1,6 @@
 """Checks of the synthetic input generators (inputs only; no method arithmetic)."""
 import numpy as np
+import pytest
 
 import synth as S
 from synth.mesh import _faces, PERMS
@@ -70,3 +71,25 @@ def test_config_sizes():
     U = S.cfd_state(M2.n)
     p = 0.4 * (U[:, 4] - 0.5 * (U[:, 1:4] ** 2).sum(1) / U[:, 0])
     assert p.min() > 0.8
+
+
+@pytest.mark.parametrize("g", [1, 2, 3, 7, 40])
+def test_stencil_spmv_brute_force(g):
+    """The SpMV input (C5): the 2D 5-point Laplacian on a g x g grid as a bipartite COO graph in
+    row-major order -- compared with a dense construction, for every chunk size."""
+    N = g * g
+    A = np.zeros((N, N), np.float32)
+    for i in range(N):
+        r, c = divmod(i, g)
+        A[i, i] = 4.0
+        for dr, dc in ((-1, 0), (0, -1), (0, 1), (1, 0)):
+            if 0 <= r + dr < g and 0 <= c + dc < g:
+                A[i, (r + dr) * g + (c + dc)] = -1.0
+    rows, cols = np.nonzero(A)                       # row-major, columns ascending
+    for chunk in (1, 5, 1 << 22):
+        n, e, w = S.stencil2d_spmv(g, chunk_rows=chunk)
+        assert n == 2 * N
+        assert np.array_equal(e[:, 0], cols) and np.array_equal(e[:, 1], N + rows)
+        assert np.array_equal(w, A[rows, cols])
+    if g == 40:
+        assert len(e) == 5 * N - 4 * g             # 499,960,000 at g = 10,000 (SURVEY §8(d) C5)
