@@ -8,10 +8,10 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-comparators --no-c3 > $OUT/launches_c2.log 2>&1
 for CFG in c2 c3; do
   V=rb,default,naive; [ $CFG = c3 ] && V=rb,default
-  timeout 1500 ncu --metrics $M --csv --log-file $OUT/variants_$CFG.csv -k regex:'^(k_edge_occ|k_finalise_rec|k_finalise3|k_naive_edges|k_naive_update)$' \
+  timeout 1500 ncu --metrics $M --csv --log-file $OUT/variants_$CFG.csv -k regex:'^(k_edge_occ|k_finalise_rec|k_finalise_rec16|k_finalise3|k_naive_edges|k_naive_update)$' \
       python tools/ncu_variants.py --config $CFG --reps 1 --variants $V > $OUT/variants_$CFG.log 2>&1
   for K in edge fin; do
-    R='k_edge_occ'; [ $K = fin ] && R='^k_finalise_rec$'
+    R='k_edge_occ'; [ $K = fin ] && R='^k_finalise_rec16$'
     timeout 1200 ncu --set full --clock-control none --import-source on -k regex:$R -c 1 -o $OUT/full_${K}_$CFG \
         python tools/ncu_variants.py --config $CFG --reps 1 --variants rb > /dev/null 2>&1
     ncu -i $OUT/full_${K}_$CFG.ncu-rep --page details > $OUT/details_${K}_$CFG.txt 2>&1

@@ -65,7 +65,8 @@ def main():
         us = v / 1000.0 if unit == "ns" else (v if unit == "us" else v * 1000.0)
         per.setdefault(short(r["Kernel Name"]), []).append(us)
     tot = sum(sum(v) for v in per.values())
-    step = {k: v for k, v in per.items() if k.split("<")[0] in ("k_edge_occ", "k_finalise_rec", "k_finalise3")}
+    step = {k: v for k, v in per.items() if k.split("<")[0] in ("k_edge_occ", "k_finalise_rec", "k_finalise_rec16",
+                                                                "k_finalise3")}
     step_tot = sum(statistics.median(v) for v in step.values()) or 1.0
     if not per:
         per = {}
@@ -81,7 +82,7 @@ def main():
     kern = {}
     order = []
     step_kernels = ("k_edge_occ", "k_edge_tma", "k_edge_staged", "k_naive_edges", "k_naive_update",
-                    "k_finalise_rec", "k_finalise3", "k_finalise")
+                    "k_finalise_rec", "k_finalise_rec16", "k_finalise3", "k_finalise")
     for r in rows:
         base = short(r["Kernel Name"]).split("<")[0]
         if base not in step_kernels:
