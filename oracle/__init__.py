@@ -59,7 +59,8 @@ def lib():
             "orc_cfd_flux": (None, [P, i64, i32, P, P, P]),
             "orc_cfd_flux_abs": (None, [P, i64, i32, P, P, P]),
             "orc_cfd_step": (None, [P, i64, i32, P, P, P, P, P]),
-            "orc_cfd_step_omp": (C.c_int, [P, i64, i32, P, P, P, P, P]),
+            "orc_cfd_step_omp": (C.c_int, [P, i64, i32, P, P, P, P, P, P, P]),
+            "orc_incidence": (None, [P, i64, i32, P, P]),
             "orc_gather_scatter": (None, [P, i64, i32, P, P, P]),
             "orc_spmv": (None, [P, i64, i32, P, P, P]),
             "orc_partition_random": (C.c_int, [i64, i32, C.c_uint64, P]),
@@ -286,15 +287,27 @@ def cfd_step(edges, n: int, normals, U, dt):
     return Uout, F
 
 
-def cfd_step_omp(edges, n: int, normals, U, dt):
-    """orc_cfd_step over all host cores (CPU-baseline timing only) -> (U', F, threads)."""
+def incidence(edges, n: int):
+    """orc_incidence: per-vertex (edge, side) lists, ascending edge -> (off [n+1], inc [2m])."""
+    e, m = _edges(edges)
+    off = np.zeros(n + 1, np.int64)
+    inc = np.zeros(max(2 * m, 1), np.int64)
+    lib().orc_incidence(_p(e), m, n, _p(off), _p(inc))
+    return off, inc
+
+
+def cfd_step_omp(edges, n: int, normals, U, dt, inc=None):
+    """orc_cfd_step over all host cores (CPU-baseline timing only; bit-identical to cfd_step)
+    -> (U', F, threads). inc: incidence(edges, n), built once per mesh, or None."""
     e, m = _edges(edges)
     Uout = np.zeros((n, 5), np.float64)
     F = np.zeros((n, 5), np.float64)
     normals = np.ascontiguousarray(normals, np.float32)
     U = np.ascontiguousarray(U, np.float32)
     dt = np.ascontiguousarray(dt, np.float32)
-    th = lib().orc_cfd_step_omp(_p(e), m, n, _p(normals), _p(U), _p(dt), _p(Uout), _p(F))
+    off, ic = (None, None) if inc is None else inc
+    th = lib().orc_cfd_step_omp(_p(e), m, n, _p(normals), _p(U), _p(dt), _p(Uout), _p(F),
+                                _p(off) if off is not None else None, _p(ic) if ic is not None else None)
     return Uout, F, int(th)
 
 

@@ -852,62 +852,80 @@ void orc_cfd_step(const int32_t *edges, int64_t m, int32_t n, const float *norma
     free(touched);
 }
 
-/* The same time step over all host cores, for the CPU baseline's timing only (SURVEY    */
-/* 8(d): "OpenMP over all host cores. Per-thread private accumulators are used"): the    */
-/* edges are split into contiguous ranges, each thread accumulates orc_cfd_flux's Phi of  */
-/* its range into a private F, the private arrays are summed, then U' = U + dt F. Same    */
-/* arithmetic per edge as orc_cfd_flux; only the summation order of F differs. Returns    */
-/* the thread count used (1 when built without OpenMP).                                  */
+/* The same time step over all host cores, for the CPU baseline's timing only (SURVEY      */
+/* 8(d) asks for the oracle "OpenMP over all host cores"). Vertex-centric: an incidence list */
+/* per vertex (its (edge, side) slots in ascending edge order) is built once per call, and   */
+/* each thread sums, for its vertices, the Phi of every incident edge -- evaluated with      */
+/* orc_cfd_flux's expression -- with the sign of the vertex's side. Each edge is evaluated  */
+/* twice (once per endpoint), but a vertex's terms are added in the order orc_cfd_flux adds  */
+/* them (ascending edge; for a self-loop +Phi then -Phi), so the result is bit-identical to  */
+/* orc_cfd_step, with no shared accumulators. (SURVEY's per-thread private accumulators were */
+/* the first version: 16 x n x 5 doubles zeroed and summed every step made it slower than    */
+/* one thread on C2.) Returns the thread count used (1 when built without OpenMP).          */
+static void cfd_edge_phi(const int32_t *edges, const float *normals, const float *U, int64_t e, double phi[5]) {
+    int32_t a = edges[2 * e], b = edges[2 * e + 1];
+    double nv[3] = {normals[3 * e], normals[3 * e + 1], normals[3 * e + 2]};
+    double Ua[5], Ub[5], ua[3], ub[3], pa, pb, ca, cb, sa, sb, Ga[5], Gb[5];
+    cfd_vertex(U + 5 * (int64_t)a, Ua, ua, &pa, &ca, &sa);
+    cfd_vertex(U + 5 * (int64_t)b, Ub, ub, &pb, &cb, &sb);
+    cfd_flux_dot(Ua, ua, pa, nv, Ga);
+    cfd_flux_dot(Ub, ub, pb, nv, Gb);
+    double nlen = sqrt(nv[0] * nv[0] + nv[1] * nv[1] + nv[2] * nv[2]);
+    double f = -nlen * ORC_SIGMA * 0.5 * (sa + sb + ca + cb);
+    for (int j = 0; j < 5; j++) phi[j] = f * (Ua[j] - Ub[j]) - 0.5 * (Ga[j] + Gb[j]);
+}
+
+/* incidence lists of the vertex-centric step: off [n+1], inc [2m] = 2 e + side, ascending e */
+void orc_incidence(const int32_t *edges, int64_t m, int32_t n, int64_t *off, int64_t *inc) {
+    for (int64_t v = 0; v <= n; v++) off[v] = 0;
+    for (int64_t e = 0; e < m; e++) { off[edges[2 * e] + 1]++; off[edges[2 * e + 1] + 1]++; }
+    for (int64_t v = 0; v < n; v++) off[v + 1] += off[v];
+    int64_t *pos = (int64_t *)malloc(sizeof(int64_t) * ((size_t)n + 1));
+    memcpy(pos, off, sizeof(int64_t) * ((size_t)n + 1));
+    for (int64_t e = 0; e < m; e++) {                /* ascending e; side 0 before side 1 */
+        inc[pos[edges[2 * e]]++] = 2 * e;
+        inc[pos[edges[2 * e + 1]]++] = 2 * e + 1;
+    }
+    free(pos);
+}
+
+/* off / inc: orc_incidence's lists (built once per mesh by the caller, like the GPU path's
+   plan), or NULL to build them here */
 int orc_cfd_step_omp(const int32_t *edges, int64_t m, int32_t n, const float *normals, const float *U,
-                     const float *dt, double *Uout, double *F) {
+                     const float *dt, double *Uout, double *F, const int64_t *off_in, const int64_t *inc_in) {
     int nth = 1;
 #ifdef _OPENMP
     nth = omp_get_max_threads();
 #endif
-    double *priv = (double *)calloc((size_t)nth * (size_t)n * 5, sizeof(double));
-    unsigned char *touched = (unsigned char *)calloc((size_t)n, 1);
-#ifdef _OPENMP
-#pragma omp parallel num_threads(nth)
-#endif
-    {
-        int tid = 0;
-#ifdef _OPENMP
-        tid = omp_get_thread_num();
-#endif
-        double *Fp = priv + (size_t)tid * (size_t)n * 5;
-        int64_t e0 = m * tid / nth, e1 = m * (tid + 1) / nth;
-        for (int64_t e = e0; e < e1; e++) {
-            int32_t a = edges[2 * e], b = edges[2 * e + 1];
-            double nv[3] = {normals[3 * e], normals[3 * e + 1], normals[3 * e + 2]};
-            double Ua[5], Ub[5], ua[3], ub[3], pa, pb, ca, cb, sa, sb, Ga[5], Gb[5];
-            cfd_vertex(U + 5 * (int64_t)a, Ua, ua, &pa, &ca, &sa);
-            cfd_vertex(U + 5 * (int64_t)b, Ub, ub, &pb, &cb, &sb);
-            cfd_flux_dot(Ua, ua, pa, nv, Ga);
-            cfd_flux_dot(Ub, ub, pb, nv, Gb);
-            double nlen = sqrt(nv[0] * nv[0] + nv[1] * nv[1] + nv[2] * nv[2]);
-            double f = -nlen * ORC_SIGMA * 0.5 * (sa + sb + ca + cb);
-            for (int j = 0; j < 5; j++) {
-                double phi = f * (Ua[j] - Ub[j]) - 0.5 * (Ga[j] + Gb[j]);
-                Fp[5 * (int64_t)a + j] += phi;
-                Fp[5 * (int64_t)b + j] -= phi;
-            }
-            touched[a] = 1;
-            touched[b] = 1;
-        }
+    int64_t *own_off = NULL, *own_inc = NULL;
+    const int64_t *off = off_in, *inc = inc_in;
+    if (!off || !inc) {
+        own_off = (int64_t *)malloc(sizeof(int64_t) * ((size_t)n + 1));
+        own_inc = (int64_t *)malloc(sizeof(int64_t) * (size_t)(2 * m + 1));
+        orc_incidence(edges, m, n, own_off, own_inc);
+        off = own_off;
+        inc = own_inc;
     }
 #ifdef _OPENMP
-#pragma omp parallel for num_threads(nth)
+#pragma omp parallel for num_threads(nth) schedule(dynamic, 1024)
 #endif
     for (int64_t v = 0; v < n; v++) {
+        double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0}, phi[5];
+        for (int64_t q = off[v]; q < off[v + 1]; q++) {
+            cfd_edge_phi(edges, normals, U, inc[q] >> 1, phi);
+            if (inc[q] & 1)
+                for (int j = 0; j < 5; j++) acc[j] -= phi[j];
+            else
+                for (int j = 0; j < 5; j++) acc[j] += phi[j];
+        }
+        const int touched = off[v + 1] > off[v];
         for (int j = 0; j < 5; j++) {
-            double acc = 0.0;
-            for (int t = 0; t < nth; t++) acc += priv[(size_t)t * (size_t)n * 5 + 5 * v + j];
-            F[5 * v + j] = acc;
-            Uout[5 * v + j] = (double)U[5 * v + j] + (touched[v] ? (double)dt[v] * acc : 0.0);
+            F[5 * v + j] = acc[j];
+            Uout[5 * v + j] = (double)U[5 * v + j] + (touched ? (double)dt[v] * acc[j] : 0.0);
         }
     }
-    free(priv);
-    free(touched);
+    free(own_off);
+    free(own_inc);
     return nth;
 }
 

@@ -208,12 +208,19 @@ def test_flux_abs_scale(small_mesh):
 
 
 def test_cfd_step_omp_matches_sequential(small_mesh):
-    """The all-core timing variant (private accumulators, CPU baseline only) computes the
-    same step up to the summation order of F."""
+    """The all-core timing variant (vertex-centric incidence sums, CPU baseline only) adds each
+    vertex's terms in orc_cfd_flux's order, so it equals the sequential step bit for bit --
+    also on a random multigraph with self-loops and parallel edges."""
     M = small_mesh
     U, dt = S.cfd_state(M.n), S.cfd_dt(M.volume)
     ref, F = O.cfd_step(M.edges, M.n, M.normals, U, dt)
     got, F2, th = O.cfd_step_omp(M.edges, M.n, M.normals, U, dt)
     assert th >= 1
-    assert np.allclose(F2, F, rtol=0, atol=1e-12 * np.abs(F).max())
-    assert np.allclose(got, ref, rtol=0, atol=1e-12)
+    assert np.array_equal(F2, F) and np.array_equal(got, ref)
+    n, e = S.random_multigraph(77, 3000, 900)
+    rng = np.random.default_rng(5)
+    nrm = rng.uniform(-1, 1, (len(e), 3)).astype(np.float32)
+    U2, dt2 = S.cfd_state(n), rng.uniform(0.01, 0.1, n).astype(np.float32)
+    ref, F = O.cfd_step(e, n, nrm, U2, dt2)
+    got, F2, _ = O.cfd_step_omp(e, n, nrm, U2, dt2)
+    assert np.array_equal(F2, F) and np.array_equal(got, ref)
