@@ -70,6 +70,17 @@ struct OccArgs {
 
 __device__ __forceinline__ int64_t occ_part(const OccArgs &a, int64_t x) { return a.order ? a.order[x] : x; }
 
+// the 8 fields of a descriptor the occupancy kernel reads (o0 .. blob_bytes), as two 128-bit
+// loads (descriptors are 48-byte records, 16-byte aligned) instead of one 32-bit load each
+__device__ __forceinline__ PartDesc load_desc8(const PartDesc *p) {
+    const int4 *q = reinterpret_cast<const int4 *>(p);
+    const int4 x = __ldg(q), y = __ldg(q + 1);
+    PartDesc d;
+    d.o0 = x.x; d.nO = x.y; d.e0 = x.z; d.s = x.w;
+    d.h0 = y.x; d.nH = y.y; d.blob16 = y.z; d.blob_bytes = y.w;
+    return d;
+}
+
 // L2 prefetch of the aligned body of [g, g + bytes)
 __device__ __forceinline__ void prefetch_region(const void *g, uint32_t bytes) {
     const uintptr_t a = reinterpret_cast<uintptr_t>(g);
@@ -90,7 +101,7 @@ __global__ void EPG_OCC_BOUNDS(BLOCK) k_edge_occ(OccArgs a) {
     constexpr int ROW = Fn::ROW, PW = Fn::PAYW;
     const int tid = threadIdx.x;
     EPG_TP(0, 0);
-    const PartDesc d = a.desc[occ_part(a, a.first + blockIdx.x)];
+    const PartDesc d = load_desc8(a.desc + occ_part(a, a.first + blockIdx.x));
     const int L = d.nO + d.nH;
     unsigned char *sblob = occ_smem;
     const uint8_t *scol = sblob + blob3_col_offset(d.nH, d.s, L, W, a.hw);   // record placement
@@ -126,8 +137,8 @@ __global__ void EPG_OCC_BOUNDS(BLOCK) k_edge_occ(OccArgs a) {
     // prefetched into L2 once this CTA's data has landed, so that CTA's first dependent DRAM
     // trips become L2 hits
     const bool ahead = a.ahead > 0 && tid == 32 && blockIdx.x + a.ahead < a.count;
-    PartDesc f{};
-    if (ahead) f = a.desc[occ_part(a, a.first + blockIdx.x + a.ahead)];
+    PartDesc f;                                    // read only by the `ahead` thread
+    if (ahead) f = load_desc8(a.desc + occ_part(a, a.first + blockIdx.x + a.ahead));
     // halo rows H_p. With few halos (nH <= nO, the EP maps) they are gathered right after the
     // wait so they fly with the bulk copies -- the halo ids open the blob, so each thread reads
     // its ids from global memory, before the wait (plan data), instead of waiting for the copy.
