@@ -25,6 +25,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--scale", type=int, default=24)
     ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--parts", default="1024,2048")
+    ap.add_argument("--rows", default="1024,2048")
+    ap.add_argument("--hubs", default="7,0,32")
     a = ap.parse_args()
     n, edges = S.rmat(a.scale)
     m = edges.shape[0]
@@ -33,13 +36,13 @@ def main():
     ctx = epg.Context(0, stream)
     E = torch.from_numpy(edges).cuda()
     X = torch.from_numpy(x).cuda()
-    for P in (1024, 2048):
+    for P in map(int, a.parts.split(",")):
         t0 = time.perf_counter()
         part, rank, rep = ctx.partition_rb(E, n, P, 1, 4096, ranked=True)
         tp = time.perf_counter() - t0
         k = epg.num_parts(m, P)
-        for rows in (1024, 2048):
-            for hub in ("7", "0", "32"):
+        for rows in map(int, a.rows.split(",")):
+            for hub in a.hubs.split(","):
                 os.environ["EPG_HUB_MIN"] = hub
                 ctx.set_exec_limits(rows, 1280 if P > 1024 else 1024)
                 L, plan = ctx.remap(E, n, part, k, halo_cap=rep.cut_cost, order_key=rank)
