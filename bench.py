@@ -567,7 +567,7 @@ def run_c3(args, torch, epg, ctx, stream, peak):
     ctx.set_exec_limits(getattr(args, "exec_rows", 0) or 704, 1024)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    part, rank, rep = ctx.partition_rb(E, M.n, P, ranked=True)
+    part, rank, rep = ctx.partition_rb(E, M.n, P, 1, getattr(args, "c3_leaf_parts", 0) or 512, ranked=True)
     t_part = time.perf_counter() - t0
     key = rank if getattr(args, "order", "growth") == "growth" else None
     pay0 = torch.from_numpy(M.normals).to(dev)
