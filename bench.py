@@ -88,7 +88,7 @@ class Workload:
             raise ValueError(config)
         self.gen_s = time.perf_counter() - t0
         if not hasattr(self, "leaf_parts"):
-            self.leaf_parts = 512
+            self.leaf_parts = 2048 if config == "c3" else 512
 
     def alg_bytes(self, touched: int) -> int:
         """SURVEY §8(d) compulsory bytes of one step."""
@@ -567,7 +567,8 @@ def run_c3(args, torch, epg, ctx, stream, peak):
     ctx.set_exec_limits(getattr(args, "exec_rows", 0) or 704, 1024)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    part, rank, rep = ctx.partition_rb(E, M.n, P, 1, getattr(args, "c3_leaf_parts", 0) or 512, ranked=True)
+    # EPG-RB leaves of 2048 partitions (profiles/r02_c3_leaf_sweep.json: R 1.2350 in 4.4 s, vs 1.2381 at 512)
+    part, rank, rep = ctx.partition_rb(E, M.n, P, 1, getattr(args, "c3_leaf_parts", 0) or 2048, ranked=True)
     t_part = time.perf_counter() - t0
     key = rank if getattr(args, "order", "growth") == "growth" else None
     pay0 = torch.from_numpy(M.normals).to(dev)
