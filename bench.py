@@ -137,6 +137,9 @@ def parse():
                     help="execution-split row cap (epg_set_exec_limits; 0 = the config's default)")
     ap.add_argument("--exec-edges", type=int, default=0,
                     help="execution-split edge cap (0: 1024, or 1280 when --part-size > 1024)")
+    ap.add_argument("--exchange", choices=["nccl", "p2p"], default="nccl",
+                    help="N > 1: the halo push through NCCL's schedule, or fused into the edge kernel over "
+                         "peer memory (EPG_EXCHANGE=p2p)")
     ap.add_argument("--no-comparators", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-sharded", action="store_true",
@@ -290,7 +293,7 @@ def bench_config(args):
             "schedule": f"EP ({args.partitioner.upper()} partitioner) + cpack remap",
             "step": "one time step of the hot path: staged edge kernel (a5) + boundary finalise (a6)",
             "l2": L2_MODE,
-            "parallelism": "single GPU" if args.gpus == 1 else f"{args.gpus} GPUs"}
+            "parallelism": "single GPU" if args.gpus == 1 else f"{args.gpus} GPUs, halo exchange: {args.exchange}"}
 
 
 def oracle_baseline(w: "Workload", budget_s: float, steps_min: int = 1):
@@ -397,6 +400,8 @@ def run_sharded(args, rank, local_rank, world):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    if args.exchange == "p2p":
+        os.environ["EPG_EXCHANGE"] = "p2p"   # read by the library at the first sharded step
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.current_stream(dev)

@@ -379,7 +379,15 @@ epg_status epg_accumulate_rows(epg_ctx *ctx, const float *src, const int32_t *id
  * its halo partials of every vertex of Halo^{g<-g'} (fixed order) and adds what higher ranks
  * send into a per-vertex accumulator in ascending rank order; (4) the boundary finalise of
  * g's shared vertices and g's untouched rows. Only the rows g owns (epg_shard_ranges) are
- * authoritative in state_out. Deterministic for a fixed G.
+ * authoritative in state_out. Deterministic for a fixed G. The interior partitions (no halo
+ * row owned by a lower rank) run while the pull is in flight (NCCL on a stream of the ctx's
+ * own), and the local finalise while the push is.
+ * EPG_EXCHANGE=p2p (environment, read when a plan first steps sharded) fuses the push into the
+ * boundary edge kernel: each partition adds its partial of a vertex owned by rank p straight
+ * into p's accumulator in peer memory (atomics over NVLink; the accumulators' CUDA IPC handles
+ * are exchanged once with ncclAllGather), and a one-float NCCL token per push pair orders the
+ * owner's accumulate-add after the pushers' kernels; the summation order of those partials
+ * is then not fixed (the rest of the step is unchanged).
  *
  * epg_comm_unique_id: ncclGetUniqueId into id_out (128 bytes, host) -- call on one rank and
  *   broadcast it (e.g. through torch.distributed).

@@ -1032,7 +1032,8 @@ epg_status run_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, 
 // edge kernel over execution partitions [first, first + count) only (no finalise)
 template <class Fn>
 epg_status run_edges_range(epg_ctx *ctx, epg_plan *pl, epg_state *state, int64_t first, int64_t count,
-                           const int32_t *order = nullptr) {
+                           const int32_t *order = nullptr, float *const *peer_acc = nullptr,
+                           const int32_t *vlo = nullptr, int rank = 0) {
     if (pl->Scap > kOccMaxEdges || pl->Lcap > occ_max_rows<Fn>())
         return ctx->fail(EPG_ERR_INFEASIBLE, "run_edges: plan exceeds the occupancy kernel limits");
     OccArgs a{};
@@ -1055,6 +1056,9 @@ epg_status run_edges_range(epg_ctx *ctx, epg_plan *pl, epg_state *state, int64_t
     a.halo_buf = pl->halo_buf;
     a.first = first;
     a.order = order;
+    a.peer_acc = peer_acc;
+    a.vlo = vlo;
+    a.rank = rank;
     a.hw = pl->hub_words;
     a.hub_acc = nullptr;   // shard ranges sum every halo partial through hv_list
     if (count <= 0) return EPG_OK;
@@ -2360,6 +2364,7 @@ struct NcclApi {
     ncclResult_t (*groupEnd)() = nullptr;
     ncclResult_t (*send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*allGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     const char *(*errorString)(ncclResult_t) = nullptr;
 };
 
@@ -2389,6 +2394,7 @@ const NcclApi *nccl_api(std::string *err) {
     NSYM(groupEnd, "ncclGroupEnd");
     NSYM(send, "ncclSend");
     NSYM(recv, "ncclRecv");
+    NSYM(allGather, "ncclAllGather");
     NSYM(errorString, "ncclGetErrorString");
 #undef NSYM
     if (!api.getUniqueId || !api.commInitRank || !api.commDestroy || !api.groupStart || !api.groupEnd || !api.send ||
@@ -2432,8 +2438,17 @@ struct ShardState {
     // NCCL: the exchanges run on a stream of their own, ordered against the ctx stream by events
     cudaStream_t comm_stream = nullptr;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // peer push (EPG_EXCHANGE=p2p): the boundary edge kernel adds the partials of foreign vertices
+    // straight into their owners' accumulators (peer memory); a 1-float token per push pair then
+    // orders the owner's accumulate-add after the pushers' kernels
+    bool p2p = false;
+    float **peer_acc = nullptr;   // DEVICE [G] accumulators of the ranks (peer-mapped)
+    int32_t *vlo = nullptr;       // DEVICE [G + 1] first cpack row of each rank's shard
+    float *tok = nullptr;         // [2 G] token send / receive slots
+    std::vector<void *> ipc_opened;
     std::vector<void *> allocs;
     ~ShardState() {
+        for (void *p : ipc_opened) cudaIpcCloseMemHandle(p);
         for (void *p : allocs) cudaFree(p);
         for (cudaEvent_t e : ev)
             if (e) cudaEventDestroy(e);
@@ -2578,6 +2593,57 @@ epg_status shard_state(epg_ctx *ctx, epg_plan *pl, int row, ShardState **out) {
         CU(cudaStreamCreateWithFlags(&S->comm_stream, cudaStreamNonBlocking));
         for (cudaEvent_t &ev : S->ev) CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     }
+    {
+        const char *xe = std::getenv("EPG_EXCHANGE");
+        S->p2p = G > 1 && xe && std::string(xe) == "p2p";
+    }
+    if (S->p2p) {
+        std::vector<int32_t> vl(G + 1);
+        for (int p = 0; p < G; p++) {
+            int64_t q8[8];
+            if ((st = epg_shard_ranges(pl, G, p, q8))) return ctx->fail(st, "run_sharded: shard ranges");
+            vl[p] = (int32_t)q8[4];
+            vl[p + 1] = (int32_t)(q8[4] + q8[5]);
+        }
+        S->vlo = (int32_t *)shard_alloc(S.get(), sizeof(int32_t) * (G + 1), &e);
+        if (e == cudaSuccess) S->peer_acc = (float **)shard_alloc(S.get(), sizeof(float *) * G, &e);
+        if (e == cudaSuccess) S->tok = (float *)shard_alloc(S.get(), sizeof(float) * 2 * G, &e);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return ctx->fail(EPG_ERR_NOMEM, "run_sharded: peer tables");
+        }
+        CU(cudaMemcpy(S->vlo, vl.data(), sizeof(int32_t) * (G + 1), cudaMemcpyHostToDevice));
+        CU(cudaMemset(S->tok, 0, sizeof(float) * 2 * G));
+        if (ctx->comm && ctx->comm->nccl) {   // exchange the accumulators' IPC handles
+            std::string err;
+            const NcclApi *n = nccl_api(&err);
+            if (!n) return ctx->fail(EPG_ERR_NCCL, err);
+            cudaIpcMemHandle_t mine;
+            CU(cudaIpcGetMemHandle(&mine, S->acc));
+            Tmp hd(ctx);
+            CU(hd.alloc(sizeof(cudaIpcMemHandle_t) * G));
+            CU(cudaMemcpy(static_cast<char *>(hd.p) + sizeof(cudaIpcMemHandle_t) * g, &mine, sizeof(mine),
+                          cudaMemcpyHostToDevice));
+            ncclResult_t r = n->allGather(static_cast<char *>(hd.p) + sizeof(cudaIpcMemHandle_t) * g, hd.p,
+                                          sizeof(cudaIpcMemHandle_t), ncclChar, ctx->comm->nccl, ctx->stream);
+            if (r != ncclSuccess) return ctx->fail(EPG_ERR_NCCL, std::string("run_sharded: ") + n->errorString(r));
+            std::vector<cudaIpcMemHandle_t> hs(G);
+            CU(cudaMemcpyAsync(hs.data(), hd.p, sizeof(cudaIpcMemHandle_t) * G, cudaMemcpyDeviceToHost, ctx->stream));
+            CU(cudaStreamSynchronize(ctx->stream));
+            std::vector<float *> tab(G, nullptr);
+            for (int p = 0; p < G; p++) {
+                if (p == g) {
+                    tab[p] = S->acc;
+                    continue;
+                }
+                void *q = nullptr;
+                CU(cudaIpcOpenMemHandle(&q, hs[p], cudaIpcMemLazyEnablePeerAccess));
+                S->ipc_opened.push_back(q);
+                tab[p] = static_cast<float *>(q);
+            }
+            CU(cudaMemcpy(S->peer_acc, tab.data(), sizeof(float *) * G, cudaMemcpyHostToDevice));
+        }   // in-process groups: run_group_t fills the table with the members' accumulators
+    }
     *out = S.release();
     shard_states()[key] = *out;
     return EPG_OK;
@@ -2617,6 +2683,28 @@ epg_status exchange(epg_ctx *ctx, ShardState *S, const float *send, const std::v
         return EPG_OK;
     }
     return EPG_OK;   // in-process groups exchange in run_sharded_group
+}
+
+// peer push: after this rank's boundary edge kernel, one float to every owner it pushed to
+// (p < g) and one from every rank that pushed to it (p > g) -- stream-ordered, so a received
+// token means the pusher's kernel (and its peer atomics) completed
+epg_status exchange_token(epg_ctx *ctx, ShardState *S, cudaStream_t stream) {
+    const int G = S->G, g = S->g;
+    Comm *c = ctx->comm;
+    if (G == 1 || !c || !c->nccl) return EPG_OK;
+    std::string err;
+    const NcclApi *n = nccl_api(&err);
+    if (!n) return ctx->fail(EPG_ERR_NCCL, err);
+    ncclResult_t r = n->groupStart();
+    for (int p = 0; p < G && r == ncclSuccess; p++) {
+        if (p < g && S->recv_off[p + 1] > S->recv_off[p]) r = n->send(S->tok + p, 1, ncclFloat, p, c->nccl, stream);
+        if (r == ncclSuccess && p > g && S->send_off[p + 1] > S->send_off[p])
+            r = n->recv(S->tok + G + p, 1, ncclFloat, p, c->nccl, stream);
+    }
+    ncclResult_t r2 = n->groupEnd();
+    if (r != ncclSuccess || r2 != ncclSuccess)
+        return ctx->fail(EPG_ERR_NCCL, std::string("run_sharded: ") + n->errorString(r != ncclSuccess ? r : r2));
+    return EPG_OK;
 }
 
 template <class Fn>
@@ -2712,8 +2800,22 @@ epg_status run_sharded_t(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t s
         if ((st = sharded_pull_pack<Fn>(ctx, S, in)) || (st = fork(0)) ||
             (st = exchange(ctx, S, S->pull_send, S->send_off, S->pull_recv, S->recv_off, cs)) ||
             (st = run_edges_range<Fn>(ctx, pl, &cur, 0, S->n_interior, S->order)) || (st = join(1)) ||
-            (st = sharded_pull_unpack<Fn>(ctx, S, in)) ||
-            (st = run_edges_range<Fn>(ctx, pl, &cur, S->n_interior, nb, S->order)) ||
+            (st = sharded_pull_unpack<Fn>(ctx, S, in)))
+            return st;
+        if (S->p2p) {   // the boundary kernel pushes foreign partials into the owners' accumulators
+            if ((st = run_edges_range<Fn>(ctx, pl, &cur, S->n_interior, nb, S->order, S->peer_acc, S->vlo, S->g)) ||
+                (st = fork(2)) || (st = exchange_token(ctx, S, cs)))
+                return st;
+            if (S->recs) {
+                if ((st = sharded_finalise_local<Fn>(ctx, pl, S, &cur)) || (st = join(3)) ||
+                    (st = sharded_acc_add<Fn>(ctx, S, &cur)))
+                    return st;
+            } else if ((st = join(3)) || (st = sharded_finalise<Fn>(ctx, pl, S, &cur))) {
+                return st;
+            }
+            continue;
+        }
+        if ((st = run_edges_range<Fn>(ctx, pl, &cur, S->n_interior, nb, S->order)) ||
             (st = sharded_push_pack<Fn>(ctx, pl, S)) || (st = fork(2)) ||
             (st = exchange(ctx, S, S->push_send, S->recv_off, S->push_recv, S->send_off, cs)))
             return st;
@@ -2737,6 +2839,13 @@ epg_status run_group_t(epg_ctx **ctxs, epg_plan **plans, epg_state *states, int 
     for (int g = 0; g < G; g++) {
         epg_status st = shard_state(ctxs[g], plans[g], Fn::ROW, &S[g]);
         if (st) return st;
+    }
+    const bool p2p = S[0]->p2p;
+    if (p2p) {   // the members' accumulators are the "peer" memory (one device)
+        std::vector<float *> tab(G);
+        for (int g = 0; g < G; g++) tab[g] = S[g]->acc;
+        for (int g = 0; g < G; g++) CU_NOCTX(cudaMemcpy(S[g]->peer_acc, tab.data(), sizeof(float *) * G,
+                                                         cudaMemcpyHostToDevice));
     }
     std::vector<cudaEvent_t> ev(G);
     for (int g = 0; g < G; g++) cudaEventCreateWithFlags(&ev[g], cudaEventDisableTiming);
@@ -2767,16 +2876,23 @@ epg_status run_group_t(epg_ctx **ctxs, epg_plan **plans, epg_state *states, int 
     sync_all();
     for (int g = 0; g < G && !st; g++) {
         if ((st = sharded_pull_unpack<Fn>(ctxs[g], S[g], (float *)states[g].state_in))) break;
+        if (p2p) {
+            st = run_edges_range<Fn>(ctxs[g], plans[g], &states[g], S[g]->n_interior, S[g]->xc - S[g]->n_interior,
+                                     S[g]->order, S[g]->peer_acc, S[g]->vlo, g);
+            continue;
+        }
         if ((st = run_edges_range<Fn>(ctxs[g], plans[g], &states[g], S[g]->n_interior, S[g]->xc - S[g]->n_interior,
                                       S[g]->order)))
             break;
         st = sharded_push_pack<Fn>(ctxs[g], plans[g], S[g]);
     }
     sync_all();
-    copy_phase(false);
-    sync_all();
+    if (!p2p) {
+        copy_phase(false);
+        sync_all();
+    }
     for (int g = 0; g < G && !st; g++) {
-        if ((st = sharded_push_accumulate<Fn>(ctxs[g], S[g]))) break;
+        if (!p2p && (st = sharded_push_accumulate<Fn>(ctxs[g], S[g]))) break;
         st = sharded_finalise<Fn>(ctxs[g], plans[g], S[g], &states[g]);
     }
     sync_all();

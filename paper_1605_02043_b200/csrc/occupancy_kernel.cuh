@@ -66,6 +66,11 @@ struct OccArgs {
     const float *state_end;    // one past the last row of state_in (bound of the 32-byte halo reads)
     const int32_t *order;      // NULL, or the execution partitions of this launch are order[first + b]
                                // (multi-GPU: a shard's interior partitions, then its boundary ones)
+    // multi-GPU peer push (EPG_EXCHANGE=p2p): the partial of a halo row owned by a lower rank p
+    // is added straight into rank p's accumulator (peer memory over NVLink) by this kernel
+    float *const *peer_acc;    // [G] accumulators of the ranks, or NULL
+    const int32_t *vlo;        // [G + 1] first cpack row of each rank's shard
+    int rank;                  // this rank
 };
 
 __device__ __forceinline__ int64_t occ_part(const OccArgs &a, int64_t x) { return a.order ? a.order[x] : x; }
@@ -404,6 +409,17 @@ __global__ void EPG_OCC_BOUNDS(BLOCK) k_edge_occ(OccArgs a) {
         } else {
 #pragma unroll
             for (int c = 0; c < ROW; c++) out[r][c] = acc[c];
+            if (a.peer_acc) {  // fused push: a foreign vertex's partial goes to its owner's accumulator
+                const int32_t h = reinterpret_cast<const int32_t *>(sblob)[j - d.nO];
+                if (h < a.vlo[a.rank]) {
+                    int p = 0;
+                    while (p + 1 < a.rank && h >= a.vlo[p + 1]) p++;
+                    float *dst = a.peer_acc[p] + (int64_t)ROW * h;
+#pragma unroll
+                    for (int c = 0; c < ROW; c++) atomicAdd(dst + c, acc[c]);
+                    __threadfence_system();   // performed in the peer's memory before this kernel ends
+                }
+            }
             if (a.hub_acc) {   // hub split: this partition's partial of a hub, pre-summed above
                 const int hx = reinterpret_cast<const int32_t *>(sblob)[d.nH + (j - d.nO)];
                 if (hx >= 0) {

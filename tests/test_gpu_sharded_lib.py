@@ -7,7 +7,10 @@ partitions, push partial sums, finalise) inside libepg.so.
   all members together equal the fp64 oracle within the Z14 tolerance (cfd) and bit for bit
   (integer-valued gather-scatter), and equal the single-GPU epg_run within fp32 rounding;
 * a one-rank NCCL communicator (epg_comm_unique_id + epg_comm_init, nranks = 1) runs the
-  same path with the NCCL transport: bit-identical to epg_run over several steps.
+  same path with the NCCL transport: bit-identical to epg_run over several steps;
+* every group test runs with both pushes: the sequential schedule and the fused peer push
+  (EPG_EXCHANGE=p2p, atomics into the owners' accumulators: integer-valued gather-scatter still
+  exact, cfd within the tolerance).
 """
 import numpy as np
 import pytest
@@ -48,8 +51,21 @@ def _owned(ctx, plan, G, g, out):
     return lo, hi, out[lo:hi].cpu().numpy()
 
 
+@pytest.fixture(params=["nccl-schedule", "p2p"])
+def exchange_mode(request, monkeypatch):
+    """The push of the exchange: the sequential schedule (partials reduced, sent, accumulated in a
+    fixed order) or the fused peer push (EPG_EXCHANGE=p2p: the boundary edge kernel adds each
+    foreign partial into its owner's accumulator; in the in-process group the members'
+    accumulators are the peer memory)."""
+    if request.param == "p2p":
+        monkeypatch.setenv("EPG_EXCHANGE", "p2p")
+    else:
+        monkeypatch.delenv("EPG_EXCHANGE", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("G", [2, 4, 8])
-def test_group_cfd_step(mesh_c1, G):
+def test_group_cfd_step(mesh_c1, G, exchange_mode):
     from paper_1605_02043_b200 import epg
     M = mesh_c1
     ctxs, Ls, plans, part = _group(G, M.edges, M.n, 256)
@@ -91,7 +107,7 @@ def test_group_cfd_step(mesh_c1, G):
 
 
 @pytest.mark.parametrize("G", [2, 8])
-def test_group_gather_scatter_exact(G):
+def test_group_gather_scatter_exact(G, exchange_mode):
     from paper_1605_02043_b200 import epg
     n, e = S.rmat(13)
     ctxs, Ls, plans, part = _group(G, e, n, 128)
