@@ -634,6 +634,16 @@ epg_status build_pipeline_blob(epg_ctx *ctx, epg_plan *pl) {
 
 inline int up16i(int x) { return (x + 15) & ~15; }
 
+// record array of the occupancy kernel: 8-float (cfd) records are two float4 arrays of
+// up8(Lcap) entries each (placed positions stay inside their group of 8); the staged rows
+// land inside it and are derived in place
+template <class Fn>
+int occ_recs_bytes(const epg_plan *pl) {
+    return Fn::REC == 8 ? 32 * ((pl->Lcap + 7) & ~7) + 64 : up16i(4 * Fn::REC * pl->Lcap + 64);
+}
+template <class Fn>
+int occ_rstride(const epg_plan *pl) { return Fn::REC == 8 ? ((pl->Lcap + 7) & ~7) : 0; }
+
 // shared-memory layout of the pipelined kernel for `nstage` stage buffers
 template <class Fn>
 size_t pipe_layout(const epg_plan *pl, bool has_payload, int nstage, PipeArgs *a) {
@@ -1005,7 +1015,8 @@ epg_status run_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, 
     CU(cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
     OccArgs a{};
     a.off_recs = up16i(pl->blob3_max);
-    const int recs_bytes = up16i(4 * Fn::REC * pl->Lcap + 64);
+    const int recs_bytes = occ_recs_bytes<Fn>(pl);
+    a.rstride = occ_rstride<Fn>(pl);
     // landing area of the staged rows inside the record array (derived in place): owned rows
     // then, for 5-float rows, one 32-byte slot per halo row (<= 32 L + 48 bytes in all)
     a.rows_land = Fn::ROW == 5 ? 16 : up16i(recs_bytes - (4 * Fn::ROW * pl->Lcap + 16) - 16);
@@ -1038,7 +1049,8 @@ epg_status run_edges_range(epg_ctx *ctx, epg_plan *pl, epg_state *state, int64_t
         return ctx->fail(EPG_ERR_INFEASIBLE, "run_edges: plan exceeds the occupancy kernel limits");
     OccArgs a{};
     a.off_recs = up16i(pl->blob3_max);
-    const int recs_bytes = up16i(4 * Fn::REC * pl->Lcap + 64);
+    const int recs_bytes = occ_recs_bytes<Fn>(pl);
+    a.rstride = occ_rstride<Fn>(pl);
     // landing area of the staged rows inside the record array (derived in place): owned rows
     // then, for 5-float rows, one 32-byte slot per halo row (<= 32 L + 48 bytes in all)
     a.rows_land = Fn::ROW == 5 ? 16 : up16i(recs_bytes - (4 * Fn::ROW * pl->Lcap + 16) - 16);
@@ -1219,7 +1231,7 @@ bool occ_applies(epg_ctx *ctx, const epg_plan *pl) {
     int dev_max = 0;
     if (cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device)) return false;
     OccArgs a{};
-    const int off_phi = up16i(pl->blob3_max) + up16i(4 * Fn::REC * pl->Lcap + 64);
+    const int off_phi = up16i(pl->blob3_max) + occ_recs_bytes<Fn>(pl);
     return (size_t)off_phi + occ_phi_bytes<Fn>(pl, &a) + 1024 <= (size_t)dev_max;
 }
 

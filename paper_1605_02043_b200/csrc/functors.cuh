@@ -203,7 +203,11 @@ struct CfdFlux {
     // f = |n| (s'_a + s'_b) -- the same expression as cfd_phi (the factors -1/2 are exact),
     // evaluated with sm_100's packed fp32x2 FMA/ADD (FFMA2 / FADD2) on component pairs
     // (rho, m_x), (m_y, m_z), (E, p'): ~32 FP instructions per edge instead of ~47.
-    __device__ __forceinline__ static void derive_occ(const float *row, float *recs, int j) {
+    // The occupancy kernel stores the record as two halves in separate float4 arrays, A = recs
+    // and B = recsB (both indexed by j): half h of record j lands in bank group (j mod 8) of its
+    // array, so the placement's in-group positions still decide the bank groups (the rec4
+    // swizzle is not needed) and both loads of an endpoint share one offset register.
+    __device__ __forceinline__ static void derive_occ(const float *row, float *recs, int j, float *recsB) {
         const float rho = row[0], mx = row[1], my = row[2], mz = row[3], E = row[4];
         const float rinv = rcp_ftz(rho);
         const float ux = mx * rinv, uy = my * rinv, uz = mz * rinv;
@@ -211,20 +215,22 @@ struct CfdFlux {
         const float p = (kGamma - 1.0f) * (E - 0.5f * rho * uu);
         const float speed = sqrt_nb(uu) + sqrt_nb(kGamma * p * rinv);
         float4 *r = reinterpret_cast<float4 *>(recs);
-        r[rec4(j, 0)] = make_float4(rho, mx, my, mz);
-        r[rec4(j, 1)] = make_float4(E, -0.5f * p, -(kSigma * 0.5f) * speed, -0.5f * rinv);
+        r[j] = make_float4(rho, mx, my, mz);
+        reinterpret_cast<float4 *>(recsB)[j] = make_float4(E, -0.5f * p, -(kSigma * 0.5f) * speed, -0.5f * rinv);
     }
-    __device__ __forceinline__ static void rec_state_occ(const float *recs, int j, float U[5]) {
-        rec_state(recs, j, U);
+    __device__ __forceinline__ static void rec_state_occ(const float *recs, int j, float U[5], const float *recsB) {
+        const float4 x = reinterpret_cast<const float4 *>(recs)[j];
+        U[0] = x.x; U[1] = x.y; U[2] = x.z; U[3] = x.w;
+        U[4] = reinterpret_cast<const float4 *>(recsB)[j].x;
     }
-    // split Phi layout of the occupancy kernel: a float4 array (Phi_0..3) and, `stride`
-    // records further, a float array (Phi_4) -- 20 B per edge, conflict-free stores and
+    // split Phi layout of the occupancy kernel: a float4 array (Phi_0..3) and a float array
+    // (Phi_4) at phisB -- 20 B per edge, conflict-free stores and
     // one 128-bit + one 32-bit shared load per incidence entry instead of three 64-bit
     static constexpr int PHIBYTES = 20;
     __device__ __forceinline__ static void edge_split(const float *recs, int a, int b, const float pw[3], int i,
-                                                      float *phis, int stride) {
-        const float4 *r = reinterpret_cast<const float4 *>(recs);
-        const float4 xa = r[rec4(a, 0)], ya = r[rec4(a, 1)], xb = r[rec4(b, 0)], yb = r[rec4(b, 1)];
+                                                      float *phis, float *phisB, const float *recsB) {
+        const float4 *r = reinterpret_cast<const float4 *>(recs), *rb = reinterpret_cast<const float4 *>(recsB);
+        const float4 xa = r[a], ya = rb[a], xb = r[b], yb = rb[b];
         const float nx = pw[0], ny = pw[1], nz = pw[2];
         const float nlen = sqrt_nb(nx * nx + ny * ny + nz * nz);
         const float f = nlen * (ya.z + yb.z);
@@ -242,16 +248,16 @@ struct CfdFlux {
         const float2 p23 = __ffma2_rn(F2, __fadd2_rn(A23, make_float2(-B23.x, -B23.y)), c23);
         const float p4 = fmaf(f, ya.x - yb.x, fmaf(-2.0f, e.y, e.x));
         reinterpret_cast<float4 *>(phis)[i] = make_float4(p01.x, p01.y, p23.x, p23.y);
-        phis[4 * stride + i] = p4;
+        phisB[i] = p4;
     }
-    __device__ __forceinline__ static void zero_split(float *phis, int i, int stride) {
+    __device__ __forceinline__ static void zero_split(float *phis, int i, float *phisB) {
         reinterpret_cast<float4 *>(phis)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        phis[4 * stride + i] = 0.f;
+        phisB[i] = 0.f;
     }
     __device__ __forceinline__ static void gather_split(const float *phis, int i, int side, float acc[5],
-                                                        int stride) {
+                                                        const float *phisB) {
         const float4 x = reinterpret_cast<const float4 *>(phis)[i];
-        const float y = phis[4 * stride + i];
+        const float y = phisB[i];
         const float sgn = side ? -1.0f : 1.0f;
         const float2 S2 = make_float2(sgn, sgn);
         const float2 a01 = __ffma2_rn(S2, make_float2(x.x, x.y), make_float2(acc[0], acc[1]));
@@ -320,14 +326,14 @@ struct GatherScatter {
     }
     static constexpr int PHIBYTES = 8;   // same layout as the records above (stride unused)
     __device__ __forceinline__ static void edge_split(const float *recs, int a, int b, const float pw[1], int i,
-                                                      float *phis, int) { edge_rec_pw(recs, a, b, pw, i, phis); }
-    __device__ __forceinline__ static void zero_split(float *phis, int i, int) { zero_phi(phis, i); }
-    __device__ __forceinline__ static void gather_split(const float *phis, int i, int side, float acc[1], int) {
+                                                      float *phis, float *, const float *) { edge_rec_pw(recs, a, b, pw, i, phis); }
+    __device__ __forceinline__ static void zero_split(float *phis, int i, float *) { zero_phi(phis, i); }
+    __device__ __forceinline__ static void gather_split(const float *phis, int i, int side, float acc[1], const float *) {
         gather_rec(phis, i, side, acc);
     }
     // occupancy-kernel hooks (same record as derive_rec)
-    __device__ __forceinline__ static void derive_occ(const float *row, float *recs, int j) { derive_rec(row, recs, j); }
-    __device__ __forceinline__ static void rec_state_occ(const float *recs, int j, float U[1]) { rec_state(recs, j, U); }
+    __device__ __forceinline__ static void derive_occ(const float *row, float *recs, int j, float *) { derive_rec(row, recs, j); }
+    __device__ __forceinline__ static void rec_state_occ(const float *recs, int j, float U[1], const float *) { rec_state(recs, j, U); }
     __device__ __forceinline__ static void finish_occ(const float U[1], const float acc[1], float dt, float out[1]) {
         finish_row(U, acc, dt, out);
     }
@@ -377,14 +383,14 @@ struct Spmv {
     }
     static constexpr int PHIBYTES = 4;
     __device__ __forceinline__ static void edge_split(const float *recs, int a, int b, const float pw[1], int i,
-                                                      float *phis, int) { edge_rec_pw(recs, a, b, pw, i, phis); }
-    __device__ __forceinline__ static void zero_split(float *phis, int i, int) { zero_phi(phis, i); }
-    __device__ __forceinline__ static void gather_split(const float *phis, int i, int side, float acc[1], int) {
+                                                      float *phis, float *, const float *) { edge_rec_pw(recs, a, b, pw, i, phis); }
+    __device__ __forceinline__ static void zero_split(float *phis, int i, float *) { zero_phi(phis, i); }
+    __device__ __forceinline__ static void gather_split(const float *phis, int i, int side, float acc[1], const float *) {
         gather_rec(phis, i, side, acc);
     }
     // occupancy-kernel hooks (same record as derive_rec)
-    __device__ __forceinline__ static void derive_occ(const float *row, float *recs, int j) { derive_rec(row, recs, j); }
-    __device__ __forceinline__ static void rec_state_occ(const float *recs, int j, float U[1]) { rec_state(recs, j, U); }
+    __device__ __forceinline__ static void derive_occ(const float *row, float *recs, int j, float *) { derive_rec(row, recs, j); }
+    __device__ __forceinline__ static void rec_state_occ(const float *recs, int j, float U[1], const float *) { rec_state(recs, j, U); }
     __device__ __forceinline__ static void finish_occ(const float U[1], const float acc[1], float dt, float out[1]) {
         finish_row(U, acc, dt, out);
     }

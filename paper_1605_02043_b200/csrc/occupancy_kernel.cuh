@@ -58,6 +58,7 @@ struct OccArgs {
     int early_pdl;             // 1: trigger dependents at the start (single-wave grids)
     int sentinel;              // zero Phi record of padded incidence entries (plan Scap)
     int pstride;               // records of the split Phi layout (>= sentinel + 1, multiple of 4)
+    int rstride;               // float4s from a derived record's first half to its second (REC = 8)
     int64_t ahead;             // > 0 (multi-wave grids): L2-prefetch partition x + ahead's ranges
     int64_t count;             // execution partitions of this launch
     // the partition's endpoint slots, edge payload and dt are bulk-copied into the Phi space
@@ -112,6 +113,8 @@ __global__ void EPG_OCC_BOUNDS(BLOCK) k_edge_occ(OccArgs a) {
     const uint8_t *scol = sblob + blob3_col_offset(d.nH, d.s, L, W, a.hw);   // record placement
     float *recs = reinterpret_cast<float *>(occ_smem + a.off_recs);
     float *phis = reinterpret_cast<float *>(occ_smem + a.off_phi);
+    float *recsB = recs + 4 * a.rstride;         // second halves of the derived records (REC = 8)
+    float *phisB = phis + 4 * a.pstride;         // Phi_4 of the split Phi records
     const float *g_rows = a.state_in + (int64_t)ROW * d.o0;
     unsigned char *rows_base = occ_smem + a.off_recs + a.rows_land;   // upper part of the record array
     float *rows = reinterpret_cast<float *>(rows_base + (reinterpret_cast<uintptr_t>(g_rows) & 15));
@@ -283,7 +286,7 @@ __global__ void EPG_OCC_BOUNDS(BLOCK) k_edge_occ(OccArgs a) {
 #pragma unroll
     for (int r = 0; r < VPT; r++) {
         const int j = tid + r * BLOCK;
-        if (j < L) Fn::derive_occ(rv[r], recs, (j & ~7) | scol[j]);   // placed record (place_kernels.cuh)
+        if (j < L) Fn::derive_occ(rv[r], recs, (j & ~7) | scol[j], recsB);   // placed record (place_kernels.cuh)
     }
     __syncthreads();
     // edges
@@ -292,10 +295,10 @@ __global__ void EPG_OCC_BOUNDS(BLOCK) k_edge_occ(OccArgs a) {
         const int i = tid + r * BLOCK;
         if (i < d.s)   // slots hold the placed record positions; bits 29-31 the Phi record's
             Fn::edge_split(recs, (int)(sl[r] & 0xffffu), (int)((sl[r] >> 16) & 0x1fffu), pw[r],
-                           (i & ~7) | (int)(sl[r] >> 29), phis, a.pstride);
+                           (i & ~7) | (int)(sl[r] >> 29), phis, phisB, recsB);
     }
     if constexpr (W > 0) {
-        if (tid == 0) Fn::zero_split(phis, a.sentinel, a.pstride);
+        if (tid == 0) Fn::zero_split(phis, a.sentinel, phisB);
     }
     __syncthreads();
     EPG_TP(0, 4);
@@ -341,7 +344,7 @@ __global__ void EPG_OCC_BOUNDS(BLOCK) k_edge_occ(OccArgs a) {
             }
             const int w = inc[q];
             float v[1] = {0.0f};
-            Fn::gather_split(phis, w >> 1, w & 1, v, a.pstride);
+            Fn::gather_split(phis, w >> 1, w & 1, v, phisB);
             part += v[0];
         }
         // carry of the open segment across threads: inclusive scan of (starts, value) with
@@ -390,7 +393,7 @@ __global__ void EPG_OCC_BOUNDS(BLOCK) k_edge_occ(OccArgs a) {
 #pragma unroll
             for (int q = 0; q < W; q++) {
                 const uint32_t w = (w2[q >> 1] >> (16 * (q & 1))) & 0xffffu;
-                Fn::gather_split(phis, (int)(w >> 1), (int)(w & 1), acc, a.pstride);
+                Fn::gather_split(phis, (int)(w >> 1), (int)(w & 1), acc, phisB);
             }
         } else if constexpr (kSegScan) {
             acc[0] = tot[j];
@@ -399,12 +402,12 @@ __global__ void EPG_OCC_BOUNDS(BLOCK) k_edge_occ(OccArgs a) {
             const int q0 = ioff[j], q1 = j + 1 < L ? ioff[j + 1] : 2 * d.s;
             for (int q = q0; q < q1; q++) {
                 const int w = inc[q];
-                Fn::gather_split(phis, w >> 1, w & 1, acc, a.pstride);
+                Fn::gather_split(phis, w >> 1, w & 1, acc, phisB);
             }
         }
         if (j < d.nO) {
             float U[ROW];
-            Fn::rec_state_occ(recs, (j & ~7) | scol[j], U);
+            Fn::rec_state_occ(recs, (j & ~7) | scol[j], U, recsB);
             Fn::finish_occ(U, acc, dtv[r], out[r]);
         } else {
 #pragma unroll
