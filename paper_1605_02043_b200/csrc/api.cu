@@ -1085,7 +1085,9 @@ epg_status run_edges_range(epg_ctx *ctx, epg_plan *pl, epg_state *state, int64_t
                 it = pl->resident_ctas.emplace(reinterpret_cast<const void *>(kern), (int64_t)occ * sms).first;
             }
             const char *e = std::getenv("EPG_PREFETCH_AHEAD");
-            a.early_pdl = 0;
+            // one-wave ranges trigger their dependents at the start, as launch_occ does: the next
+            // PDL launch's prologue (plan data only; it waits before reading state) overlaps this one
+            a.early_pdl = count <= it->second ? 1 : 0;
             a.ahead = count > it->second ? (e ? std::atoll(e) : it->second) : 0;
             a.count = count;
         }
