@@ -730,6 +730,7 @@ __global__ void k_finalise_rec16(const int4 *__restrict__ recs, const int32_t *_
                                  float *__restrict__ state_out, const float *__restrict__ vconst, int32_t S,
                                  int64_t touched, int64_t n) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    EPG_TP(14, 0);
     // records, overflow entries and dt are plan / constant data: loaded before the wait
     int4 r = make_int4(0, -1, 0, 0);
     int h[6] = {0, 0, 0, 0, 0, 0};
@@ -747,6 +748,7 @@ __global__ void k_finalise_rec16(const int4 *__restrict__ recs, const int32_t *_
         if (Fn::kUsesConst && r.y >= 0) dt = vconst[r.x];
     }
     ptx::pdl_wait();
+    EPG_TP(14, 1);
     ptx::pdl_launch_dependents();
     if (t < S) {
         const int64_t v = r.x;
@@ -763,6 +765,7 @@ __global__ void k_finalise_rec16(const int4 *__restrict__ recs, const int32_t *_
             }
         }
         Fn::finalise_add(state_out + Fn::ROW * v, acc, dt);
+        EPG_TP(14, 2);
         return;
     }
     const int64_t v = touched + (t - S);

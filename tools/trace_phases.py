@@ -39,6 +39,9 @@ def main():
     ap.add_argument("--rr", type=int, default=0,
                     help="R > 0: trace the last step of 2R round-robin steps over R replicas (bench.py's "
                          "headline mode: direct launches chained by PDL, inputs evicted) instead of one cold step")
+    ap.add_argument("--chain", action="store_true",
+                    help="with --rr: trace the finalise of the last step and the edge kernel launched after it "
+                         "(times relative to the earliest finalise CTA start)")
     a = ap.parse_args()
     os.environ["EPG_LIB_PATH"] = build_trace_lib()
     sys.path.insert(0, ROOT)
@@ -88,6 +91,9 @@ def main():
             for i in range(2 * a.rr):              # the traced stamps are those of the last launch
                 pr, u, o, nr, dd = reps[i % a.rr]
                 ctx.run(pr, epg.KERNEL_CFD_FLUX, u, o, nr, dd, 1)
+            if a.chain:   # one more edge kernel: its stamps follow the finalise traced above
+                pr, u, o, nr, dd = reps[(2 * a.rr) % a.rr]
+                ctx.run_edges(pr, epg.KERNEL_CFD_FLUX, u, o, nr, dd)
             torch.cuda.synchronize()
         else:
             torch.cuda._sleep(2_000_000)               # keep the GPU busy while the host enqueues
@@ -100,6 +106,9 @@ def main():
         t = buf.reshape(1024, niters, npts)[:nblk, 0, :].astype(np.int64)
         epg.lib.epg_debug_trace_clear()
         base = t[:, 0][t[:, 0] > 0].min()
+        if a.chain:
+            f0 = buf.reshape(1024, niters, npts)[:, 14, 0].astype(np.int64)
+            base = f0[f0 > 0].min()
         print(f"variant {v} rep {rep}: k_exec={plan.k_exec} CTAs traced={nblk}")
         for pt in range(npts):
             col = t[:, pt]
