@@ -218,10 +218,12 @@ struct CfdFlux {
         r[j] = make_float4(rho, mx, my, mz);
         reinterpret_cast<float4 *>(recsB)[j] = make_float4(E, -0.5f * p, -(kSigma * 0.5f) * speed, -0.5f * rinv);
     }
-    __device__ __forceinline__ static void rec_state_occ(const float *recs, int j, float U[5], const float *recsB) {
+    // the conserved state of record j; its last component (E) is the caller's register copy of
+    // the staged row (a 32-bit load from the 16-byte-strided B array would conflict 4-way)
+    __device__ __forceinline__ static void rec_state_occ(const float *recs, int j, float U[5], float last) {
         const float4 x = reinterpret_cast<const float4 *>(recs)[j];
         U[0] = x.x; U[1] = x.y; U[2] = x.z; U[3] = x.w;
-        U[4] = reinterpret_cast<const float4 *>(recsB)[j].x;
+        U[4] = last;
     }
     // split Phi layout of the occupancy kernel: a float4 array (Phi_0..3) and a float array
     // (Phi_4) at phisB -- 20 B per edge, conflict-free stores and
@@ -333,7 +335,7 @@ struct GatherScatter {
     }
     // occupancy-kernel hooks (same record as derive_rec)
     __device__ __forceinline__ static void derive_occ(const float *row, float *recs, int j, float *) { derive_rec(row, recs, j); }
-    __device__ __forceinline__ static void rec_state_occ(const float *recs, int j, float U[1], const float *) { rec_state(recs, j, U); }
+    __device__ __forceinline__ static void rec_state_occ(const float *, int, float U[1], float last) { U[0] = last; }
     __device__ __forceinline__ static void finish_occ(const float U[1], const float acc[1], float dt, float out[1]) {
         finish_row(U, acc, dt, out);
     }
@@ -390,7 +392,7 @@ struct Spmv {
     }
     // occupancy-kernel hooks (same record as derive_rec)
     __device__ __forceinline__ static void derive_occ(const float *row, float *recs, int j, float *) { derive_rec(row, recs, j); }
-    __device__ __forceinline__ static void rec_state_occ(const float *recs, int j, float U[1], const float *) { rec_state(recs, j, U); }
+    __device__ __forceinline__ static void rec_state_occ(const float *, int, float U[1], float last) { U[0] = last; }
     __device__ __forceinline__ static void finish_occ(const float U[1], const float acc[1], float dt, float out[1]) {
         finish_row(U, acc, dt, out);
     }

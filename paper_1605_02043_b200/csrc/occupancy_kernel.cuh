@@ -283,9 +283,11 @@ __global__ void EPG_OCC_BOUNDS(BLOCK) k_edge_occ(OccArgs a) {
         }
     }
     __syncthreads();
+    float ulast[VPT];                              // last state component of the owned rows, kept for the update
 #pragma unroll
     for (int r = 0; r < VPT; r++) {
         const int j = tid + r * BLOCK;
+        ulast[r] = rv[r][ROW - 1];
         if (j < L) Fn::derive_occ(rv[r], recs, (j & ~7) | scol[j], recsB);   // placed record (place_kernels.cuh)
     }
     __syncthreads();
@@ -407,7 +409,7 @@ __global__ void EPG_OCC_BOUNDS(BLOCK) k_edge_occ(OccArgs a) {
         }
         if (j < d.nO) {
             float U[ROW];
-            Fn::rec_state_occ(recs, (j & ~7) | scol[j], U, recsB);
+            Fn::rec_state_occ(recs, (j & ~7) | scol[j], U, ulast[r]);
             Fn::finish_occ(U, acc, dtv[r], out[r]);
         } else {
 #pragma unroll
