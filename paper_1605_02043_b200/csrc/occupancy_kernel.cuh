@@ -376,6 +376,7 @@ __global__ void EPG_OCC_BOUNDS(BLOCK) k_edge_occ(OccArgs a) {
         __syncthreads();
     }
     float out[VPT][ROW];
+    bool pushed = false;                           // this thread added partials into peer memory
 #pragma unroll
     for (int r = 0; r < VPT; r++) {
         const int j = tid + r * BLOCK;
@@ -421,19 +422,22 @@ __global__ void EPG_OCC_BOUNDS(BLOCK) k_edge_occ(OccArgs a) {
                     while (p + 1 < a.rank && h >= a.vlo[p + 1]) p++;
                     float *dst = a.peer_acc[p] + (int64_t)ROW * h;
 #pragma unroll
-                    for (int c = 0; c < ROW; c++) atomicAdd(dst + c, acc[c]);
-                    __threadfence_system();   // performed in the peer's memory before this kernel ends
+                    for (int c = 0; c < ROW; c++) ptx::red_add_f32(dst + c, acc[c]);
+                    pushed = true;
                 }
             }
             if (a.hub_acc) {   // hub split: this partition's partial of a hub, pre-summed above
                 const int hx = reinterpret_cast<const int32_t *>(sblob)[d.nH + (j - d.nO)];
                 if (hx >= 0) {
 #pragma unroll
-                    for (int c = 0; c < ROW; c++) atomicAdd(a.hub_acc + (int64_t)ROW * hx + c, acc[c]);
+                    for (int c = 0; c < ROW; c++) ptx::red_add_f32(a.hub_acc + (int64_t)ROW * hx + c, acc[c]);
                 }
             }
         }
     }
+    // the pushed partials are performed in the peers' memory before this kernel ends (one fence
+    // per pushing thread, after its last push; outside the loop, so the hub reductions stay REDs)
+    if (pushed) __threadfence_system();
     __syncthreads();                               // records and Phi no longer read
     // pack: owned rows at the 16-byte phase of their destination, then the halo partials
     float *g_out = a.state_out + (int64_t)ROW * d.o0;

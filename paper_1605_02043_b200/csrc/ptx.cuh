@@ -43,6 +43,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 
+// fire-and-forget float add to global memory (RED, no return): written out so that no fence
+// elsewhere in the kernel turns the reduction into a returning atomic (ATOMG)
+__device__ __forceinline__ void red_add_f32(float *gmem, float v) {
+    asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(__cvta_generic_to_global(gmem)), "f"(v) : "memory");
+}
+
 // 1-D TMA bulk copy global -> shared, completion counted on `bar` (bytes % 16 == 0,
 // both addresses 16-byte aligned)
 __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src_gmem, uint32_t bytes, uint64_t *bar) {

@@ -208,3 +208,33 @@ def test_plan_options_bitexact(cfg, P):
     ref2, _ = O.cfd_step(M.edges, M.n, M.normals, ref.astype(np.float32), dt)
     err = np.abs(base - ref2).max(axis=0) / np.abs(ref2).max(axis=0)
     assert err.max() <= 2e-5
+
+
+def test_run_edges_one_wave_chain_equals_run():
+    """One-wave epg_run_edges launches trigger their PDL dependents at the start, so the next
+    launch's plan-data prologue overlaps them: chains of run_edges + run_finalise over two
+    replicas (own plans and buffers, one context stream), issued back to back for three
+    rounds, give epg_run's result bit for bit (the dependent still waits before it reads state)."""
+    from paper_1605_02043_b200 import epg
+    M = S.config_mesh("c1")
+    ctx, L, plan, U, dt, Un, nrm, dtn = _prep(M, 1024)
+    assert plan.k_exec <= 148 * 4                # one resident wave
+    part, _ = ctx.partition(dev(M.edges), M.n, 1024)
+    L2, plan2 = ctx.remap(dev(M.edges), M.n, part, epg.num_parts(M.m, 1024))   # a second replica
+    reps = [(plan, Un, nrm, dtn),
+            (plan2, ctx.permute_rows(dev(U), L2.vertex_perm, epg.PERM_SCATTER),
+             ctx.permute_rows(dev(M.normals), L2.edge_perm, epg.PERM_GATHER),
+             ctx.permute_rows(dev(dt), L2.vertex_perm, epg.PERM_SCATTER))]
+    chain, ref = [], []
+    for pl, u, nr, dd in reps:
+        chain.append([pl, u.clone(), torch.empty_like(u), nr, dd])
+        ref.append(ctx.run(pl, epg.KERNEL_CFD_FLUX, u.clone(), torch.empty_like(u), nr, dd, 3).clone())
+    for _ in range(3):
+        for c in chain:
+            pl, a, b, nr, dd = c
+            ctx.run_edges(pl, epg.KERNEL_CFD_FLUX, a, b, nr, dd)
+            ctx.run_finalise(pl, epg.KERNEL_CFD_FLUX, a, b, nr, dd)
+            c[1], c[2] = b, a
+    torch.cuda.synchronize()
+    for c, r in zip(chain, ref):
+        assert torch.equal(c[1], r)
