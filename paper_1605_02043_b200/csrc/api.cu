@@ -876,10 +876,14 @@ epg_status launch_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t step
     }
     float *bufs[2] = {static_cast<float *>(state->state_in), static_cast<float *>(state->state_out)};
     const int64_t fin_work = pl->S + (pl->n - pl->touched);
+    const int prewait_pf = a.prewait_pf;
     for (int32_t s = 0; s < steps; s++) {
         a.state_in = bufs[s & 1];
         a.state_out = bufs[(s + 1) & 1];
         a.state_end = a.state_in + (int64_t)Fn::ROW * pl->n;
+        // the pre-wait L2 prefetch helps a step whose rows were evicted since they were written;
+        // the later steps of a call read rows the previous step has just written
+        a.prewait_pf = s == 0 ? prewait_pf : 0;
         cudaAccessPolicyWindow win{};
         const bool use_win = hub_window(ctx, pl, a.state_in, 4 * Fn::ROW, &win);
         cudaEvent_t t0 = ctx->prof_begin();
@@ -1017,6 +1021,7 @@ epg_status run_occ(epg_ctx *ctx, epg_plan *pl, epg_state *state, int32_t steps, 
     a.off_recs = up16i(pl->blob3_max);
     const int recs_bytes = occ_recs_bytes<Fn>(pl);
     a.rstride = occ_rstride<Fn>(pl);
+    a.prewait_pf = std::getenv("EPG_PREWAIT_PF") ? std::atoi(std::getenv("EPG_PREWAIT_PF")) : 1;
     // landing area of the staged rows inside the record array (derived in place): owned rows
     // then, for 5-float rows, one 32-byte slot per halo row (<= 32 L + 48 bytes in all)
     a.rows_land = Fn::ROW == 5 ? 16 : up16i(recs_bytes - (4 * Fn::ROW * pl->Lcap + 16) - 16);
@@ -1051,6 +1056,7 @@ epg_status run_edges_range(epg_ctx *ctx, epg_plan *pl, epg_state *state, int64_t
     a.off_recs = up16i(pl->blob3_max);
     const int recs_bytes = occ_recs_bytes<Fn>(pl);
     a.rstride = occ_rstride<Fn>(pl);
+    a.prewait_pf = std::getenv("EPG_PREWAIT_PF") ? std::atoi(std::getenv("EPG_PREWAIT_PF")) : 1;
     // landing area of the staged rows inside the record array (derived in place): owned rows
     // then, for 5-float rows, one 32-byte slot per halo row (<= 32 L + 48 bytes in all)
     a.rows_land = Fn::ROW == 5 ? 16 : up16i(recs_bytes - (4 * Fn::ROW * pl->Lcap + 16) - 16);

@@ -59,6 +59,7 @@ struct OccArgs {
     int sentinel;              // zero Phi record of padded incidence entries (plan Scap)
     int pstride;               // records of the split Phi layout (>= sentinel + 1, multiple of 4)
     int rstride;               // float4s from a derived record's first half to its second (REC = 8)
+    int prewait_pf;            // single-wave grids: L2-prefetch the state rows before the PDL wait
     int64_t ahead;             // > 0 (multi-wave grids): L2-prefetch partition x + ahead's ranges
     int64_t count;             // execution partitions of this launch
     // the partition's endpoint slots, edge payload and dt are bulk-copied into the Phi space
@@ -161,6 +162,18 @@ __global__ void EPG_OCC_BOUNDS(BLOCK) k_edge_occ(OccArgs a) {
         for (int r = 0; r < VPT; r++) {
             const int j = tid + r * BLOCK;
             hid[r] = j < d.nH ? __ldg(gh + j) : 0;
+        }
+    }
+    // single-wave grids start while the previous kernel (the last step's finalise) runs: the
+    // owned rows and the early halo rows are prefetched into L2 now, so the copies after the
+    // wait hit L2 (a prefetch never returns stale data -- L2 is the point of coherence -- and
+    // the copies themselves still wait)
+    if (a.early_pdl && a.prewait_pf) {
+        if (tid == 64) prefetch_region(g_rows, rows_bytes);
+        if (early_halo) {
+#pragma unroll
+            for (int r = 0; r < VPT; r++)
+                if (tid + r * BLOCK < d.nH) ptx::prefetch_l2(a.state_in + (int64_t)ROW * hid[r]);
         }
     }
     ptx::pdl_wait();                               // state_in is final from here on

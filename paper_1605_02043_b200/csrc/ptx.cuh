@@ -59,6 +59,11 @@ __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src_gmem, u
         : "memory");
 }
 
+// prefetch of the global-memory line holding `gmem` into L2
+__device__ __forceinline__ void prefetch_l2(const void *gmem) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(gmem));
+}
+
 // 1-D bulk prefetch of global memory into L2 (address and size 16-byte aligned)
 __device__ __forceinline__ void bulk_prefetch_l2(const void *src_gmem, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src_gmem), "r"(bytes) : "memory");
