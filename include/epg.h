@@ -138,7 +138,9 @@ typedef struct {
 
 /* -- context ------------------------------------------------------------------ */
 /* Create a context on CUDA device `device`, enqueuing on `cuda_stream` (a
- * cudaStream_t; NULL = the legacy default stream). */
+ * cudaStream_t; NULL = the legacy default stream). The library's temporaries come from the
+ * device's default stream-ordered memory pool; its release threshold is raised to
+ * EPG_POOL_KEEP_GB GiB (default 32) so freed scratch stays mapped for the next call. */
 epg_status epg_create(int device, void *cuda_stream, epg_ctx **out);
 void epg_destroy(epg_ctx *ctx);
 /* Message of the last failed call on ctx (ctx-owned, valid until the next call). */

@@ -1587,6 +1587,21 @@ epg_status epg_create(int device, void *cuda_stream, epg_ctx **out) {
         return EPG_ERR_CUDA;
     }
     if (cudaSetDevice(device) != cudaSuccess) return EPG_ERR_CUDA;
+    // the library's temporaries come from the device's default stream-ordered pool; keep up to
+    // EPG_POOL_KEEP_GB (default 32) GiB of freed memory mapped instead of returning it at every
+    // synchronisation, so partition / remap / plan builds reuse their multi-GB scratch instead of
+    // mapping it afresh each time
+    {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            const char *e = std::getenv("EPG_POOL_KEEP_GB");
+            uint64_t keep = (uint64_t)(e ? std::max(0.0, std::atof(e)) : 32.0) << 30;
+            uint64_t cur = 0;
+            if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &cur) == cudaSuccess && cur < keep)
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        cudaGetLastError();
+    }
     epg_ctx *c = new epg_ctx();
     c->device = device;
     c->stream = static_cast<cudaStream_t>(cuda_stream);
