@@ -2,21 +2,24 @@
 // partition, several CTAs resident per SM.
 //
 // Per partition p (the paper's thread block; staging as in P:719-724):
-//   1. one thread issues two 1-D TMA bulk copies on an mbarrier: the partition's plan
-//      blob (halo ids + incidence lists) and its owned state rows O_p, a contiguous range
-//      of the cpack layout; meanwhile every thread prefetches the slots and edge payload
-//      of its edges and the dt of its vertices into registers (coalesced global loads);
-//   2. the halo rows H_p (the C = sum_v (p_v - 1) redundant loads of Eq. (1)) are gathered
-//      with cp.async into the same shared array;
-//   3. each staged row is turned in place into a 32-byte derived record;
-//   4. one thread per edge evaluates the interaction from shared memory into a Phi record;
-//   5. one thread per local vertex sums its incidence list in a fixed order (no atomics);
-//   6. owned results U + dt F and the halo partial sums are packed in shared memory and
+//   0. before the PDL wait (plan data only): the descriptor, one thread's 1-D TMA bulk copies of
+//      the plan blob (halo ids, incidence lists, record placement) and of the partition's slots,
+//      edge payload and dt (into the Phi space, dead until the edge phase), the halo ids of a
+//      halo-light partition and, in single-wave grids, L2 prefetches of its state rows;
+//   1. after the wait: a bulk copy of its owned state rows O_p, a contiguous range of the cpack
+//      layout, and the halo rows H_p (the C = sum_v (p_v - 1) redundant loads of Eq. (1)),
+//      gathered with cp.async into the same shared array;
+//   2. each staged row is turned in place into a derived record (two float4 halves in two
+//      arrays, at the placed position of place_kernels.cuh);
+//   3. one thread per edge evaluates the interaction from shared memory into a Phi record;
+//   4. one thread per local vertex sums its incidence list in a fixed order (no atomics);
+//   5. owned results U + dt F and the halo partial sums are packed in shared memory and
 //      written back with two TMA bulk stores (contiguous: the owned range of state_out,
 //      the partition's slice of the halo buffer).
-// k_finalise3 then adds the halo partials of shared vertices (p_v > 1) to their owners'
-// rows in a fixed order. Latency is hidden by occupancy (3-4 CTAs per SM) rather than by an explicit pipeline;
-// execution partitions are bounded so every buffer fits.
+// The boundary finalise (k_finalise_rec16) then adds the halo partials of shared vertices
+// (p_v > 1) to their owners' rows in a fixed order. Latency is hidden by occupancy (3-4 CTAs per
+// SM) and programmatic dependent launch rather than by an explicit pipeline; execution
+// partitions are bounded so every buffer fits.
 #pragma once
 
 #include <stdint.h>
