@@ -238,3 +238,28 @@ def test_run_edges_one_wave_chain_equals_run():
     torch.cuda.synchronize()
     for c, r in zip(chain, ref):
         assert torch.equal(c[1], r)
+
+
+def test_prewait_prefetch_bitexact():
+    """Single-wave grids L2-prefetch their state rows before the PDL wait (EPG_PREWAIT_PF, on by
+    default): a hint only -- the results with and without it are identical, and equal epg_run's
+    multi-step call whose later steps skip it."""
+    from paper_1605_02043_b200 import epg
+    M = S.config_mesh("c1")
+    ctx, L, plan, U, dt, Un, nrm, dtn = _prep(M, 1024)
+    assert plan.k_exec <= 148 * 4
+    outs = {}
+    for pf in ("0", "1"):
+        old = _env("EPG_PREWAIT_PF", pf)
+        try:
+            a, b = Un.clone(), torch.empty_like(Un)
+            for _ in range(2):                     # two one-step calls (each a first step)
+                ctx.run(plan, epg.KERNEL_CFD_FLUX, a, b, nrm, dtn, 1)
+                a, b = b, a
+            torch.cuda.synchronize()
+            outs[pf] = a.clone()
+        finally:
+            _env("EPG_PREWAIT_PF", old)
+    assert torch.equal(outs["0"], outs["1"])
+    two = ctx.run(plan, epg.KERNEL_CFD_FLUX, Un.clone(), torch.empty_like(Un), nrm, dtn, 2)
+    assert torch.equal(two, outs["1"])
