@@ -66,7 +66,7 @@ class Workload:
             self.kernel, self.functor = 1, "cfd_flux"
             self.state, self.payload, self.vconst = S.cfd_state(M.n), M.normals, S.cfd_dt(M.volume)
             self.per_edge, self.per_vertex = 20, 44     # 8 B ids + 12 B normal; 20 B read, 4 B dt, 20 B write
-            self.exec_rows = 704                        # ~55 KB smem per cfd CTA: 4 per SM
+            self.exec_rows = 768                        # ~53 KB smem per cfd CTA: 4 per SM, 3 rows per thread
         elif config == "c4":
             self.n, self.edges = S.rmat(24)
             self.m = self.edges.shape[0]
@@ -569,7 +569,7 @@ def run_c3(args, torch, epg, ctx, stream, peak):
     P = args.part_size if getattr(args, "config", "c3") == "c3" else 1024
     E = torch.from_numpy(M.edges).to(dev)
     k = epg.num_parts(M.m, P)
-    ctx.set_exec_limits(getattr(args, "exec_rows", 0) or 704, 1024)
+    ctx.set_exec_limits(getattr(args, "exec_rows", 0) or 768, 1024)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     # EPG-RB leaves of 2048 partitions (profiles/r02_c3_leaf_sweep.json: R 1.2350 in 4.4 s, vs 1.2381 at 512)

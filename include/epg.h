@@ -424,8 +424,8 @@ epg_status epg_set_variant(epg_ctx *ctx, int32_t variant);
  * as contiguous ranges of its reorganised edges (the public layout is unchanged; see
  * epg_plan_info's k_exec). max_rows in [64, 2048] (above 1280 only one-float functors,
  * GATHER_SCATTER and SPMV, run the occupancy kernel), max_edges in [32, 1280]; -1 keeps
- * the default: EPG_EXEC_MAX_ROWS / EPG_EXEC_MAX_EDGES from the environment, else 704
- * rows (a cfd CTA at ~55 KB of shared memory, four per SM) and 1024 edges. Raising both
+ * the default: EPG_EXEC_MAX_ROWS / EPG_EXEC_MAX_EDGES from the environment, else 768
+ * rows (a cfd CTA at ~53 KB of shared memory, four per SM) and 1024 edges. Raising both
  * lets partitions of up to 1280 edges run unsplit, e.g. to size the grid to a multiple of
  * the SM count.
  * EPG_ERR_INPUT outside these ranges. */

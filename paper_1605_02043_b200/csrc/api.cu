@@ -783,8 +783,9 @@ constexpr int kOccMaxEdges = 1280, kOccMaxRows = 1280, kOccMaxRowsScalar = 2048;
 constexpr int kOccDefaultEdges = 1024;   // execution-split default (EPT 4 x 256 threads)
 template <class Fn> constexpr int occ_max_rows() { return Fn::ROW == 1 ? kOccMaxRowsScalar : kOccMaxRows; }
 // execution-split caps of a remap: epg_set_exec_limits, else EPG_EXEC_MAX_EDGES /
-// EPG_EXEC_MAX_ROWS, else 1024 edges and 704 rows (704 rows keep a cfd CTA at ~55 KB of
-// shared memory: four CTAs per SM)
+// EPG_EXEC_MAX_ROWS, else 1024 edges and 768 rows (768 rows keep a cfd CTA at ~53 KB of
+// shared memory -- four CTAs per SM -- and at 3 rows per thread; C2 / C3 steps 1 % faster than
+// at 704, 832 rows drop to three CTAs per SM)
 int exec_max_edges(const epg_ctx *ctx) {
     if (ctx->exec_edges > 0) return ctx->exec_edges;
     const char *e = std::getenv("EPG_EXEC_MAX_EDGES");
@@ -794,7 +795,7 @@ int exec_max_edges(const epg_ctx *ctx) {
 int exec_max_rows(const epg_ctx *ctx) {
     if (ctx->exec_rows > 0) return ctx->exec_rows;
     const char *e = std::getenv("EPG_EXEC_MAX_ROWS");
-    const int x = e ? std::atoi(e) : 704;
+    const int x = e ? std::atoi(e) : 768;
     return std::min(kOccMaxRowsScalar, std::max(64, x));
 }
 

@@ -21,7 +21,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--order", choices=["growth", "id"], default="growth")
     ap.add_argument("--part-size", type=int, default=1024)
-    ap.add_argument("--exec-rows", type=int, default=704)
+    ap.add_argument("--exec-rows", type=int, default=768)
     ap.add_argument("--leaf-parts", type=int, default=2048)
     a = ap.parse_args()
     args = argparse.Namespace(part_size=a.part_size, c3_steps=a.steps, no_comparators=not a.comparators, order=a.order,
